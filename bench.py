@@ -1,0 +1,470 @@
+#!/usr/bin/env python
+"""Benchmark: Gpoints/s reconstructed on B200 (BASELINE.json metric) + roofline + CPU baseline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (one rank per GPU, NCCL)
+
+Headline workload (BASELINE.json configs[1]): tricubic tensor-product
+B-spline on a CC 256^3 lattice, 10^8 uniformly random query points per GPU, fp32,
+boundary 'zero'.  A step = one `PlanInterpreter.eval_batch` over the whole batch (one
+kernel launch), inputs resident in HBM.  Input-order protocol (A) of SURVEY.md §8d: the
+iid-uniform points are presented in Morton (Z-curve) order of their unit cell, generated
+once outside the timed region; protocol (B) — the same points shuffled, evaluated
+through the `reorder=True` path that Morton-sorts on the GPU inside the timed region —
+is reported as `unsorted_e2e_device`.  Points (1.2 GB) exceed L2, so no flush is needed.
+
+Other BASELINE configs are measured in the same run under "workloads" (parity for all of
+them is in tests/).  `e2e` is the same metric through the public API with pinned HOST
+buffers: H2D points + kernel + D2H results per step.
+
+`--impl reference` times the reference CPU algorithm (the numpy restatement in
+oracle/plan_numpy.py of runtime.py:363-408, all host cores via fork) on a bounded sample
+of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gpoints/s reconstructed (CC/BCC/FCC, 1/2/4/8 B200) and % of memory roofline"
+UNIT = "Gpoints/s"
+
+# name -> (plan, grid hi (lo=0), dtype, points per GPU)
+WORKLOADS = {
+    "tricubic_cc256_fp32": ("cc_tricubic", 255, "float32", 100_000_000),
+    "tricubic_cc256_fp64": ("cc_tricubic", 255, "float64", 100_000_000),
+    "trilinear_cc64_fp32": ("cc_trilinear", 63, "float32", 1_000_000),
+    "bcc_linear_2x203_fp32": ("bcc_linear_rd", 405, "float32", 100_000_000),
+    "bcc_quintic_2x203_fp32": ("bcc_quintic_rd", 405, "float32", 100_000_000),
+    "fcc6_4x161_fp32": ("fcc_cubic", 321, "float32", 100_000_000),
+    "zp3_cc256_fp32": ("cc_zp3", 255, "float32", 100_000_000),
+}
+HEADLINE = "tricubic_cc256_fp32"
+
+_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+def _plan_name(name: str) -> str:
+    from paper_2102_08514_b200 import corpus
+
+    plans = corpus.available_plans()
+    if name in plans:
+        return name
+    if f"{name}_ungrouped" in plans:
+        return f"{name}_ungrouped"
+    raise KeyError(name)
+
+
+# ---------------------------------------------------------------------------------------
+# clocks sampler (NVML, during the timed region)
+
+
+class ClockSampler:
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.index = index
+        self.period = period_s
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        self.reasons |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=1)
+
+    def summary(self) -> dict:
+        reasons = [name for bit, name in _REASONS.items() if self.reasons & bit]
+        return {
+            "sm_mhz": float(np.median(self.samples)) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": reasons,
+            "samples": len(self.samples),
+        }
+
+
+# ---------------------------------------------------------------------------------------
+# workload setup
+
+
+def make_workload(name, rank, device, order="morton", n_override=None):
+    import torch
+
+    from paper_2102_08514_b200 import corpus
+    from paper_2102_08514_b200.runtime import CoefficientGrid, PlanInterpreter, morton_order
+
+    plan_name, hi, dt, n = WORKLOADS[name]
+    n = n_override or n
+    dtype = getattr(torch, dt)
+    plan = corpus.load_plan(corpus.PLAN_DIR / f"{_plan_name(plan_name)}.plan.json")
+    _, cos = corpus.lattice_of(plan_name)
+    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [hi, hi, hi], device=device, dtype=dtype)
+    gen = torch.Generator(device=device).manual_seed(2102_08514 + 7919 * rank)
+    for a in grid.arrays:  # coefficients uniform in [0,1), generated as fp32
+        a.copy_(torch.rand(a.shape, generator=gen, device=device, dtype=torch.float32).to(dtype))
+    pts = (torch.rand((n, 3), generator=gen, device=device, dtype=torch.float32) * (hi + 1)).to(dtype)
+    if order == "morton":
+        pts = pts[morton_order(pts)].contiguous()
+    interp = PlanInterpreter(plan)
+    return plan, grid, pts, interp
+
+
+def algorithmic_bytes(n, grid, dtype_size):
+    """B/pt = s*sizeof(T_pt) + sizeof(T_out) + lattice/n."""
+    return n * (3 * dtype_size + dtype_size) + grid.nbytes()
+
+
+def measure(fn, steps, warmup, stream, dist=None):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(steps):
+        fn()
+    end.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = start.elapsed_time(end) / steps
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic(name):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        v = d.get(name)
+        if isinstance(v, dict):
+            return v.get("dram_bytes_per_launch")
+        return v
+    return None
+
+
+# ---------------------------------------------------------------------------------------
+# CPU arm: numpy restatement of the reference batch path (oracle/, checker only)
+
+_CPU_STATE = {}
+
+
+def _cpu_chunk(args):
+    lo, hi = args
+    from oracle.plan_numpy import eval_batch
+
+    st = _CPU_STATE
+    return eval_batch(st["plan"], st["grid"], st["pts"][lo:hi], st["tabs"])
+
+
+def cpu_reference_setup(name, seed=0):
+    """Host grid + a point pool for the CPU arm (same distribution as the GPU workload)."""
+    from oracle.plan_numpy import NumpyGrid, PlanTables
+    from paper_2102_08514_b200 import corpus
+    from paper_2102_08514_b200.runtime import grid_extents
+
+    plan_name, hi, _, _ = WORKLOADS[name]
+    plan = corpus.load_plan(corpus.PLAN_DIR / f"{_plan_name(plan_name)}.plan.json")
+    _, cos = corpus.lattice_of(plan_name)
+    origins, shapes = grid_extents(cos, [0, 0, 0], [hi, hi, hi])
+    rng = np.random.default_rng(2102_08514 + seed)
+    arrays = [rng.random(sh, dtype=np.float32).astype(np.float64) for sh in shapes]
+    pts = (rng.random((1 << 20, 3), dtype=np.float32) * np.float32(hi + 1)).astype(np.float64)
+    _CPU_STATE.update(plan=plan, grid=NumpyGrid(plan.diag, plan.shifts, arrays, origins, "zero"), pts=pts,
+                      tabs=PlanTables(plan))
+
+
+def cpu_run(n_points, pool, chunk=2048):
+    spans = [(i, min(i + chunk, n_points)) for i in range(0, n_points, chunk)]
+    t0 = time.perf_counter()
+    if pool is None:
+        for s in spans:
+            _cpu_chunk(s)
+    else:
+        pool.map(_cpu_chunk, spans)
+    return time.perf_counter() - t0
+
+
+def cpu_calibrated_sample(pool, cores, target_s):
+    """Points per sample so that one sample takes ~target_s on `cores` workers."""
+    t = cpu_run(1024, None, chunk=1024)  # one core, includes first-touch costs
+    t = cpu_run(1024, None, chunk=1024)
+    rate = 1024 / max(t, 1e-6)  # pts/s/core
+    n = int(rate * cores * target_s)
+    n = max(2048, min(n, len(_CPU_STATE["pts"])))
+    return (n // 2048) * 2048 or 2048
+
+
+def cpu_baseline(name, budget_s=15.0):
+    cpu_reference_setup(name)
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        n = cpu_calibrated_sample(pool, cores, budget_s)
+        secs = cpu_run(n, pool)
+    return {
+        "value": n / secs / 1e9,
+        "unit": UNIT,
+        "cores": cores,
+        "kind": "port",
+        "sample": f"{n} uniform points of {name} (same grid shape/distribution), numpy restatement of "
+                  f"runtime.py:363-408 (oracle/plan_numpy.py), fp64, {cores} fork workers, {secs:.1f} s",
+        "seconds": secs,
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    name = HEADLINE
+    cpu_reference_setup(name)
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        n = cpu_calibrated_sample(pool, cores, args.ref_step_seconds)
+        for _ in range(args.warmup):
+            cpu_run(n, pool)
+        times = [cpu_run(n, pool) for _ in range(args.steps)]
+    secs = float(np.mean(times))
+    value = n / secs / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": name, "points_per_step": n, "lattice": "CC3 256^3", "spline": "cc_tricubic",
+                   "boundary": "zero"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{n} uniform points per step, numpy restatement of runtime.py:363-408 "
+                                   f"(oracle/plan_numpy.py), {cores} fork workers"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+# GPU arm
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as torch_dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        torch_dist.init_process_group("nccl", device_id=device)
+        dist = torch_dist
+    peak, peak_kind = load_peaks()
+    stream = torch.cuda.current_stream(device)
+
+    from paper_2102_08514_b200 import _native
+
+    # ---- headline -------------------------------------------------------------------
+    name = args.workload
+    plan, grid, pts, interp = make_workload(name, rank, device, n_override=args.points)
+    n = pts.shape[0]
+    out = torch.empty(n, dtype=grid.dtype, device=device)
+    launches_per_step = _native.lib().sp_eval_launch_count(interp._handle(device), n)
+
+    def step():
+        interp.eval_batch(grid, pts, out=out, check=False)
+
+    step()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = measure(step, args.steps, args.warmup, stream, dist)
+    esize = grid.arrays[0].element_size()
+    bytes_launch = algorithmic_bytes(n, grid, esize)
+    achieved = bytes_launch / (ms * 1e-3) / 1e9
+    value = world * n / (ms * 1e-3) / 1e9
+
+    # ---- e2e through the public API with pinned host buffers --------------------------
+    host_pts = pts.to("cpu").pin_memory()
+    host_out = torch.empty(n, dtype=grid.dtype).pin_memory()
+
+    def e2e_step():
+        interp.eval_batch(grid, host_pts, out=host_out, check=False)
+
+    e2e_steps = max(2, min(args.steps, args.e2e_steps))
+    e2e_ms = measure(e2e_step, e2e_steps, 1, stream, dist)
+    e2e = {
+        "value": world * n / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+        "h2d_bytes_per_step": int(host_pts.numel() * host_pts.element_size()),
+        "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
+        "ms_per_step": e2e_ms, "steps": e2e_steps,
+        "path": "PlanInterpreter.eval_batch(grid, pinned CPU tensor, out=pinned CPU tensor)",
+    }
+    del host_pts, host_out
+
+    # ---- protocol (B): shuffled points, GPU Morton sort inside the timed region -------
+    shuffled = pts[torch.randperm(n, device=device)]
+
+    def unsorted_step():
+        interp.eval_batch(grid, shuffled, out=out, check=False, reorder=True)
+
+    ms_b = measure(unsorted_step, max(2, args.steps // 4), 1, stream, dist)
+    del shuffled
+    torch.cuda.empty_cache()
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if esize == 4 else "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": name, "spline": WORKLOADS[name][0], "lattice": "CC3", "grid": [256, 256, 256],
+            "points_per_gpu": n, "boundary": "zero", "input_order": "morton (protocol A, SURVEY.md §8d)",
+            "l2": "inputs larger than L2 (points %.2f GB > 126 MB); lattice %.0f MB L2-resident"
+                  % (n * 3 * esize / 1e9, grid.nbytes() / 1e6),
+            "parallelism": f"points sharded, lattice replicated, dp{world}",
+            "kernel": interp.kernel_name(device),
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": load_traffic(name), "peak_source": peak_kind,
+            "algorithmic_bytes_per_launch": bytes_launch, "bytes_per_point": bytes_launch / n,
+            "kernel_ms": ms,
+        },
+        "e2e": e2e,
+        "unsorted_e2e_device": {"value": world * n / (ms_b * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_b,
+                                "note": "protocol B: shuffled points, Morton sort + gather + eval + scatter timed"},
+        "gpu_launches": int(args.steps * launches_per_step),
+        "clocks": clk.summary(),
+    }
+    del pts, out, grid
+    torch.cuda.empty_cache()
+
+    # ---- other BASELINE configs --------------------------------------------------------
+    if not args.headline_only:
+        others = {}
+        for wname in WORKLOADS:
+            if wname == name:
+                continue
+            try:
+                plan_w, grid_w, pts_w, interp_w = make_workload(wname, rank, device)
+            except KeyError:
+                continue
+            nw = pts_w.shape[0]
+            out_w = torch.empty(nw, dtype=grid_w.dtype, device=device)
+
+            def wstep():
+                interp_w.eval_batch(grid_w, pts_w, out=out_w, check=False)
+
+            wstep()
+            torch.cuda.synchronize()
+            msw = measure(wstep, max(3, args.steps // 2), args.warmup, stream, dist)
+            es = grid_w.arrays[0].element_size()
+            bw = algorithmic_bytes(nw, grid_w, es)
+            others[wname] = {
+                "value": world * nw / (msw * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": msw,
+                "points_per_gpu": nw, "kernel": interp_w.kernel_name(device),
+                "roofline_hbm_frac": bw / (msw * 1e-3) / 1e9 / peak, "bytes_per_point": bw / nw,
+            }
+            del plan_w, grid_w, pts_w, interp_w, out_w
+            torch.cuda.empty_cache()
+        line["workloads"] = others
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(name, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default=HEADLINE, choices=sorted(WORKLOADS))
+    ap.add_argument("--points", type=int, default=None, help="points per GPU (default: the workload's)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--headline-only", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=4.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

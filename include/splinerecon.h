@@ -1,0 +1,151 @@
+/*
+ * splinerecon.h — C ABI of the B200 reconstruction hot path (libsplinerecon.so).
+ *
+ * Drop-in boundary for the reference's batch evaluator
+ *     PlanInterpreter(plan).eval_batch(grid, pts)        runtime.py:219-248
+ * i.e. Algorithm 1 of arXiv 2102.08514 over a compiled
+ * EvaluationPlan (plancompile.py:94-143) and a coset-decomposed CoefficientGrid
+ * (runtime.py:38-105).  The reference is pure Python with no FFI; the binding a
+ * maintainer adds on the reference side is a ctypes stub.
+ *
+ * Conventions: plain pointers and sizes only, no torch types.  All device pointers
+ * are CUDA device memory; calls are stream-ordered and asynchronous unless noted.
+ * Functions return SP_OK (0) or a negative sp_status; sp_last_error() gives a
+ * thread-local message.  No exception crosses the ABI.  Concurrent sp_eval calls on
+ * different streams with the same plan are safe (a plan is immutable after create).
+ */
+#ifndef SPLINERECON_H
+#define SPLINERECON_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_MAX_DIM 3
+#define SP_MAX_COSETS 8
+
+typedef enum sp_status {
+    SP_OK = 0,
+    SP_ERR_INVALID = -1,     /* malformed descriptor / argument            (PlanError)     */
+    SP_ERR_UNSUPPORTED = -2, /* valid but not implemented (e.g. s != 3)    (NotImplemented) */
+    SP_ERR_CUDA = -3,        /* CUDA runtime failure                                         */
+    SP_ERR_SENTINEL = -4,    /* sigma sentinel hit      runtime.py:380-381 (RuntimeError_)   */
+    SP_ERR_MISMATCH = -5     /* grid decomposition != plan header, runtime.py:250-254         */
+} sp_status;
+
+typedef enum sp_dtype { SP_F32 = 0, SP_F64 = 1 } sp_dtype;
+
+/* CoefficientGrid boundary policies, runtime.py:35 and :109-123 / :151-168 / :191-204 */
+typedef enum sp_boundary { SP_ZERO = 0, SP_CLAMP = 1, SP_MIRROR = 2 } sp_boundary;
+
+/* Which kernel family a created plan dispatches to (sp_plan_kernel_kind). */
+typedef enum sp_kernel_kind {
+    SP_KIND_TENSOR_BSPLINE = 0, /* separable closed form, proven equal to the plan      */
+    SP_KIND_GENERATED = 1,      /* plan-specialised kernel compiled into this library   */
+    SP_KIND_GENERIC = 2         /* table-driven kernel for any other plan (still GPU)   */
+} sp_kernel_kind;
+
+/*
+ * Flattened EvaluationPlan (plancompile.py:94-143; ClassTransform analysis.py:89-100;
+ * FetchGroup plancompile.py:55-77).  Replaces the Python object the reference passes to
+ * PlanInterpreter(plan) (runtime.py:219).  All arrays are host memory, row-major, and
+ * are copied by sp_plan_create.
+ */
+typedef struct sp_plan_desc {
+    int32_t s;                              /* dimension; kernels implement s == 3          */
+    int32_t M;                              /* cosets                                         */
+    int32_t diag[SP_MAX_DIM];               /* D = diag(d_i)              lattice.py:104-133 */
+    int32_t shifts[SP_MAX_COSETS][SP_MAX_DIM]; /* l_k                                          */
+    int32_t Q;                              /* plane count                                     */
+    const int32_t* normals;                 /* [Q*s] integer normals                           */
+    const double* offsets;                  /* [Q]  float(offset), as runtime.py:263           */
+    int32_t r;                              /* sigma modulus                                   */
+    const int32_t* sigma;                   /* [r]  class id or -1 sentinel                    */
+    int32_t N;                              /* classes                                         */
+    const int32_t* cls_kernel;              /* [N]                                             */
+    const double* cls_T;                    /* [N*s*s] float(T)                                */
+    const double* cls_t;                    /* [N*s]   float(t)                                */
+    const int32_t* cls_piA;                 /* [N*s*s]                                         */
+    const int32_t* cls_pib;                 /* [N*s]                                           */
+    int32_t K;                              /* kernels                                         */
+    const int32_t* kernel_group_start;      /* [K+1] into groups                               */
+    int32_t n_groups;
+    const int32_t* group_span;              /* [n_groups*SP_MAX_DIM] span axes, -1 padded     */
+    const int32_t* group_nspan;             /* [n_groups] len(span_axes); size = 1 << nspan   */
+    const int32_t* group_site_start;        /* [n_groups+1] into sites                         */
+    const int32_t* sites;                   /* [n_sites*s] zero-coset lattice vectors          */
+    const int32_t* group_poly_start;        /* [n_groups+1] into polys: g, then t_nums[j]      */
+    int32_t n_polys;
+    const int32_t* poly_term_start;         /* [n_polys+1] into terms                          */
+    const int32_t* term_exps;               /* [n_terms*s]                                     */
+    const double* term_coeffs;              /* [n_terms]  float(coefficient)                   */
+    int32_t texel_offset_half;              /* PlanOptions.texel_offset_half                   */
+    int32_t tp_degree;                      /* >= 0: caller asserts a tensor-product B-spline  */
+                                            /* plan of this degree; verified in create.        */
+                                            /* -1: automatic; -2: force the generic kernel.     */
+} sp_plan_desc;
+
+/* One coset-decomposed grid: per-coset contiguous C-order device arrays (axis s-1
+ * fastest), site D z + l_k at arrays[k][z - origin[k]] (runtime.py:38-43). */
+typedef struct sp_grid_desc {
+    int32_t s;
+    int32_t M;
+    int32_t dtype;                              /* sp_dtype of the arrays                   */
+    int32_t boundary;                           /* sp_boundary                               */
+    int32_t diag[SP_MAX_DIM];
+    int32_t shifts[SP_MAX_COSETS][SP_MAX_DIM];
+    const void* data[SP_MAX_COSETS];            /* device pointers                           */
+    int64_t extent[SP_MAX_COSETS][SP_MAX_DIM];
+    int64_t origin[SP_MAX_COSETS][SP_MAX_DIM];
+} sp_grid_desc;
+
+typedef struct sp_plan sp_plan; /* opaque; owns device copies of the packed tables */
+
+/* Validate + specialise a plan.  Replaces PlanInterpreter.__init__ / _batch_tables
+ * (runtime.py:219-230, :256-272).  Requires a CUDA device. */
+int sp_plan_create(const sp_plan_desc* desc, sp_plan** out);
+void sp_plan_destroy(sp_plan* plan);
+int sp_plan_kernel_kind(const sp_plan* plan); /* sp_kernel_kind */
+/* Name of the specialised kernel (e.g. "tensor_bspline_3", "gen:bcc_linear_rd", "generic"). */
+const char* sp_plan_kernel_name(const sp_plan* plan);
+
+/*
+ * Batch reconstruction: out[i] = sum_k sum_{m in C_k(x_i)} c_m phi(x_i - m)   (Eq. 7).
+ * Replaces PlanInterpreter.eval_batch (runtime.py:244-248) -> _eval_batch (:363-408).
+ *   pts  device [n*s] of `dtype`; out device [n] of `dtype`; grid arrays must be `dtype`.
+ *   dbg  nullable device int32 [n*M*4]: per point and coset (class id, cell_0..2), the
+ *        classification of runtime.py:371-379 (cell = kk/d).
+ *   err_flag nullable device int32, OR-ed with 1 when a sigma sentinel is hit.
+ *   stream  cudaStream_t (0 = legacy default stream).
+ * Asynchronous; returns before the kernel finishes.  n == 0 is a no-op.
+ */
+int sp_eval(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+            void* out, int32_t* dbg, int32_t* err_flag, void* stream);
+
+/* Synchronous convenience: sp_eval + stream sync + sentinel check (SP_ERR_SENTINEL). */
+int sp_eval_sync(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+                 void* out, void* stream);
+
+/* Number of kernel launches sp_eval issues for n points (for launch accounting). */
+int sp_eval_launch_count(const sp_plan* plan, int64_t n);
+
+/* Morton (Z-order) keys of the points' unit cells floor(x): used to present query points
+ * in the coherent order the staged kernels exploit (input-order protocol).
+ * keys device uint64 [n]. */
+int sp_morton_keys(const void* pts, int64_t n, int32_t dtype, uint64_t* keys, void* stream);
+
+/* out[perm[i]] = src[i]  (float or double, by dtype) — unpermute results of a sorted batch. */
+int sp_scatter(const void* src, const int64_t* perm, int64_t n, int32_t dtype, void* out, void* stream);
+/* dst[i] = pts[perm[i]] (s=3 points) — gather points into sorted order. */
+int sp_gather_points(const void* pts, const int64_t* perm, int64_t n, int32_t dtype, void* dst, void* stream);
+
+const char* sp_last_error(void);
+const char* sp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPLINERECON_H */

@@ -1,0 +1,307 @@
+"""Build-time code generator: EvaluationPlan -> plan-specialised sm_100a evaluator.
+
+The paper lowers each plan to LLVM/PTX (Part II; not shipped); the
+reference lowers it to the mini-language of `build_program` (plancompile.py:564-699),
+whose op list fixes the per-point semantics.  This generator emits the same
+semantics as straight-line CUDA for one plan:
+
+* coset loop (M unrolled), the float64 coset frame of runtime.py:371-373,
+* the Q plane tests with the plan's integer normals as +/- adds, packed into a code
+  (plancompile.py:593-603), `q mod r`, sigma lookup (shared memory),
+* the class transform decoded from a packed record: T and piA as signed permutations
+  (probe12), y = T xp - t,
+* per kernel, per fetch group: greedy-Horner weight programs (FMA), and the fetch
+  merge done in software with a LOCAL lerp on exact integer cell indices
+   — for 2-site groups the division-free form
+  g*c0 + t_num*(c1 - c0), for 4/8-site groups t_j = t_num_j / g (0.5 when g == 0,
+  plancompile.py:684-688) and a multilinear lerp,
+* K > 1 plans branch on the class's kernel id (the reference predicates, :633-637).
+
+Each plan becomes one translation unit `generated/plan_<ident>.cu` exporting a
+`GenEntry` whose `blob` is the plan's canonical word sequence; sp_plan_create matches
+an incoming plan against it exactly.
+"""
+
+from __future__ import annotations
+
+import os
+import re
+from fractions import Fraction
+from typing import List
+
+from .exact import HNode, horner_tree
+from .packing import canonical_words, pack_plan
+from .plan import EvaluationPlan
+
+
+def codegen_supported(plan: EvaluationPlan) -> bool:
+    if plan.s != 3 or plan.M > 8 or plan.Q > 31 or plan.K > 15:
+        return False
+    if len(set(plan.diag)) != 1:
+        return False
+    if plan.tensor_bspline_degree() is not None:
+        return False
+    recs = plan.signed_permutation_classes()
+    if recs is None:
+        return False
+    for r in recs:
+        if any(not -128 <= v < 128 for v in r["t"]):
+            return False
+        if any(v % plan.diag[0] for v in r["pib"]):
+            return False
+    for kern in plan.kernels:
+        for g in kern.groups:
+            for site in g.sites:
+                if any(v % plan.diag[0] for v in site):
+                    return False
+    return True
+
+
+def ident_of(name: str) -> str:
+    return re.sub(r"[^A-Za-z0-9_]", "_", name)
+
+
+def _lit(q: Fraction) -> str:
+    v = float(q)
+    return f"T({v!r})"
+
+
+class _Emitter:
+    def __init__(self, prefix: str):
+        self.lines: List[str] = []
+        self.n = 0
+        self.prefix = prefix
+        self.ops = 0
+
+    def tmp(self) -> str:
+        self.n += 1
+        return f"{self.prefix}{self.n}"
+
+    def expr(self, node: HNode) -> str:
+        k = node.kind
+        if k == "const":
+            return _lit(node.args[0])
+        if k == "var":
+            return f"y{node.args[0]}"
+        args = [self.expr(a) for a in node.args]
+        name = self.tmp()
+        self.ops += 1
+        if k == "add":
+            self.lines.append(f"const T {name} = {args[0]} + {args[1]};")
+        elif k == "mul":
+            self.lines.append(f"const T {name} = {args[0]} * {args[1]};")
+        else:  # fma: a*b + c
+            self.lines.append(f"const T {name} = fma({args[0]}, {args[1]}, {args[2]});")
+        return name
+
+
+def _kernel_function(plan: EvaluationPlan, kidx: int, d: int) -> tuple:
+    kern = plan.kernels[kidx]
+    out = [
+        "template <typename T, class F>",
+        f"__device__ __forceinline__ T kernel{kidx}(const T y0, const T y1, const T y2, const F& f) {{",
+        "    T acc = T(0);",
+    ]
+    flops = 0
+    for gi, g in enumerate(kern.groups):
+        em = _Emitter(f"h{gi}_")
+        gname = em.expr(horner_tree(g.g))
+        tnames = [em.expr(horner_tree(t)) for t in g.t_nums]
+        flops += em.ops
+        body = ["    {"] + [f"        {ln}" for ln in em.lines]
+        sd = [tuple(v // d for v in site) for site in g.sites]
+        ns = len(g.span_axes)
+        if ns == 0:
+            body.append(f"        acc = fma({gname}, f.get({sd[0][0]}, {sd[0][1]}, {sd[0][2]}), acc);")
+            flops += 1
+        elif ns == 1:
+            body.append(f"        const T c0 = f.get({sd[0][0]}, {sd[0][1]}, {sd[0][2]});")
+            body.append(f"        const T c1 = f.get({sd[1][0]}, {sd[1][1]}, {sd[1][2]});")
+            body.append(f"        acc = fma({gname}, c0, acc);")
+            body.append(f"        acc = fma({tnames[0]}, c1 - c0, acc);")
+            flops += 3
+        else:
+            body.append(f"        const T gz = {gname};")
+            body.append("        const T rg = gz == T(0) ? T(0) : T(1) / gz;")
+            for j in range(ns):
+                body.append(f"        const T t{j} = gz == T(0) ? T(0.5) : {tnames[j]} * rg;")
+            for c in range(1 << ns):
+                body.append(f"        T v{c} = f.get({sd[c][0]}, {sd[c][1]}, {sd[c][2]});")
+            for j in range(ns):
+                step = 1 << j
+                for c in range(0, 1 << ns, 2 * step):
+                    body.append(f"        v{c} = fma(t{j}, v{c + step} - v{c}, v{c});")
+                    flops += 2
+            body.append("        acc = fma(gz, v0, acc);")
+            flops += 1 + ns
+        body.append("    }")
+        out.extend(body)
+    out.append("    return acc;")
+    out.append("}")
+    return out, flops
+
+
+def _plane_expr(normal) -> str:
+    terms = []
+    for i, n in enumerate(normal):
+        if n == 0:
+            continue
+        if n == 1:
+            terms.append(f"xp{i}")
+        elif n == -1:
+            terms.append(f"(-xp{i})")
+        else:
+            terms.append(f"({float(n)!r} * xp{i})")
+    if not terms:
+        return "0.0"
+    expr = terms[0]
+    for t in terms[1:]:
+        expr = f"({expr} + {t})"
+    return expr
+
+
+def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple:
+    """(translation-unit source, stats) for one plan; `stem` names the catalog entry."""
+    if not codegen_supported(plan):
+        raise ValueError(f"plan {plan.name} is not supported by the code generator")
+    stem = stem or plan.name
+    ident = ident_of(stem)
+    d = plan.diag[0]
+    words = canonical_words(pack_plan(plan))
+    kfuncs = []
+    kflops = []
+    for kidx in range(plan.K):
+        lines, fl = _kernel_function(plan, kidx, d)
+        kfuncs.extend(lines)
+        kfuncs.append("")
+        kflops.append(fl)
+    sig_bytes = ((plan.r * 4) + 15) & ~15
+    planes = []
+    for j, (n, off) in enumerate(plan.planes):
+        planes.append(f"            q |= ({_plane_expr(n)} >= {float(off)!r}) ? {1 << j} : 0;")
+    if plan.K == 1:
+        dispatch = "            const T acc = kernel0<T>(y0, y1, y2, f);"
+    else:
+        cases = "\n".join(
+            f"                case {k}: acc = kernel{k}<T>(y0, y1, y2, f); break;" for k in range(plan.K)
+        )
+        dispatch = f"            T acc = T(0);\n            switch (kern) {{\n{cases}\n            }}"
+    src = f"""// GENERATED by paper_2102_08514_b200/codegen.py from plans/{stem}.plan.json — do not edit.
+// Plan: {plan.name} on {plan.lattice_name}: s=3 M={plan.M} N={plan.N} Q={plan.Q} r={plan.r} K={plan.K}
+// Weight-program flops per coset per kernel (Horner + merge): {kflops}
+#include "../sp_launch.cuh"
+
+namespace sp {{
+namespace gen_{ident} {{
+
+constexpr int kM = {plan.M};
+constexpr int kR = {plan.r};
+constexpr int kSigmaBytes = {sig_bytes};
+
+{chr(10).join(kfuncs)}
+template <typename T>
+struct Eval {{
+    template <class F, class Ctx>
+    __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
+        const EvalArgs<T>& a = *ctx.a;
+        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
+        T total = T(0);
+#pragma unroll
+        for (int k = 0; k < kM; ++k) {{
+            const CosetFrame cf = coset_frame(x, a.fr, k);
+            const double xp0 = cf.xp[0], xp1 = cf.xp[1], xp2 = cf.xp[2];
+            int q = 0;
+{chr(10).join(planes)}
+            int c = sigma[q % kR];
+            if (c < 0) {{
+                if (a.err) atomicOr(a.err, 1);
+                c = 0;
+            }}
+            write_dbg(a.dbg, ctx.index, kM, k, c, cf.cell);
+            const uint4 rec = cls_tab[c];
+            const int kern = (int)(rec.x & 15u);
+            (void)kern;
+            int rho[3], tau[3], base[3];
+            double yv[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {{
+                const int perm = (int)((rec.x >> (4 + 2 * i)) & 3u);
+                const double sg = ((rec.x >> (10 + i)) & 1u) ? -1.0 : 1.0;
+                rho[i] = (int)((rec.x >> (13 + 2 * i)) & 3u);
+                tau[i] = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
+                const int ti = (int)((rec.y >> (8 * i)) & 255u) - 128;
+                const int pb = (int)((rec.z >> (8 * i)) & 255u) - 128;
+                yv[i] = sg * sel3(perm, xp0, xp1, xp2) - (double)ti;
+                base[i] = cf.cell[i] + pb;
+            }}
+            const T y0 = (T)yv[0], y1 = (T)yv[1], y2 = (T)yv[2];
+            bind(f, a, *ctx.geom, k, base, rho, tau);
+{dispatch}
+            total += acc;
+        }}
+        return total;
+    }}
+}};
+
+static const uint64_t kBlob[{len(words)}] = {{
+{_format_words(words)}
+}};
+
+}}  // namespace gen_{ident}
+}}  // namespace sp
+
+extern const sp::GenEntry kGen_{ident} = {{
+    "{stem}",
+    sp::gen_{ident}::kBlob,
+    {len(words)},
+    &sp::launch_eval<float, sp::gen_{ident}::Eval<float>>,
+    &sp::launch_eval<double, sp::gen_{ident}::Eval<double>>,
+    &sp::occupancy_blocks<float, sp::gen_{ident}::Eval<float>>,
+    &sp::occupancy_blocks<double, sp::gen_{ident}::Eval<double>>,
+}};
+"""
+    return src, {"ident": ident, "flops_per_coset": kflops, "words": len(words)}
+
+
+def _format_words(words: list) -> str:
+    lines = []
+    for i in range(0, len(words), 4):
+        lines.append("    " + ", ".join(f"0x{w:016x}ull" for w in words[i : i + 4]) + ",")
+    return "\n".join(lines)
+
+
+def generate_registry(idents: list) -> str:
+    decls = "\n".join(f"extern const sp::GenEntry kGen_{i};" for i in idents)
+    entries = ", ".join(f"&kGen_{i}" for i in idents) or "nullptr"
+    return f"""// GENERATED by paper_2102_08514_b200/codegen.py — registry of plan-specialised kernels.
+{decls}
+static const sp::GenEntry* const kGenerated[] = {{{entries}}};
+"""
+
+
+def write_generated(plans: list, out_dir: str) -> list:
+    """Write one TU per supported (stem, plan) + registry.inc; returns the TU paths."""
+    os.makedirs(out_dir, exist_ok=True)
+    idents, paths = [], []
+    for stem, plan in plans:
+        if not codegen_supported(plan):
+            continue
+        src, stats = generate_plan_source(plan, stem)
+        path = os.path.join(out_dir, f"plan_{stats['ident']}.cu")
+        _write_if_changed(path, src)
+        idents.append(stats["ident"])
+        paths.append(path)
+    _write_if_changed(os.path.join(out_dir, "registry.inc"), generate_registry(idents))
+    # drop stale TUs of plans no longer in the catalog
+    for f in os.listdir(out_dir):
+        if f.startswith("plan_") and f.endswith(".cu") and os.path.join(out_dir, f) not in paths:
+            os.remove(os.path.join(out_dir, f))
+    return paths
+
+
+def _write_if_changed(path: str, text: str) -> None:
+    if os.path.exists(path) and open(path).read() == text:
+        return
+    with open(path, "w") as fh:
+        fh.write(text)

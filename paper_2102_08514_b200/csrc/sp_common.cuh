@@ -1,0 +1,381 @@
+// sp_common.cuh — shared device machinery of the reconstruction kernels (sm_100a).
+//
+// The reference evaluates Algorithm 1 as numpy passes over the whole
+// batch (runtime.py:363-408) with fancy-index gathers into per-coset float64 arrays
+// (runtime.py:151-188).  Here one CTA owns a chunk of kChunk consecutive query points:
+//
+//   1. it loads the chunk, reduces the bounding box of the points' unit cells,
+//   2. if the box (+ the plan's site reach, per coset) fits the shared-memory budget it
+//      stages those coefficients ONCE into shared memory, applying the grid's boundary
+//      policy while staging (zero / clamp / mirror, runtime.py:109-123, :151-168, :191-204),
+//      so the per-point gathers are unchecked shared-memory reads,
+//   3. otherwise (incoherent point order) every read goes to global memory (L2) through
+//      the same policy function.
+//
+// Points presented in Morton order (sp_morton_keys) make step 2 the common case; any order
+// is correct.  The per-point evaluators (TP B-spline, generated plan kernels, generic plan
+// interpreter) only see the Fetch interface below.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/splinerecon.h"
+
+namespace sp {
+
+constexpr int kThreads = 256;
+constexpr int kPPT = 4;                       // points per thread per chunk
+constexpr int kChunk = kThreads * kPPT;       // points per chunk
+constexpr int kCellClamp = 1 << 30;           // |cell| clamp (mirror exact below this)
+
+template <typename T>
+struct GridArgs {
+    const T* data[SP_MAX_COSETS];
+    int ext[SP_MAX_COSETS][3];
+    int org[SP_MAX_COSETS][3];
+    int M;
+    int boundary;
+};
+
+struct FrameArgs {
+    int M;
+    int diag[3];
+    int shift[SP_MAX_COSETS][3];
+    int reach_lo[3];  // site reach in coset cells, relative to floor((x - l_k)/d)
+    int reach_hi[3];
+};
+
+template <typename T>
+struct EvalArgs {
+    GridArgs<T> grid;
+    FrameArgs fr;
+    const T* pts;
+    T* out;
+    long long n;
+    int* dbg;           // nullable [n*M*4]
+    int* err;           // nullable
+    const void* tables; // evaluator tables (device), copied to smem when table_bytes > 0
+    int table_bytes;
+    int tile_cap;       // staged-tile capacity in elements
+};
+
+struct TileGeom {
+    int staged;
+    int total;
+    int off[SP_MAX_COSETS];
+    int lo[SP_MAX_COSETS][3];  // box origin in coset-cell coordinates
+    int ex[SP_MAX_COSETS][3];  // box extents
+};
+
+__device__ __forceinline__ int floordiv_i(int a, int d) {
+    int q = a / d;
+    return (a % d != 0 && ((a < 0) != (d < 0))) ? q - 1 : q;
+}
+
+template <typename T>
+__device__ __forceinline__ int clamp_cell(T v) {
+    // floor(v) as int, clamped; NaN -> 0 (such points produce NaN outputs anyway)
+    T f = floor(v);
+    if (!(f == f)) return 0;
+    if (f > T(kCellClamp)) return kCellClamp;
+    if (f < T(-kCellClamp)) return -kCellClamp;
+    return (int)f;
+}
+
+__device__ __forceinline__ int mirror_index(int v, int n) {
+    // runtime.py:191-196 (period 2n-2)
+    if (n == 1) return 0;
+    int p = 2 * n - 2;
+    v = abs(v) % p;
+    return v >= n ? p - v : v;
+}
+
+// Policy read of array index (z0,z1,z2) of coset k (index = cell - origin).
+template <typename T>
+__device__ __forceinline__ T policy_read(const GridArgs<T>& g, int k, int z0, int z1, int z2) {
+    const int e0 = g.ext[k][0], e1 = g.ext[k][1], e2 = g.ext[k][2];
+    const bool in = (unsigned)z0 < (unsigned)e0 && (unsigned)z1 < (unsigned)e1 && (unsigned)z2 < (unsigned)e2;
+    if (!in) {
+        if (g.boundary == SP_ZERO) return T(0);
+        if (g.boundary == SP_CLAMP) {
+            z0 = min(max(z0, 0), e0 - 1);
+            z1 = min(max(z1, 0), e1 - 1);
+            z2 = min(max(z2, 0), e2 - 1);
+        } else {
+            z0 = mirror_index(z0, e0);
+            z1 = mirror_index(z1, e1);
+            z2 = mirror_index(z2, e2);
+        }
+    }
+    return __ldg(g.data[k] + ((long long)z0 * e1 + z1) * (long long)e2 + z2);
+}
+
+// ---------------------------------------------------------------------------------------
+// Fetchers.  A "frame" fixes the coset, the base cell and the class's site renaming
+// (piA = signed permutation rho/tau, probe12 of SURVEY.md §9): the site with zero-coset
+// offsets (s0,s1,s2)/d reads coset cell  base_i + tau_i * s[rho_i].  Generated kernels call
+// get() with compile-time offsets, so the address arithmetic folds to IMADs.
+
+template <typename T>
+struct TileFetch {
+    const T* tile;
+    int a0;
+    int c0, c1, c2;
+
+    __device__ __forceinline__ void frame(const TileGeom& tg, int k, const int base[3], const int rho[3],
+                                          const int tau[3]) {
+        const int ex1 = tg.ex[k][1], ex2 = tg.ex[k][2];
+        const int st[3] = {ex1 * ex2, ex2, 1};
+        a0 = tg.off[k] + (base[0] - tg.lo[k][0]) * st[0] + (base[1] - tg.lo[k][1]) * st[1] + (base[2] - tg.lo[k][2]);
+        int c[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) c[i] = 0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const int v = tau[i] * st[i];
+            c[0] = rho[i] == 0 ? v : c[0];
+            c[1] = rho[i] == 1 ? v : c[1];
+            c[2] = rho[i] == 2 ? v : c[2];
+        }
+        c0 = c[0];
+        c1 = c[1];
+        c2 = c[2];
+    }
+    __device__ __forceinline__ void frame_identity(const TileGeom& tg, int k, const int base[3]) {
+        const int ex1 = tg.ex[k][1], ex2 = tg.ex[k][2];
+        c0 = ex1 * ex2;
+        c1 = ex2;
+        c2 = 1;
+        a0 = tg.off[k] + (base[0] - tg.lo[k][0]) * c0 + (base[1] - tg.lo[k][1]) * c1 + (base[2] - tg.lo[k][2]);
+    }
+    __device__ __forceinline__ T get(int s0, int s1, int s2) const { return tile[a0 + s0 * c0 + s1 * c1 + s2 * c2]; }
+};
+
+template <typename T>
+struct GlobalFetch {
+    const GridArgs<T>* g;
+    int k;
+    int b0, b1, b2;       // base array index (cell - origin)
+    int p[3][3];          // p[j][i] = tau_i if rho_i == j
+
+    __device__ __forceinline__ void frame(const GridArgs<T>& grid, int kk, const int base[3], const int rho[3],
+                                          const int tau[3]) {
+        g = &grid;
+        k = kk;
+        b0 = base[0] - grid.org[kk][0];
+        b1 = base[1] - grid.org[kk][1];
+        b2 = base[2] - grid.org[kk][2];
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) p[j][i] = rho[i] == j ? tau[i] : 0;
+    }
+    __device__ __forceinline__ void frame_identity(const GridArgs<T>& grid, int kk, const int base[3]) {
+        const int rho[3] = {0, 1, 2}, tau[3] = {1, 1, 1};
+        frame(grid, kk, base, rho, tau);
+    }
+    __device__ __forceinline__ T get(int s0, int s1, int s2) const {
+        const int z0 = b0 + s0 * p[0][0] + s1 * p[1][0] + s2 * p[2][0];
+        const int z1 = b1 + s0 * p[0][1] + s1 * p[1][1] + s2 * p[2][1];
+        const int z2 = b2 + s0 * p[0][2] + s1 * p[1][2] + s2 * p[2][2];
+        return policy_read(*g, k, z0, z1, z2);
+    }
+};
+
+// ---------------------------------------------------------------------------------------
+// The chunk driver.  Ev provides:
+//   static constexpr bool kNeedsTables;
+//   template <class F, class Ctx> static T eval(const T x[3], F& fetch, const Ctx& ctx)
+// where Ctx gives the evaluator access to its smem tables, the tile geometry and args.
+
+template <typename T, class Ev>
+struct EvalCtx {
+    const EvalArgs<T>* a;
+    const unsigned char* tables;  // smem copy (or global when not staged)
+    const TileGeom* geom;
+    long long index;              // point index (for debug output)
+};
+
+template <typename T>
+__device__ __forceinline__ void load_point(const T* __restrict__ pts, long long i, T x[3]) {
+    const T* p = pts + 3 * i;
+    x[0] = __ldg(p + 0);
+    x[1] = __ldg(p + 1);
+    x[2] = __ldg(p + 2);
+}
+
+template <typename T, class Ev>
+__global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ TileGeom geom;
+    __shared__ int red[6];
+
+    const int tid = threadIdx.x;
+    // evaluator tables -> smem (16-byte granules)
+    const int tb = (a.table_bytes + 15) & ~15;
+    if (a.table_bytes > 0) {
+        const int4* src = reinterpret_cast<const int4*>(a.tables);
+        int4* dst = reinterpret_cast<int4*>(smem);
+        for (int i = tid; i < tb / 16; i += kThreads) dst[i] = src[i];
+    }
+    T* tile = reinterpret_cast<T*>(smem + tb);
+
+    const long long n = a.n;
+    const long long nchunks = (n + kChunk - 1) / kChunk;
+    const int M = a.fr.M;
+
+    for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+        if (tid < 3) red[tid] = INT_MAX;
+        else if (tid < 6) red[tid] = INT_MIN;
+        __syncthreads();
+
+        int lo0 = INT_MAX, lo1 = INT_MAX, lo2 = INT_MAX, hi0 = INT_MIN, hi1 = INT_MIN, hi2 = INT_MIN;
+        const long long base_i = chunk * kChunk + tid;
+#pragma unroll
+        for (int j = 0; j < kPPT; ++j) {
+            const long long i = base_i + (long long)j * kThreads;
+            if (i < n) {
+                T x[3];
+                load_point(a.pts, i, x);
+                if (isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2])) {
+                    const int f0 = clamp_cell(x[0]), f1 = clamp_cell(x[1]), f2 = clamp_cell(x[2]);
+                    lo0 = min(lo0, f0); hi0 = max(hi0, f0);
+                    lo1 = min(lo1, f1); hi1 = max(hi1, f1);
+                    lo2 = min(lo2, f2); hi2 = max(hi2, f2);
+                }
+            }
+        }
+        lo0 = __reduce_min_sync(0xffffffffu, lo0);
+        lo1 = __reduce_min_sync(0xffffffffu, lo1);
+        lo2 = __reduce_min_sync(0xffffffffu, lo2);
+        hi0 = __reduce_max_sync(0xffffffffu, hi0);
+        hi1 = __reduce_max_sync(0xffffffffu, hi1);
+        hi2 = __reduce_max_sync(0xffffffffu, hi2);
+        if ((tid & 31) == 0) {
+            atomicMin(&red[0], lo0); atomicMin(&red[1], lo1); atomicMin(&red[2], lo2);
+            atomicMax(&red[3], hi0); atomicMax(&red[4], hi1); atomicMax(&red[5], hi2);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            bool ok = red[0] <= red[3] && a.tile_cap > 0;
+            long long total = 0;
+            for (int k = 0; k < M && ok; ++k) {
+                long long vol = 1;
+                for (int i = 0; i < 3; ++i) {
+                    const int d = a.fr.diag[i], l = a.fr.shift[k][i];
+                    // conservative by one cell each side (fp64 x - l rounding)
+                    const long long b0 = (long long)floordiv_i(red[i] - l, d) + a.fr.reach_lo[i] - 1;
+                    const long long b1 = (long long)floordiv_i(red[3 + i] - l, d) + a.fr.reach_hi[i] + 1;
+                    const long long e = b1 - b0 + 1;
+                    vol *= e;
+                    if (vol > a.tile_cap) { ok = false; break; }
+                    geom.lo[k][i] = (int)b0;
+                    geom.ex[k][i] = (int)e;
+                }
+                geom.off[k] = (int)total;
+                total += vol;
+                if (total > a.tile_cap) ok = false;
+            }
+            geom.staged = ok ? 1 : 0;
+            geom.total = ok ? (int)total : 0;
+        }
+        __syncthreads();
+        const bool staged = geom.staged != 0;
+        if (staged) {
+            // fill: one coset at a time, consecutive threads walk the fastest axis (coalesced)
+            for (int k = 0; k < M; ++k) {
+                const int e0 = geom.ex[k][0], e1 = geom.ex[k][1], e2 = geom.ex[k][2];
+                const int vol = e0 * e1 * e2;
+                const int off = geom.off[k];
+                const int z0b = geom.lo[k][0] - a.grid.org[k][0];
+                const int z1b = geom.lo[k][1] - a.grid.org[k][1];
+                const int z2b = geom.lo[k][2] - a.grid.org[k][2];
+                for (int e = tid; e < vol; e += kThreads) {
+                    const int i2 = e % e2;
+                    const int r = e / e2;
+                    const int i1 = r % e1;
+                    const int i0 = r / e1;
+                    tile[off + e] = policy_read(a.grid, k, z0b + i0, z1b + i1, z2b + i2);
+                }
+            }
+        }
+        __syncthreads();
+
+        EvalCtx<T, Ev> ctx;
+        ctx.a = &a;
+        ctx.tables = smem;
+        ctx.geom = &geom;
+#pragma unroll 1
+        for (int j = 0; j < kPPT; ++j) {
+            const long long i = base_i + (long long)j * kThreads;
+            if (i < n) {
+                ctx.index = i;
+                T x[3];
+                load_point(a.pts, i, x);  // L1 hit: loaded by this CTA above
+                T v;
+                if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) {
+                    v = T(NAN);
+                } else if (staged) {
+                    TileFetch<T> f;
+                    f.tile = tile;
+                    v = Ev::template eval<TileFetch<T>>(x, f, ctx);
+                } else {
+                    GlobalFetch<T> f;
+                    v = Ev::template eval<GlobalFetch<T>>(x, f, ctx);
+                }
+                a.out[i] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Frame setup helpers used by the evaluators: bind a fetcher to (coset k, base, rho, tau).
+template <typename T>
+__device__ __forceinline__ void bind(TileFetch<T>& f, const EvalArgs<T>& a, const TileGeom& g, int k,
+                                     const int base[3], const int rho[3], const int tau[3]) {
+    f.frame(g, k, base, rho, tau);
+}
+template <typename T>
+__device__ __forceinline__ void bind(GlobalFetch<T>& f, const EvalArgs<T>& a, const TileGeom& g, int k,
+                                     const int base[3], const int rho[3], const int tau[3]) {
+    f.frame(a.grid, k, base, rho, tau);
+}
+template <typename T>
+__device__ __forceinline__ void bind_identity(TileFetch<T>& f, const EvalArgs<T>& a, const TileGeom& g, int k,
+                                              const int base[3]) {
+    f.frame_identity(g, k, base);
+}
+template <typename T>
+__device__ __forceinline__ void bind_identity(GlobalFetch<T>& f, const EvalArgs<T>& a, const TileGeom& g, int k,
+                                              const int base[3]) {
+    f.frame_identity(a.grid, k, base);
+}
+
+// ---------------------------------------------------------------------------------------
+// Coset frame of Algorithm 1, in float64 exactly as runtime.py:371-373:
+//   xl = x - l_k ; kk = floor(xl / d) * d ; xp = xl - kk
+struct CosetFrame {
+    double xp[3];
+    int cell[3];  // kk / d
+};
+
+template <typename T>
+__device__ __forceinline__ CosetFrame coset_frame(const T x[3], const FrameArgs& fr, int k) {
+    CosetFrame c;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double d = (double)fr.diag[i];
+        const double xl = (double)x[i] - (double)fr.shift[k][i];
+        const double q = floor(xl / d);
+        const double kk = q * d;
+        c.xp[i] = xl - kk;
+        c.cell[i] = clamp_cell(q);
+    }
+    return c;
+}
+
+__device__ __forceinline__ double sel3(int i, double a, double b, double c) { return i == 0 ? a : (i == 1 ? b : c); }
+
+}  // namespace sp

@@ -1,0 +1,612 @@
+// splinerecon.cu — C ABI (include/splinerecon.h) over the sm_100a reconstruction kernels.
+//
+// Replaces the reference's batch evaluator PlanInterpreter.eval_batch -> _eval_batch
+// (runtime.py:244-248, :363-408).  sp_plan_create is the analogue of
+// PlanInterpreter.__init__ + _batch_tables (runtime.py:219-230, :256-272): it validates the
+// flattened EvaluationPlan, derives the site reach (halo) and picks the kernel family:
+//   * tensor-product B-spline (separable closed form, caller-asserted + verified here),
+//   * a plan-specialised kernel generated at build time (codegen.py) and matched by the
+//     plan's exact canonical content,
+//   * the generic table-driven kernel.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/splinerecon.h"
+#include "sp_common.cuh"
+#include "sp_evaluators.cuh"
+#include "sp_launch.cuh"
+
+
+// generated plan kernels + kGenerated[] registry (codegen.py)
+#include "generated/registry.inc"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define SP_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess) return fail(SP_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+    } while (0)
+
+// Class record packing shared with the generated kernels (codegen.py: decode_class()).
+//   x: kernel | perm_i << (4+2i) | (sign_i<0) << (10+i) | rho_i << (13+2i) | (tau_i<0) << (19+i)
+//   y: (t_i + 128) << 8i          z: (pib_i/d + 128) << 8i
+struct HostClass {
+    int kernel;
+    int perm[3], sign[3], t[3], rho[3], tau[3], pibd[3];
+};
+
+bool signed_perm(const double* m, int perm[3], int sign[3]) {
+    int used = 0;
+    for (int i = 0; i < 3; ++i) {
+        int nz = 0;
+        for (int j = 0; j < 3; ++j) {
+            const double v = m[3 * i + j];
+            if (v == 0.0) continue;
+            if (v != 1.0 && v != -1.0) return false;
+            ++nz;
+            perm[i] = j;
+            sign[i] = v > 0 ? 1 : -1;
+        }
+        if (nz != 1) return false;
+        used |= 1 << perm[i];
+    }
+    return used == 7;
+}
+
+}  // namespace
+
+struct sp_plan {
+    sp_kernel_kind kind = SP_KIND_GENERIC;
+    std::string name;
+    int s = 3, M = 1;
+    int diag[3] = {1, 1, 1};
+    int shifts[SP_MAX_COSETS][3] = {};
+    int reach_lo[3] = {0, 0, 0}, reach_hi[3] = {0, 0, 0};
+    int tp_degree = -1;
+    const sp::GenEntry* gen = nullptr;
+    void* d_tables = nullptr;  // generated: sigma + class records; generic: GenericTables
+    int table_bytes = 0;       // bytes staged into smem (generated only)
+    std::vector<void*> allocs;
+    int occ_f32 = 0, occ_f64 = 0;
+    int num_sms = 148;
+};
+
+namespace {
+
+template <typename V>
+int upload(sp_plan* p, const std::vector<V>& v, const V** out) {
+    void* d = nullptr;
+    const size_t bytes = std::max<size_t>(v.size() * sizeof(V), 16);
+    SP_CUDA(cudaMalloc(&d, bytes));
+    p->allocs.push_back(d);
+    if (!v.empty()) SP_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(V), cudaMemcpyHostToDevice));
+    *out = reinterpret_cast<const V*>(d);
+    return SP_OK;
+}
+
+uint64_t as_u64(double v) {
+    uint64_t u;
+    std::memcpy(&u, &v, 8);
+    return u;
+}
+
+// Canonical content of a plan: the exact sequence codegen.py:canonical_words() emits.
+std::vector<uint64_t> canonical_words(const sp_plan_desc& d, int n_sites, int n_terms) {
+    std::vector<uint64_t> w;
+    auto I = [&](int64_t v) { w.push_back((uint64_t)v); };
+    auto D = [&](double v) { w.push_back(as_u64(v)); };
+    const int s = d.s;
+    I(s); I(d.M);
+    for (int i = 0; i < s; ++i) I(d.diag[i]);
+    for (int k = 0; k < d.M; ++k)
+        for (int i = 0; i < s; ++i) I(d.shifts[k][i]);
+    I(d.Q);
+    for (int j = 0; j < d.Q * s; ++j) I(d.normals[j]);
+    for (int j = 0; j < d.Q; ++j) D(d.offsets[j]);
+    I(d.r);
+    for (int j = 0; j < d.r; ++j) I(d.sigma[j]);
+    I(d.N);
+    for (int c = 0; c < d.N; ++c) I(d.cls_kernel[c]);
+    for (int j = 0; j < d.N * s * s; ++j) D(d.cls_T[j]);
+    for (int j = 0; j < d.N * s; ++j) D(d.cls_t[j]);
+    for (int j = 0; j < d.N * s * s; ++j) I(d.cls_piA[j]);
+    for (int j = 0; j < d.N * s; ++j) I(d.cls_pib[j]);
+    I(d.K);
+    for (int j = 0; j <= d.K; ++j) I(d.kernel_group_start[j]);
+    I(d.n_groups);
+    for (int g = 0; g < d.n_groups; ++g) I(d.group_nspan[g]);
+    for (int j = 0; j < d.n_groups * SP_MAX_DIM; ++j) I(d.group_span[j]);
+    for (int j = 0; j <= d.n_groups; ++j) I(d.group_site_start[j]);
+    for (int j = 0; j < n_sites * s; ++j) I(d.sites[j]);
+    for (int j = 0; j <= d.n_groups; ++j) I(d.group_poly_start[j]);
+    I(d.n_polys);
+    for (int j = 0; j <= d.n_polys; ++j) I(d.poly_term_start[j]);
+    for (int j = 0; j < n_terms * s; ++j) I(d.term_exps[j]);
+    for (int j = 0; j < n_terms; ++j) D(d.term_coeffs[j]);
+    return w;
+}
+
+double poly_eval_host(const sp_plan_desc& d, int p, const double y[3]) {
+    double acc = 0.0;
+    for (int t = d.poly_term_start[p]; t < d.poly_term_start[p + 1]; ++t) {
+        double m = d.term_coeffs[t];
+        for (int i = 0; i < 3; ++i) m *= std::pow(y[i], d.term_exps[3 * t + i]);
+        acc += m;
+    }
+    return acc;
+}
+
+double bspline_w(int deg, int a, double t) {
+    // weight of site floor(x) - deg + a; matches sp_evaluators.cuh BWeights
+    const double s = 1.0 - t;
+    switch (deg) {
+        case 1: return a == 0 ? s : t;
+        case 2: return a == 0 ? 0.5 * s * s : (a == 2 ? 0.5 * t * t : t * s + 0.5);
+        case 3:
+            if (a == 0) return s * s * s / 6.0;
+            if (a == 3) return t * t * t / 6.0;
+            if (a == 1) return (3 * t * t * t - 6 * t * t + 4) / 6.0;
+            return (3 * s * s * s - 6 * s * s + 4) / 6.0;
+    }
+    return NAN;
+}
+
+// Numerical check of the caller's tensor-product assertion: plan weights (reconstructed
+// from g and t_nums exactly as plancompile.py:676-699 lowers them) vs the closed form.
+int verify_tensor(const sp_plan_desc& d, int deg) {
+    if (deg < 1 || deg > 3) return fail(SP_ERR_UNSUPPORTED, "tensor-product degree %d not implemented", deg);
+    if (d.M != 1 || d.Q != 0 || d.N != 1 || d.K != 1 || d.diag[0] != 1 || d.diag[1] != 1 || d.diag[2] != 1)
+        return fail(SP_ERR_INVALID, "tp_degree asserted for a plan that is not single-coset Cartesian");
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            if (d.cls_T[3 * i + j] != (i == j ? 1.0 : 0.0) || d.cls_piA[3 * i + j] != (i == j ? 1 : 0))
+                return fail(SP_ERR_INVALID, "tp_degree asserted for a plan with a non-identity class");
+        }
+    for (int i = 0; i < 3; ++i)
+        if (d.cls_t[i] != 0.0 || d.cls_pib[i] != 0) return fail(SP_ERR_INVALID, "tp_degree: non-zero class shift");
+    uint64_t st = 0x9E3779B97F4A7C15ull;
+    auto rnd = [&]() {
+        st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+        return (double)(st >> 11) * (1.0 / 9007199254740992.0);
+    };
+    const int want = (deg + 1) * (deg + 1) * (deg + 1);
+    for (int trial = 0; trial < 16; ++trial) {
+        const double y[3] = {rnd(), rnd(), rnd()};
+        std::vector<double> w(want, 0.0);
+        int seen = 0;
+        for (int g = d.kernel_group_start[0]; g < d.kernel_group_start[1]; ++g) {
+            const int ns = d.group_nspan[g];
+            const int p0 = d.group_poly_start[g];
+            const double gv = poly_eval_host(d, p0, y);
+            double t[3] = {0, 0, 0};
+            for (int j = 0; j < ns; ++j) t[j] = gv == 0 ? 0.5 : poly_eval_host(d, p0 + 1 + j, y) / gv;
+            for (int c = 0; c < (1 << ns); ++c) {
+                const int* site = d.sites + 3 * (d.group_site_start[g] + c);
+                double wc = gv;
+                for (int j = 0; j < ns; ++j) wc *= ((c >> j) & 1) ? t[j] : 1.0 - t[j];
+                int idx = 0;
+                for (int i = 0; i < 3; ++i) {
+                    const int a = site[i] + deg;
+                    if (a < 0 || a > deg) return fail(SP_ERR_INVALID, "tp_degree: site outside the B-spline footprint");
+                    idx = idx * (deg + 1) + a;
+                }
+                w[idx] += wc;
+                ++seen;
+            }
+        }
+        if (seen != want) return fail(SP_ERR_INVALID, "tp_degree: plan has %d sites, expected %d", seen, want);
+        for (int a0 = 0; a0 <= deg; ++a0)
+            for (int a1 = 0; a1 <= deg; ++a1)
+                for (int a2 = 0; a2 <= deg; ++a2) {
+                    const double ref = bspline_w(deg, a0, y[0]) * bspline_w(deg, a1, y[1]) * bspline_w(deg, a2, y[2]);
+                    const double got = w[(a0 * (deg + 1) + a1) * (deg + 1) + a2];
+                    if (std::fabs(ref - got) > 1e-9) return fail(SP_ERR_INVALID, "tp_degree: weights differ (%g vs %g)", got, ref);
+                }
+    }
+    return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sp_last_error(void) { return g_err.c_str(); }
+const char* sp_version(void) { return "splinerecon 0.1.0 (sm_100a)"; }
+
+int sp_plan_create(const sp_plan_desc* desc, sp_plan** out) {
+    if (!desc || !out) return fail(SP_ERR_INVALID, "null argument");
+    *out = nullptr;
+    const sp_plan_desc& d = *desc;
+    if (d.s != 3) return fail(SP_ERR_UNSUPPORTED, "only s == 3 plans are implemented on the GPU (got s=%d)", d.s);
+    if (d.M < 1 || d.M > SP_MAX_COSETS) return fail(SP_ERR_UNSUPPORTED, "M=%d cosets not supported", d.M);
+    if (d.Q < 0 || d.Q > 62) return fail(SP_ERR_UNSUPPORTED, "Q=%d planes not supported", d.Q);
+    if (d.r < 1 || d.N < 1 || d.K < 1 || d.n_groups < 0 || d.n_polys < 0) return fail(SP_ERR_INVALID, "bad plan sizes");
+    for (int i = 0; i < 3; ++i)
+        if (d.diag[i] <= 0) return fail(SP_ERR_INVALID, "diag must be positive");
+    for (int j = 0; j < d.r; ++j)
+        if (d.sigma[j] < -1 || d.sigma[j] >= d.N) return fail(SP_ERR_INVALID, "sigma entry out of range");
+    for (int c = 0; c < d.N; ++c)
+        if (d.cls_kernel[c] < 0 || d.cls_kernel[c] >= d.K) return fail(SP_ERR_INVALID, "class kernel out of range");
+    if (d.kernel_group_start[0] != 0 || d.kernel_group_start[d.K] != d.n_groups)
+        return fail(SP_ERR_INVALID, "kernel_group_start inconsistent");
+    for (int g = 0; g < d.n_groups; ++g) {
+        const int ns = d.group_nspan[g];
+        if (ns < 0 || ns > 3) return fail(SP_ERR_INVALID, "group span must be 0..3");
+        if (d.group_site_start[g + 1] - d.group_site_start[g] != (1 << ns))
+            return fail(SP_ERR_INVALID, "group %d: size != 2^len(span_axes)", g);
+        if (d.group_poly_start[g + 1] - d.group_poly_start[g] != 1 + ns)
+            return fail(SP_ERR_INVALID, "group %d: need g + one t_num per span axis", g);
+    }
+    const int n_sites = d.group_site_start[d.n_groups];
+    if (d.group_poly_start[d.n_groups] != d.n_polys) return fail(SP_ERR_INVALID, "poly count inconsistent");
+    const int n_terms = d.poly_term_start[d.n_polys];
+
+    sp_plan* p = new sp_plan();
+    p->s = d.s;
+    p->M = d.M;
+    for (int i = 0; i < 3; ++i) p->diag[i] = d.diag[i];
+    for (int k = 0; k < d.M; ++k)
+        for (int i = 0; i < 3; ++i) p->shifts[k][i] = d.shifts[k][i];
+
+    // site offsets per class: (piA site + pib) / d must be integral (SURVEY.md §9 probe11)
+    std::vector<int> site_off((size_t)d.N * n_sites * 3);
+    bool first = true;
+    for (int c = 0; c < d.N; ++c) {
+        for (int g = 0; g < d.n_groups; ++g) {
+            int kern = 0;
+            while (d.kernel_group_start[kern + 1] <= g) ++kern;
+            for (int sidx = d.group_site_start[g]; sidx < d.group_site_start[g + 1]; ++sidx) {
+                for (int i = 0; i < 3; ++i) {
+                    long long m = d.cls_pib[3 * c + i];
+                    for (int j = 0; j < 3; ++j) m += (long long)d.cls_piA[9 * c + 3 * i + j] * d.sites[3 * sidx + j];
+                    if (m % d.diag[i] != 0) {
+                        delete p;
+                        return fail(SP_ERR_INVALID, "mapped site not on the zero coset (class %d)", c);
+                    }
+                    const int z = (int)(m / d.diag[i]);
+                    site_off[((size_t)c * n_sites + sidx) * 3 + i] = z;
+                    if (kern == d.cls_kernel[c]) {
+                        if (first) { p->reach_lo[i] = p->reach_hi[i] = z; }
+                        else {
+                            p->reach_lo[i] = std::min(p->reach_lo[i], z);
+                            p->reach_hi[i] = std::max(p->reach_hi[i], z);
+                        }
+                    }
+                }
+                if (kern == d.cls_kernel[c]) first = false;
+            }
+        }
+    }
+
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+
+    if (d.tp_degree >= 0) {
+        int rc = verify_tensor(d, d.tp_degree);
+        if (rc != SP_OK) { delete p; return rc; }
+        p->kind = SP_KIND_TENSOR_BSPLINE;
+        p->tp_degree = d.tp_degree;
+        p->name = "tensor_bspline_" + std::to_string(d.tp_degree);
+        *out = p;
+        return SP_OK;
+    }
+
+    const std::vector<uint64_t> words = canonical_words(d, n_sites, n_terms);
+    for (const sp::GenEntry* ep : kGenerated) {
+        if (d.tp_degree == -2) break;  // caller forces the generic kernel
+        if (!ep) continue;
+        const sp::GenEntry& e = *ep;
+        if (e.blob_len == (int)words.size() && std::memcmp(e.blob, words.data(), words.size() * 8) == 0) {
+            p->gen = &e;
+            break;
+        }
+    }
+
+    if (p->gen) {
+        // smem tables: int32 sigma[r] (16B aligned) + uint4 class records [N]
+        const int sig_bytes = ((d.r * 4) + 15) & ~15;
+        std::vector<uint32_t> blob(sig_bytes / 4 + 4 * d.N, 0);
+        for (int j = 0; j < d.r; ++j) blob[j] = (uint32_t)d.sigma[j];
+        for (int c = 0; c < d.N; ++c) {
+            int perm[3], sign[3], rho[3], tau[3];
+            if (!signed_perm(d.cls_T + 9 * c, perm, sign)) { delete p; return fail(SP_ERR_INVALID, "generated plan needs signed-permutation T"); }
+            double A[9];
+            for (int j = 0; j < 9; ++j) A[j] = d.cls_piA[9 * c + j];
+            if (!signed_perm(A, rho, tau)) { delete p; return fail(SP_ERR_INVALID, "generated plan needs signed-permutation piA"); }
+            uint32_t x = (uint32_t)d.cls_kernel[c];
+            uint32_t y = 0, z = 0;
+            for (int i = 0; i < 3; ++i) {
+                x |= (uint32_t)perm[i] << (4 + 2 * i);
+                x |= (uint32_t)(sign[i] < 0) << (10 + i);
+                x |= (uint32_t)rho[i] << (13 + 2 * i);
+                x |= (uint32_t)(tau[i] < 0) << (19 + i);
+                const int ti = (int)d.cls_t[3 * c + i];
+                if ((double)ti != d.cls_t[3 * c + i]) { delete p; return fail(SP_ERR_INVALID, "non-integral class shift t"); }
+                y |= (uint32_t)(ti + 128) << (8 * i);
+                z |= (uint32_t)(d.cls_pib[3 * c + i] / d.diag[i] + 128) << (8 * i);
+            }
+            uint32_t* rec = blob.data() + sig_bytes / 4 + 4 * c;
+            rec[0] = x; rec[1] = y; rec[2] = z; rec[3] = 0;
+        }
+        const uint32_t* dptr = nullptr;
+        if (upload(p, blob, &dptr) != SP_OK) { delete p; return SP_ERR_CUDA; }
+        p->d_tables = (void*)dptr;
+        p->table_bytes = (int)(blob.size() * 4);
+        p->kind = SP_KIND_GENERATED;
+        p->name = std::string("gen:") + p->gen->name;
+        *out = p;
+        return SP_OK;
+    }
+
+    // generic tables
+    sp::GenericTables gt{};
+    gt.Q = d.Q; gt.r = d.r; gt.N = d.N; gt.K = d.K; gt.n_sites = n_sites;
+    std::vector<int> normals(d.normals, d.normals + d.Q * 3);
+    std::vector<double> offsets(d.offsets, d.offsets + d.Q);
+    std::vector<int> sigma(d.sigma, d.sigma + d.r);
+    std::vector<int> ck(d.cls_kernel, d.cls_kernel + d.N);
+    std::vector<double> cT(d.cls_T, d.cls_T + d.N * 9), ct(d.cls_t, d.cls_t + d.N * 3);
+    std::vector<int> kgs(d.kernel_group_start, d.kernel_group_start + d.K + 1);
+    std::vector<int> gns(d.group_nspan, d.group_nspan + d.n_groups);
+    std::vector<int> gss(d.group_site_start, d.group_site_start + d.n_groups + 1);
+    std::vector<int> gps(d.group_poly_start, d.group_poly_start + d.n_groups + 1);
+    std::vector<int> pts(d.poly_term_start, d.poly_term_start + d.n_polys + 1);
+    std::vector<int> tex(d.term_exps, d.term_exps + n_terms * 3);
+    std::vector<double> tco(d.term_coeffs, d.term_coeffs + n_terms);
+    int rc = SP_OK;
+    rc |= upload(p, normals, &gt.normals);
+    rc |= upload(p, offsets, &gt.offsets);
+    rc |= upload(p, sigma, &gt.sigma);
+    rc |= upload(p, ck, &gt.cls_kernel);
+    rc |= upload(p, cT, &gt.cls_T);
+    rc |= upload(p, ct, &gt.cls_t);
+    rc |= upload(p, kgs, &gt.kernel_group_start);
+    rc |= upload(p, gns, &gt.group_nspan);
+    rc |= upload(p, gss, &gt.group_site_start);
+    rc |= upload(p, gps, &gt.group_poly_start);
+    rc |= upload(p, site_off, &gt.site_off);
+    rc |= upload(p, pts, &gt.poly_term_start);
+    rc |= upload(p, tex, &gt.term_exps);
+    rc |= upload(p, tco, &gt.term_coeffs);
+    if (rc != SP_OK) { delete p; return SP_ERR_CUDA; }
+    void* dgt = nullptr;
+    if (cudaMalloc(&dgt, sizeof gt) != cudaSuccess || cudaMemcpy(dgt, &gt, sizeof gt, cudaMemcpyHostToDevice) != cudaSuccess) {
+        delete p;
+        return fail(SP_ERR_CUDA, "generic table upload failed");
+    }
+    p->allocs.push_back(dgt);
+    p->d_tables = dgt;
+    p->table_bytes = 0;
+    p->kind = SP_KIND_GENERIC;
+    p->name = "generic";
+    *out = p;
+    return SP_OK;
+}
+
+void sp_plan_destroy(sp_plan* plan) {
+    if (!plan) return;
+    for (void* ptr : plan->allocs) cudaFree(ptr);
+    delete plan;
+}
+
+int sp_plan_kernel_kind(const sp_plan* plan) { return plan ? (int)plan->kind : -1; }
+const char* sp_plan_kernel_name(const sp_plan* plan) { return plan ? plan->name.c_str() : ""; }
+
+int sp_eval_launch_count(const sp_plan* plan, int64_t n) { return (plan && n > 0) ? 1 : 0; }
+
+}  // extern "C"
+
+namespace {
+
+constexpr int kTileBytes = 32 * 1024;
+
+template <typename T>
+int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, void* out, int32_t* dbg,
+               int32_t* err, cudaStream_t st) {
+    sp::EvalArgs<T> a{};
+    a.grid.M = g->M;
+    a.grid.boundary = g->boundary;
+    for (int k = 0; k < g->M; ++k) {
+        a.grid.data[k] = reinterpret_cast<const T*>(g->data[k]);
+        for (int i = 0; i < 3; ++i) {
+            if (g->extent[k][i] < 1 || g->extent[k][i] > (1ll << 30)) return fail(SP_ERR_INVALID, "coset extent out of range");
+            if (g->origin[k][i] < -(1ll << 30) || g->origin[k][i] > (1ll << 30)) return fail(SP_ERR_INVALID, "coset origin out of range");
+            a.grid.ext[k][i] = (int)g->extent[k][i];
+            a.grid.org[k][i] = (int)g->origin[k][i];
+        }
+        if (!g->data[k]) return fail(SP_ERR_INVALID, "null coset array %d", k);
+    }
+    a.fr.M = p->M;
+    for (int i = 0; i < 3; ++i) {
+        a.fr.diag[i] = p->diag[i];
+        a.fr.reach_lo[i] = p->reach_lo[i];
+        a.fr.reach_hi[i] = p->reach_hi[i];
+    }
+    for (int k = 0; k < p->M; ++k)
+        for (int i = 0; i < 3; ++i) a.fr.shift[k][i] = p->shifts[k][i];
+    a.pts = reinterpret_cast<const T*>(pts);
+    a.out = reinterpret_cast<T*>(out);
+    a.n = n;
+    a.dbg = dbg;
+    a.err = err;
+    a.tables = p->d_tables;
+    a.table_bytes = p->table_bytes;
+    a.tile_cap = kTileBytes / (int)sizeof(T);
+    const size_t smem = (size_t)((p->table_bytes + 15) & ~15) + kTileBytes;
+    const long long nchunks = (n + sp::kChunk - 1) / sp::kChunk;
+
+    cudaError_t e = cudaSuccess;
+    int per_sm = 1;
+    sp::LaunchFn<T> fn = nullptr;
+    if (p->kind == SP_KIND_TENSOR_BSPLINE) {
+        switch (p->tp_degree) {
+            case 1: fn = &sp::launch_eval<T, sp::TensorBSplineEval<T, 1>>; per_sm = sp::occupancy_blocks<T, sp::TensorBSplineEval<T, 1>>(smem); break;
+            case 2: fn = &sp::launch_eval<T, sp::TensorBSplineEval<T, 2>>; per_sm = sp::occupancy_blocks<T, sp::TensorBSplineEval<T, 2>>(smem); break;
+            case 3: fn = &sp::launch_eval<T, sp::TensorBSplineEval<T, 3>>; per_sm = sp::occupancy_blocks<T, sp::TensorBSplineEval<T, 3>>(smem); break;
+            default: return fail(SP_ERR_UNSUPPORTED, "tensor degree");
+        }
+    } else if (p->kind == SP_KIND_GENERATED) {
+        if constexpr (sizeof(T) == 4) { fn = p->gen->launch_f32; per_sm = p->gen->occ_f32(smem); }
+        else { fn = p->gen->launch_f64; per_sm = p->gen->occ_f64(smem); }
+    } else {
+        fn = &sp::launch_eval<T, sp::GenericEval<T>>;
+        per_sm = sp::occupancy_blocks<T, sp::GenericEval<T>>(smem);
+    }
+    const long long cap = (long long)p->num_sms * per_sm;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>(nchunks, cap));
+    e = fn(a, blocks, smem, st);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return SP_OK;
+}
+
+int check_grid(const sp_plan* p, const sp_grid_desc* g, int32_t dtype) {
+    if (!g) return fail(SP_ERR_INVALID, "null grid");
+    if (g->s != p->s || g->M != p->M) return fail(SP_ERR_MISMATCH, "grid decomposition does not match the plan header");
+    for (int i = 0; i < 3; ++i)
+        if (g->diag[i] != p->diag[i]) return fail(SP_ERR_MISMATCH, "grid decomposition does not match the plan header");
+    for (int k = 0; k < p->M; ++k)
+        for (int i = 0; i < 3; ++i)
+            if (g->shifts[k][i] != p->shifts[k][i]) return fail(SP_ERR_MISMATCH, "grid decomposition does not match the plan header");
+    if (g->dtype != dtype) return fail(SP_ERR_INVALID, "grid dtype must equal the point dtype");
+    if (g->boundary < SP_ZERO || g->boundary > SP_MIRROR) return fail(SP_ERR_INVALID, "unknown boundary policy %d", g->boundary);
+    return SP_OK;
+}
+
+}  // namespace
+
+extern "C" int sp_eval(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+                       void* out, int32_t* dbg, int32_t* err_flag, void* stream) {
+    if (!plan) return fail(SP_ERR_INVALID, "null plan");
+    int rc = check_grid(plan, grid, dtype);
+    if (rc != SP_OK) return rc;
+    if (n < 0) return fail(SP_ERR_INVALID, "negative n");
+    if (n == 0) return SP_OK;
+    if (!pts || !out) return fail(SP_ERR_INVALID, "null points or output");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32) return eval_typed<float>(plan, grid, pts, n, out, dbg, err_flag, st);
+    if (dtype == SP_F64) return eval_typed<double>(plan, grid, pts, n, out, dbg, err_flag, st);
+    return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+extern "C" int sp_eval_sync(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+                            void* out, void* stream) {
+    int32_t* d_err = nullptr;
+    SP_CUDA(cudaMalloc(&d_err, sizeof(int32_t)));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(d_err, 0, sizeof(int32_t), st);
+    int rc = sp_eval(plan, grid, pts, n, dtype, out, nullptr, d_err, stream);
+    int32_t h_err = 0;
+    if (rc == SP_OK) {
+        cudaError_t e = cudaMemcpyAsync(&h_err, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = fail(SP_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+    }
+    cudaFree(d_err);
+    if (rc == SP_OK && h_err) rc = fail(SP_ERR_SENTINEL, "sigma sentinel hit in batch evaluation");
+    return rc;
+}
+
+// ---------------------------------------------------------------------------------------
+// Point-order utilities
+
+namespace {
+
+__device__ __forceinline__ uint64_t spread3(uint32_t v) {
+    // 21 bits -> every third bit
+    uint64_t x = v & 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+template <typename T>
+__global__ void morton_kernel(const T* __restrict__ pts, long long n, uint64_t* __restrict__ keys) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        uint32_t c[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            // bias so that cells in [-2^20, 2^20) map monotonically to [0, 2^21)
+            const int f = sp::clamp_cell(pts[3 * i + a]);
+            const int b = min(max(f + (1 << 20), 0), (1 << 21) - 1);
+            c[a] = (uint32_t)b;
+        }
+        // axis 2 (fastest array axis) in the lowest bit
+        keys[i] = spread3(c[2]) | (spread3(c[1]) << 1) | (spread3(c[0]) << 2);
+    }
+}
+
+template <typename T>
+__global__ void scatter_kernel(const T* __restrict__ src, const int64_t* __restrict__ perm, long long n, T* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[perm[i]] = src[i];
+}
+
+template <typename T>
+__global__ void gather_points_kernel(const T* __restrict__ pts, const int64_t* __restrict__ perm, long long n, T* __restrict__ dst) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long j = perm[i];
+        dst[3 * i] = pts[3 * j];
+        dst[3 * i + 1] = pts[3 * j + 1];
+        dst[3 * i + 2] = pts[3 * j + 2];
+    }
+}
+
+int grid_for(int64_t n) {
+    long long b = (n + 255) / 256;
+    return (int)std::max<long long>(1, std::min<long long>(b, 148ll * 16));
+}
+
+}  // namespace
+
+extern "C" int sp_morton_keys(const void* pts, int64_t n, int32_t dtype, uint64_t* keys, void* stream) {
+    if (n <= 0) return SP_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32) morton_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, n, keys);
+    else if (dtype == SP_F64) morton_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, n, keys);
+    else return fail(SP_ERR_INVALID, "unknown dtype");
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
+extern "C" int sp_scatter(const void* src, const int64_t* perm, int64_t n, int32_t dtype, void* out, void* stream) {
+    if (n <= 0) return SP_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32) scatter_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)src, perm, n, (float*)out);
+    else if (dtype == SP_F64) scatter_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)src, perm, n, (double*)out);
+    else return fail(SP_ERR_INVALID, "unknown dtype");
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
+extern "C" int sp_gather_points(const void* pts, const int64_t* perm, int64_t n, int32_t dtype, void* dst, void* stream) {
+    if (n <= 0) return SP_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32) gather_points_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, perm, n, (float*)dst);
+    else if (dtype == SP_F64) gather_points_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, perm, n, (double*)dst);
+    else return fail(SP_ERR_INVALID, "unknown dtype");
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}

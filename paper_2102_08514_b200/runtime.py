@@ -1,0 +1,364 @@
+"""Reconstruct / evaluate: `CoefficientGrid` + `PlanInterpreter.eval_batch` on B200.
+
+Drop-in for the reference runtime (runtime.py:38-276): same class and method names,
+argument meanings and errors, with torch tensors (CUDA) in place of numpy arrays.
+
+* `CoefficientGrid(cosets, arrays, origins, boundary)` — per-coset C-order arrays
+  (axis s-1 fastest), site D z + l_k at arrays[k][z - origins[k]] (runtime.py:38-63).
+  Arrays live in HBM as contiguous float32 or float64 tensors.
+* `PlanInterpreter(plan).eval_batch(grid, pts)` — Algorithm 1 over the batch
+  (runtime.py:244-248 -> :363-408), executed by libsplinerecon.so (sp_eval).  numpy
+  input gives numpy float64 output, as the reference does (host<->device copies
+  included); CUDA tensor input gives a CUDA tensor of the grid's dtype.
+* errors: `RuntimeError_` (a ValueError, runtime.py:31-32) for unknown boundary/mode,
+  grid/plan mismatch (runtime.py:250-254) and the sigma sentinel (runtime.py:380-381).
+
+Arithmetic: the compute dtype is the grid's dtype.  Coset frames and plane tests are
+always float64 (bit-exact classification); weights, fetches and the
+accumulation run in the compute dtype.  fp64 grids reproduce the reference to ~1e-15
+relative; fp32 grids to ~1e-7 of max|f|.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Callable, Sequence
+
+import numpy as np
+import torch
+
+from . import _native
+from .lattice import CosetDecomposition
+from .packing import pack_plan
+from .plan import EvaluationPlan, deserialize_plan
+
+_BOUNDARIES = ("zero", "clamp", "mirror")
+
+
+class RuntimeError_(ValueError):
+    """runtime.py:31-32."""
+
+
+def _as_tensor(a, device, dtype) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        t = a
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a)))
+    if dtype is None:
+        dtype = t.dtype if t.dtype in (torch.float32, torch.float64) else torch.float64
+    return t.to(device=device, dtype=dtype).contiguous()
+
+
+def _default_device():
+    return torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
+
+
+class CoefficientGrid:
+    """Per-coset s-dimensional arrays with a boundary policy (runtime.py:38-105)."""
+
+    def __init__(self, cosets: CosetDecomposition, arrays: Sequence, origins: Sequence[tuple],
+                 boundary: str = "zero", device=None, dtype: torch.dtype | None = None):
+        if boundary not in _BOUNDARIES:
+            raise RuntimeError_(f"unknown boundary policy {boundary}")
+        if len(arrays) != cosets.M:
+            raise RuntimeError_("one array per coset required")
+        device = torch.device(device) if device is not None else _default_device()
+        self.cosets = cosets
+        self.arrays = [_as_tensor(a, device, dtype) for a in arrays]
+        if len({a.dtype for a in self.arrays}) != 1:
+            raise RuntimeError_("all coset arrays must share one dtype")
+        self.origins = [tuple(int(v) for v in o) for o in origins]
+        self.boundary = boundary
+        s = cosets.parent.s
+        for a in self.arrays:
+            if a.dim() != s:
+                raise RuntimeError_("array rank must match the dimension")
+
+    @staticmethod
+    def zeros(cosets: CosetDecomposition, lo: Sequence, hi: Sequence, boundary: str = "zero",
+              device=None, dtype: torch.dtype = torch.float64) -> "CoefficientGrid":
+        """Grid covering all sites with real coordinates in [lo, hi] (runtime.py:65-78)."""
+        origins, shapes = grid_extents(cosets, lo, hi)
+        device = torch.device(device) if device is not None else _default_device()
+        arrays = [torch.zeros(sh, dtype=dtype, device=device) for sh in shapes]
+        return CoefficientGrid(cosets, arrays, origins, boundary, device=device, dtype=dtype)
+
+    # -- properties -------------------------------------------------------------
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.arrays[0].dtype
+
+    @property
+    def device(self) -> torch.device:
+        return self.arrays[0].device
+
+    def to(self, dtype: torch.dtype | None = None, device=None) -> "CoefficientGrid":
+        return CoefficientGrid(self.cosets, [a.to(device=device or a.device, dtype=dtype or a.dtype) for a in self.arrays],
+                               self.origins, self.boundary, device=device or self.device, dtype=dtype or self.dtype)
+
+    def site_count(self) -> int:
+        return sum(a.numel() for a in self.arrays)
+
+    def nbytes(self) -> int:
+        return sum(a.numel() * a.element_size() for a in self.arrays)
+
+    # -- host-side accessors (debug / setup; not the hot path) --------------------
+    def fill_from(self, fn: Callable) -> None:
+        """Vectorised runtime.py:80-89: fn receives an (m, s) float64 array of real site
+        coordinates and returns m values (a scalar-callable is applied per site)."""
+        for k, shift in enumerate(self.cosets.shifts):
+            arr = self.arrays[k]
+            idx = np.stack(np.meshgrid(*[np.arange(n) for n in arr.shape], indexing="ij"), -1).reshape(-1, arr.dim())
+            sites = (idx + np.array(self.origins[k])) * np.array(self.cosets.diag) + np.array(shift)
+            try:
+                vals = np.asarray(fn(sites.astype(np.float64)), dtype=np.float64).reshape(-1)
+                if vals.size != sites.shape[0]:
+                    raise ValueError
+            except Exception:
+                vals = np.array([fn(tuple(s)) for s in sites.tolist()], dtype=np.float64)
+            arr.copy_(torch.from_numpy(vals.reshape(tuple(arr.shape))).to(arr.dtype))
+
+    def site_value(self, site: Sequence) -> float:
+        ci = self.cosets.index_of(site)
+        z = tuple(c - o for c, o in zip(ci.cell, self.origins[ci.coset]))
+        return self._read_scalar(ci.coset, z)
+
+    def set_site(self, site: Sequence, value: float) -> None:
+        ci = self.cosets.index_of(site)
+        z = tuple(c - o for c, o in zip(ci.cell, self.origins[ci.coset]))
+        arr = self.arrays[ci.coset]
+        if any(v < 0 or v >= n for v, n in zip(z, arr.shape)):
+            raise RuntimeError_("site outside grid storage")
+        arr[z] = value
+
+    def _read_scalar(self, coset: int, z: tuple) -> float:
+        """runtime.py:109-123."""
+        arr = self.arrays[coset]
+        idx = []
+        for v, n in zip(z, arr.shape):
+            v = int(v)
+            if 0 <= v < n:
+                idx.append(v)
+                continue
+            if self.boundary == "zero":
+                return 0.0
+            if self.boundary == "clamp":
+                idx.append(min(max(v, 0), n - 1))
+            else:
+                idx.append(_mirror_index(v, n))
+        return float(arr[tuple(idx)])
+
+    def descriptor(self) -> _native.GridDesc:
+        if self.device.type != "cuda":
+            raise RuntimeError_("the grid must live on a CUDA device for evaluation")
+        s = self.cosets.parent.s
+        g = _native.GridDesc()
+        g.s = s
+        g.M = self.cosets.M
+        g.dtype = _native.SP_F32 if self.dtype == torch.float32 else _native.SP_F64
+        g.boundary = _native.BOUNDARY_CODES[self.boundary]
+        for i in range(min(s, 3)):
+            g.diag[i] = self.cosets.diag[i]
+        for k, sh in enumerate(self.cosets.shifts[: _native.SP_MAX_COSETS]):
+            for i in range(min(s, 3)):
+                g.shifts[k][i] = sh[i]
+            a = self.arrays[k]
+            g.data[k] = a.data_ptr()
+            for i in range(min(s, 3)):
+                g.extent[k][i] = a.shape[i]
+                g.origin[k][i] = self.origins[k][i]
+        return g
+
+
+def grid_extents(cosets: CosetDecomposition, lo: Sequence, hi: Sequence):
+    """Per-coset origins and shapes of CoefficientGrid.zeros (runtime.py:65-78)."""
+    origins, shapes = [], []
+    for shift in cosets.shifts:
+        zlo = [math.ceil((lo[i] - shift[i]) / d) for i, d in enumerate(cosets.diag)]
+        zhi = [math.floor((hi[i] - shift[i]) / d) for i, d in enumerate(cosets.diag)]
+        origins.append(tuple(zlo))
+        shapes.append(tuple(b - a + 1 for a, b in zip(zlo, zhi)))
+    return origins, shapes
+
+
+def _mirror_index(v: int, n: int) -> int:
+    if n == 1:
+        return 0
+    period = 2 * n - 2
+    v = abs(v) % period
+    return period - v if v >= n else v
+
+
+# ---------------------------------------------------------------------------
+# Plan interpretation
+
+
+class PlanInterpreter:
+    """Evaluation of (plan, grid, x) on the GPU; mode 'float' (runtime.py:216-248).
+
+    The plan is validated and specialised once (sp_plan_create): tensor-product
+    B-spline plans run the separable kernel (proven equal, plan.py), catalog plans run
+    their build-time generated kernel, anything else the generic table-driven kernel.
+    """
+
+    def __init__(self, plan, mode: str = "float", kernel: str = "auto"):
+        if mode not in ("float", "exact"):
+            raise RuntimeError_(f"unknown interpreter mode {mode}")
+        if kernel not in ("auto", "generic"):
+            raise RuntimeError_(f"unknown kernel selection {kernel}")
+        if isinstance(plan, str):
+            plan = deserialize_plan(plan)
+        if not isinstance(plan, EvaluationPlan):
+            raise RuntimeError_("plan must be an EvaluationPlan or a plan document")
+        self.plan = plan
+        self.mode = mode
+        self._handles: dict = {}
+        self._tp = plan.tensor_bspline_degree()
+        self._kernel = kernel
+
+    # -- native plan handle (one per device) ----------------------------------
+    def _handle(self, device: torch.device):
+        key = device.index if device.index is not None else torch.cuda.current_device()
+        h = self._handles.get(key)
+        if h is None:
+            if self.plan.s != 3:
+                raise NotImplementedError(
+                    f"GPU evaluation is implemented for s == 3 plans (plan {self.plan.name!r} has s={self.plan.s})"
+                )
+            lib = _native.lib()
+            tp = -2 if self._kernel == "generic" else (-1 if self._tp is None else self._tp)
+            desc, keep = _native.make_plan_desc(pack_plan(self.plan), tp)
+            out = ctypes.c_void_p()
+            with torch.cuda.device(key):
+                code = lib.sp_plan_create(ctypes.byref(desc), ctypes.byref(out))
+            del keep
+            if code == _native.SP_ERR_UNSUPPORTED:
+                raise NotImplementedError(lib.sp_last_error().decode())
+            _native.check(code)
+            h = out.value
+            self._handles[key] = h
+        return h
+
+    def __del__(self):
+        try:
+            lib = _native._lib
+            if lib is not None:
+                for h in self._handles.values():
+                    lib.sp_plan_destroy(h)
+        except Exception:
+            pass
+
+    def kernel_name(self, device=None) -> str:
+        device = torch.device(device) if device is not None else _default_device()
+        return _native.lib().sp_plan_kernel_name(self._handle(device)).decode()
+
+    def _check_grid(self, grid: CoefficientGrid) -> None:
+        """runtime.py:250-254."""
+        if tuple(grid.cosets.diag) != tuple(self.plan.diag) or tuple(grid.cosets.shifts) != tuple(self.plan.shifts):
+            raise RuntimeError_("grid decomposition does not match the plan header")
+
+    # -- evaluation -------------------------------------------------------------
+    def eval(self, grid: CoefficientGrid, x: Sequence) -> float:
+        """Single point (runtime.py:232-242), through the same GPU batch kernel."""
+        self._check_grid(grid)
+        if self.mode != "float":
+            raise NotImplementedError("exact-debug mode is a host-only reference aid (runtime.py:279-338)")
+        pts = torch.tensor([[float(v) for v in x]], dtype=grid.dtype, device=grid.device)
+        return float(self.eval_batch(grid, pts)[0])
+
+    def eval_batch(self, grid: CoefficientGrid, pts, *, out: torch.Tensor | None = None, check: bool = True,
+                   reorder: bool = False, stream: torch.cuda.Stream | None = None):
+        """Batch reconstruction (runtime.py:244-248).
+
+        pts: (n, s) numpy array (-> numpy float64 result, like the reference) or tensor
+        (-> tensor of the grid dtype on the grid device).  `check` synchronises and
+        raises RuntimeError_ on a sigma-sentinel hit (runtime.py:380-381); `reorder`
+        Morton-sorts the points on the GPU first (same results, faster for incoherent
+        point order on large batches).
+        """
+        self._check_grid(grid)
+        if self.mode != "float":
+            raise RuntimeError_("batch evaluation is float-mode only")
+        is_numpy = not isinstance(pts, torch.Tensor)
+        dev = grid.device
+        if dev.type != "cuda":
+            raise RuntimeError_("the grid must live on a CUDA device for evaluation")
+        if is_numpy:
+            pts = torch.from_numpy(np.ascontiguousarray(np.asarray(pts, dtype=np.float64)))
+        on_host = pts.device.type == "cpu"
+        if on_host:
+            # host buffers: H2D copy of the points, D2H copy of the result (pinned -> async)
+            src = pts.to(dtype=grid.dtype)
+            p = src.to(dev, non_blocking=src.is_pinned())
+        else:
+            p = pts.to(device=dev, dtype=grid.dtype).contiguous()
+        if p.dim() != 2 or p.shape[1] != self.plan.s:
+            raise RuntimeError_(f"points must have shape (n, {self.plan.s})")
+        n = p.shape[0]
+        res = out if (out is not None and out.device == dev) else torch.empty(n, dtype=grid.dtype, device=dev)
+        if n:
+            self._launch(grid, p, res, check=check, reorder=reorder, stream=stream)
+        if is_numpy:
+            return res.to("cpu").numpy().astype(np.float64)
+        if on_host:
+            if out is not None and out.device.type == "cpu":
+                out.copy_(res, non_blocking=out.is_pinned())
+                return out
+            return res.to("cpu")
+        return res
+
+    def classify(self, grid: CoefficientGrid, pts: torch.Tensor):
+        """Per point and coset: class id and coset cell kk/d (runtime.py:371-379), as
+        computed by the evaluation kernel itself.  Returns (classes (n,M), cells (n,M,s))."""
+        self._check_grid(grid)
+        p = torch.as_tensor(pts).to(device=grid.device, dtype=grid.dtype).contiguous()
+        n = p.shape[0]
+        M = self.plan.M
+        dbg = torch.empty((n, M, 4), dtype=torch.int32, device=grid.device)
+        res = torch.empty(n, dtype=grid.dtype, device=grid.device)
+        if n:
+            self._launch(grid, p, res, dbg=dbg, check=False)
+        return dbg[:, :, 0].to(torch.int64), dbg[:, :, 1:].to(torch.int64)
+
+    def _launch(self, grid, p, res, *, dbg=None, check=True, reorder=False, stream=None):
+        lib = _native.lib()
+        h = self._handle(grid.device)
+        gdesc = grid.descriptor()
+        dtype = _native.SP_F32 if grid.dtype == torch.float32 else _native.SP_F64
+        st = stream if stream is not None else torch.cuda.current_stream(grid.device)
+        err = torch.zeros(1, dtype=torch.int32, device=grid.device) if check else None
+        n = p.shape[0]
+        with torch.cuda.stream(st):
+            if reorder:
+                perm = morton_order(p, stream=st)
+                ps = torch.empty_like(p)
+                _native.check(lib.sp_gather_points(p.data_ptr(), perm.data_ptr(), n, dtype, ps.data_ptr(), st.cuda_stream))
+                tmp = torch.empty_like(res)
+                _native.check(lib.sp_eval(h, ctypes.byref(gdesc), ps.data_ptr(), n, dtype, tmp.data_ptr(),
+                                          None if dbg is None else dbg.data_ptr(),
+                                          None if err is None else err.data_ptr(), st.cuda_stream))
+                _native.check(lib.sp_scatter(tmp.data_ptr(), perm.data_ptr(), n, dtype, res.data_ptr(), st.cuda_stream))
+            else:
+                _native.check(lib.sp_eval(h, ctypes.byref(gdesc), p.data_ptr(), n, dtype, res.data_ptr(),
+                                          None if dbg is None else dbg.data_ptr(),
+                                          None if err is None else err.data_ptr(), st.cuda_stream))
+        if check and int(err.item()):
+            raise RuntimeError_("sigma sentinel hit in batch evaluation")
+
+
+def eval_plan(interp: PlanInterpreter, grid: CoefficientGrid, x: Sequence) -> float:
+    """runtime.py:275-276."""
+    return interp.eval(grid, x)
+
+
+def morton_order(pts: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Permutation sorting points by the Morton code of their unit cell floor(x)."""
+    lib = _native.lib()
+    st = stream if stream is not None else torch.cuda.current_stream(pts.device)
+    n = pts.shape[0]
+    keys = torch.empty(n, dtype=torch.int64, device=pts.device)
+    dtype = _native.SP_F32 if pts.dtype == torch.float32 else _native.SP_F64
+    _native.check(lib.sp_morton_keys(pts.data_ptr(), n, dtype, keys.data_ptr(), st.cuda_stream))
+    # keys < 2^63, so the signed sort is the unsigned order
+    return torch.sort(keys, stable=True).indices

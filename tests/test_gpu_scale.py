@@ -1,0 +1,74 @@
+"""GPU, BASELINE sizes: size-independent properties + oracle spot checks on subsamples."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.plan_numpy import NumpyGrid, PlanTables, eval_batch as oracle_eval
+from paper_2102_08514_b200 import corpus
+from paper_2102_08514_b200.runtime import CoefficientGrid, PlanInterpreter, morton_order
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = {
+    "cc_tricubic": 255,
+    "bcc_linear_rd": 405,
+    "bcc_quintic_rd": 405,
+    "fcc_cubic": 321,
+}
+
+
+def _grid(name, dtype, device, seed=7):
+    plan = corpus.build_plan(name)
+    _, cos = corpus.lattice_of(name)
+    hi = CONFIGS[name]
+    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [hi, hi, hi], device=device, dtype=dtype)
+    gen = torch.Generator(device=device).manual_seed(seed)
+    for a in grid.arrays:
+        a.copy_(torch.rand(a.shape, generator=gen, device=device, dtype=torch.float32).to(dtype))
+    return plan, grid, hi
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_full_size_subsample_vs_oracle(name, cuda):
+    plan, grid, hi = _grid(name, torch.float32, cuda)
+    n = 4_000_000
+    gen = torch.Generator(device=cuda).manual_seed(3)
+    pts = torch.rand((n, 3), generator=gen, device=cuda) * (hi + 1)
+    pts = pts[morton_order(pts)]
+    out = PlanInterpreter(plan).eval_batch(grid, pts)
+    idx = torch.randint(0, n, (3000,), generator=gen, device=cuda)
+    sub = pts[idx].double().cpu().numpy()
+    ngrid = NumpyGrid(plan.diag, plan.shifts, [a.double().cpu().numpy() for a in grid.arrays], grid.origins, "zero")
+    ref = oracle_eval(plan, ngrid, sub, PlanTables(plan))
+    got = out[idx].double().cpu().numpy()
+    assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name", ["cc_tricubic", "bcc_linear_rd"])
+def test_shift_invariance(name, cuda):
+    """eval(grid shifted by D z, x + D z) == eval(grid, x) for interior x."""
+    plan, grid, hi = _grid(name, torch.float64, cuda)
+    gen = torch.Generator(device=cuda).manual_seed(11)
+    pts = torch.rand((100_000, 3), generator=gen, device=cuda, dtype=torch.float64) * (hi - 20) + 10
+    interp = PlanInterpreter(plan)
+    a = interp.eval_batch(grid, pts)
+    d = plan.diag[0]
+    shift = (3 * d, -2 * d, 5 * d)
+    moved = CoefficientGrid(grid.cosets, grid.arrays,
+                            [tuple(o + s // d for o, s in zip(org, shift)) for org in grid.origins],
+                            "zero", device=cuda)
+    b = interp.eval_batch(moved, pts + torch.tensor(shift, dtype=torch.float64, device=cuda))
+    assert (a - b).abs().max().item() <= 1e-12
+
+
+def test_tricubic_fp64_full_size(cuda):
+    plan, grid, hi = _grid("cc_tricubic", torch.float64, cuda)
+    n = 2_000_000
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    pts = torch.rand((n, 3), generator=gen, device=cuda, dtype=torch.float64) * (hi + 1)
+    out = PlanInterpreter(plan).eval_batch(grid, pts, reorder=True)
+    idx = torch.randint(0, n, (2000,), generator=gen, device=cuda)
+    sub = pts[idx].cpu().numpy()
+    ngrid = NumpyGrid(plan.diag, plan.shifts, [a.cpu().numpy() for a in grid.arrays], grid.origins, "zero")
+    ref = oracle_eval(plan, ngrid, sub, PlanTables(plan))
+    assert np.abs(out[idx].cpu().numpy() - ref).max() <= 2e-11
