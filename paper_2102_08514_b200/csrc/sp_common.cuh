@@ -2,7 +2,7 @@
 //
 // The reference evaluates Algorithm 1 as numpy passes over the whole
 // batch (runtime.py:363-408) with fancy-index gathers into per-coset float64 arrays
-// (runtime.py:151-188).  Here one CTA owns a chunk of kChunk consecutive query points:
+// (runtime.py:151-188).  Here one CTA owns a chunk of kThreads*ppt consecutive query points:
 //
 //   1. it loads the chunk, reduces the bounding box of the points' unit cells,
 //   2. if the box (+ the plan's site reach, per coset) fits the shared-memory budget it
@@ -25,8 +25,7 @@
 namespace sp {
 
 constexpr int kThreads = 256;
-constexpr int kPPT = 4;                       // points per thread per chunk
-constexpr int kChunk = kThreads * kPPT;       // points per chunk
+constexpr int kMaxPPT = 8;                    // points per thread per chunk (runtime <= this)
 constexpr int kCellClamp = 1 << 30;           // |cell| clamp (mirror exact below this)
 
 template <typename T>
@@ -58,6 +57,8 @@ struct EvalArgs {
     const void* tables; // evaluator tables (device), copied to smem when table_bytes > 0
     int table_bytes;
     int tile_cap;       // staged-tile capacity in elements
+    int ppt;            // points per thread per chunk (chunk = kThreads * ppt)
+    int margin;         // extra halo cells (1 for float64 points on shifted cosets, else 0)
 };
 
 struct TileGeom {
@@ -111,6 +112,27 @@ __device__ __forceinline__ T policy_read(const GridArgs<T>& g, int k, int z0, in
     return __ldg(g.data[k] + ((long long)z0 * e1 + z1) * (long long)e2 + z2);
 }
 
+// Out-of-line variant for the (rare) unstaged path: keeps the kernels' code small.  Scalar
+// arguments only (a pointer to the kernel-parameter struct would force a local copy of it).
+template <typename T>
+__device__ __noinline__ T policy_read_slow(const T* data, int e0, int e1, int e2, int boundary, int z0, int z1,
+                                           int z2) {
+    const bool in = (unsigned)z0 < (unsigned)e0 && (unsigned)z1 < (unsigned)e1 && (unsigned)z2 < (unsigned)e2;
+    if (!in) {
+        if (boundary == SP_ZERO) return T(0);
+        if (boundary == SP_CLAMP) {
+            z0 = min(max(z0, 0), e0 - 1);
+            z1 = min(max(z1, 0), e1 - 1);
+            z2 = min(max(z2, 0), e2 - 1);
+        } else {
+            z0 = mirror_index(z0, e0);
+            z1 = mirror_index(z1, e1);
+            z2 = mirror_index(z2, e2);
+        }
+    }
+    return __ldg(data + ((long long)z0 * e1 + z1) * (long long)e2 + z2);
+}
+
 // ---------------------------------------------------------------------------------------
 // Fetchers.  A "frame" fixes the coset, the base cell and the class's site renaming
 // (piA = signed permutation rho/tau, probe12 of SURVEY.md §9): the site with zero-coset
@@ -119,6 +141,7 @@ __device__ __forceinline__ T policy_read(const GridArgs<T>& g, int k, int z0, in
 
 template <typename T>
 struct TileFetch {
+    static constexpr bool kIsTile = true;
     const T* tile;
     int a0;
     int c0, c1, c2;
@@ -154,15 +177,19 @@ struct TileFetch {
 
 template <typename T>
 struct GlobalFetch {
-    const GridArgs<T>* g;
-    int k;
+    static constexpr bool kIsTile = false;
+    const T* data;
+    int e0, e1, e2, boundary;
     int b0, b1, b2;       // base array index (cell - origin)
     int p[3][3];          // p[j][i] = tau_i if rho_i == j
 
     __device__ __forceinline__ void frame(const GridArgs<T>& grid, int kk, const int base[3], const int rho[3],
                                           const int tau[3]) {
-        g = &grid;
-        k = kk;
+        data = grid.data[kk];
+        e0 = grid.ext[kk][0];
+        e1 = grid.ext[kk][1];
+        e2 = grid.ext[kk][2];
+        boundary = grid.boundary;
         b0 = base[0] - grid.org[kk][0];
         b1 = base[1] - grid.org[kk][1];
         b2 = base[2] - grid.org[kk][2];
@@ -179,7 +206,7 @@ struct GlobalFetch {
         const int z0 = b0 + s0 * p[0][0] + s1 * p[1][0] + s2 * p[2][0];
         const int z1 = b1 + s0 * p[0][1] + s1 * p[1][1] + s2 * p[2][1];
         const int z2 = b2 + s0 * p[0][2] + s1 * p[1][2] + s2 * p[2][2];
-        return policy_read(*g, k, z0, z1, z2);
+        return policy_read_slow(data, e0, e1, e2, boundary, z0, z1, z2);
     }
 };
 
@@ -197,13 +224,26 @@ struct EvalCtx {
     long long index;              // point index (for debug output)
 };
 
-template <typename T>
-__device__ __forceinline__ void load_point(const T* __restrict__ pts, long long i, T x[3]) {
-    const T* p = pts + 3 * i;
-    x[0] = __ldg(p + 0);
-    x[1] = __ldg(p + 1);
-    x[2] = __ldg(p + 2);
+// cp.async (LDGSTS) element copy global -> shared; src_bytes = 0 zero-fills (boundary 'zero').
+template <int BYTES>
+__device__ __forceinline__ void cp_async_elem(void* smem_dst, const void* gsrc, int src_bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(gsrc), "n"(BYTES), "r"(src_bytes)
+                 : "memory");
 }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Fast unsigned division by a runtime divisor (Granlund-Montgomery), valid for n < 2^31.
+struct FastDiv {
+    unsigned d, m, s;
+    __device__ __forceinline__ void init(unsigned div) {
+        d = div;
+        s = 0;
+        while ((1u << s) < div) ++s;
+        m = (unsigned)((((unsigned long long)1 << 32) * ((1ull << s) - div)) / div + 1);
+    }
+    __device__ __forceinline__ unsigned div(unsigned n) const { return (__umulhi(n, m) + n) >> s; }
+};
 
 template <typename T, class Ev>
 __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
@@ -212,6 +252,7 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
     __shared__ int red[6];
 
     const int tid = threadIdx.x;
+    const int lane = tid & 31;
     // evaluator tables -> smem (16-byte granules)
     const int tb = (a.table_bytes + 15) & ~15;
     if (a.table_bytes > 0) {
@@ -219,31 +260,46 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
         int4* dst = reinterpret_cast<int4*>(smem);
         for (int i = tid; i < tb / 16; i += kThreads) dst[i] = src[i];
     }
-    T* tile = reinterpret_cast<T*>(smem + tb);
+    const int ppt = a.ppt;
+    const int chunk_pts = kThreads * ppt;
+    T* spts = reinterpret_cast<T*>(smem + tb);                        // [chunk_pts * 3]
+    T* tile = spts + ((chunk_pts * 3 * (int)sizeof(T) + 15) & ~15) / (int)sizeof(T);
 
     const long long n = a.n;
-    const long long nchunks = (n + kChunk - 1) / kChunk;
+    const long long nchunks = (n + chunk_pts - 1) / chunk_pts;
     const int M = a.fr.M;
 
     for (long long chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+        const long long first = chunk * chunk_pts;
+        const int cnt = (int)min((long long)chunk_pts, n - first);
+        // 1. points -> smem, coalesced (16-byte vectors when aligned)
+        {
+            const T* src = a.pts + 3 * first;
+            const int nel = 3 * cnt;
+            constexpr int kVec = 16 / (int)sizeof(T);
+            if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                const int nvec = nel / kVec;
+                const int4* s4 = reinterpret_cast<const int4*>(src);
+                int4* d4 = reinterpret_cast<int4*>(spts);
+                for (int v = tid; v < nvec; v += kThreads) d4[v] = __ldg(s4 + v);
+                for (int e = nvec * kVec + tid; e < nel; e += kThreads) spts[e] = __ldg(src + e);
+            } else {
+                for (int e = tid; e < nel; e += kThreads) spts[e] = __ldg(src + e);
+            }
+        }
         if (tid < 3) red[tid] = INT_MAX;
         else if (tid < 6) red[tid] = INT_MIN;
         __syncthreads();
 
+        // 2. bounding box of the chunk's unit cells floor(x)
         int lo0 = INT_MAX, lo1 = INT_MAX, lo2 = INT_MAX, hi0 = INT_MIN, hi1 = INT_MIN, hi2 = INT_MIN;
-        const long long base_i = chunk * kChunk + tid;
-#pragma unroll
-        for (int j = 0; j < kPPT; ++j) {
-            const long long i = base_i + (long long)j * kThreads;
-            if (i < n) {
-                T x[3];
-                load_point(a.pts, i, x);
-                if (isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2])) {
-                    const int f0 = clamp_cell(x[0]), f1 = clamp_cell(x[1]), f2 = clamp_cell(x[2]);
-                    lo0 = min(lo0, f0); hi0 = max(hi0, f0);
-                    lo1 = min(lo1, f1); hi1 = max(hi1, f1);
-                    lo2 = min(lo2, f2); hi2 = max(hi2, f2);
-                }
+        for (int j = tid; j < cnt; j += kThreads) {
+            const T x0 = spts[3 * j], x1 = spts[3 * j + 1], x2 = spts[3 * j + 2];
+            if (isfinite(x0) && isfinite(x1) && isfinite(x2)) {
+                const int f0 = clamp_cell(x0), f1 = clamp_cell(x1), f2 = clamp_cell(x2);
+                lo0 = min(lo0, f0); hi0 = max(hi0, f0);
+                lo1 = min(lo1, f1); hi1 = max(hi1, f1);
+                lo2 = min(lo2, f2); hi2 = max(hi2, f2);
             }
         }
         lo0 = __reduce_min_sync(0xffffffffu, lo0);
@@ -252,7 +308,7 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
         hi0 = __reduce_max_sync(0xffffffffu, hi0);
         hi1 = __reduce_max_sync(0xffffffffu, hi1);
         hi2 = __reduce_max_sync(0xffffffffu, hi2);
-        if ((tid & 31) == 0) {
+        if (lane == 0) {
             atomicMin(&red[0], lo0); atomicMin(&red[1], lo1); atomicMin(&red[2], lo2);
             atomicMax(&red[3], hi0); atomicMax(&red[4], hi1); atomicMax(&red[5], hi2);
         }
@@ -264,9 +320,8 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
                 long long vol = 1;
                 for (int i = 0; i < 3; ++i) {
                     const int d = a.fr.diag[i], l = a.fr.shift[k][i];
-                    // conservative by one cell each side (fp64 x - l rounding)
-                    const long long b0 = (long long)floordiv_i(red[i] - l, d) + a.fr.reach_lo[i] - 1;
-                    const long long b1 = (long long)floordiv_i(red[3 + i] - l, d) + a.fr.reach_hi[i] + 1;
+                    const long long b0 = (long long)floordiv_i(red[i] - l, d) + a.fr.reach_lo[i] - a.margin;
+                    const long long b1 = (long long)floordiv_i(red[3 + i] - l, d) + a.fr.reach_hi[i] + a.margin;
                     const long long e = b1 - b0 + 1;
                     vol *= e;
                     if (vol > a.tile_cap) { ok = false; break; }
@@ -282,50 +337,72 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
         }
         __syncthreads();
         const bool staged = geom.staged != 0;
+
+        // 3. stage the coefficient box (+ halo) with cp.async, boundary policy applied here
         if (staged) {
-            // fill: one coset at a time, consecutive threads walk the fastest axis (coalesced)
             for (int k = 0; k < M; ++k) {
-                const int e0 = geom.ex[k][0], e1 = geom.ex[k][1], e2 = geom.ex[k][2];
-                const int vol = e0 * e1 * e2;
-                const int off = geom.off[k];
+                const int e1 = geom.ex[k][1], e2 = geom.ex[k][2];
+                const int vol = geom.ex[k][0] * e1 * e2;
+                T* dst = tile + geom.off[k];
                 const int z0b = geom.lo[k][0] - a.grid.org[k][0];
                 const int z1b = geom.lo[k][1] - a.grid.org[k][1];
                 const int z2b = geom.lo[k][2] - a.grid.org[k][2];
+                const int g0 = a.grid.ext[k][0], g1 = a.grid.ext[k][1], g2 = a.grid.ext[k][2];
+                const T* base = a.grid.data[k];
+                FastDiv fd2, fd1;
+                fd2.init((unsigned)e2);
+                fd1.init((unsigned)e1);
+#pragma unroll 4
                 for (int e = tid; e < vol; e += kThreads) {
-                    const int i2 = e % e2;
-                    const int r = e / e2;
-                    const int i1 = r % e1;
-                    const int i0 = r / e1;
-                    tile[off + e] = policy_read(a.grid, k, z0b + i0, z1b + i1, z2b + i2);
+                    const int r = (int)fd2.div((unsigned)e);
+                    const int i2 = e - r * e2;
+                    const int i0 = (int)fd1.div((unsigned)r);
+                    const int i1 = r - i0 * e1;
+                    int z0 = z0b + i0, z1 = z1b + i1, z2 = z2b + i2;
+                    int bytes = (int)sizeof(T);
+                    if (!((unsigned)z0 < (unsigned)g0 && (unsigned)z1 < (unsigned)g1 && (unsigned)z2 < (unsigned)g2)) {
+                        if (a.grid.boundary == SP_ZERO) {
+                            bytes = 0;
+                            z0 = z1 = z2 = 0;
+                        } else if (a.grid.boundary == SP_CLAMP) {
+                            z0 = min(max(z0, 0), g0 - 1);
+                            z1 = min(max(z1, 0), g1 - 1);
+                            z2 = min(max(z2, 0), g2 - 1);
+                        } else {
+                            z0 = mirror_index(z0, g0);
+                            z1 = mirror_index(z1, g1);
+                            z2 = mirror_index(z2, g2);
+                        }
+                    }
+                    cp_async_elem<sizeof(T)>(dst + e, base + ((long long)z0 * g1 + z1) * (long long)g2 + z2, bytes);
                 }
             }
+            cp_async_wait_all();
         }
         __syncthreads();
 
+        // 4. evaluate
         EvalCtx<T, Ev> ctx;
         ctx.a = &a;
         ctx.tables = smem;
         ctx.geom = &geom;
 #pragma unroll 1
-        for (int j = 0; j < kPPT; ++j) {
-            const long long i = base_i + (long long)j * kThreads;
-            if (i < n) {
-                ctx.index = i;
-                T x[3];
-                load_point(a.pts, i, x);  // L1 hit: loaded by this CTA above
-                T v;
-                if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) {
-                    v = T(NAN);
-                } else if (staged) {
-                    TileFetch<T> f;
-                    f.tile = tile;
-                    v = Ev::template eval<TileFetch<T>>(x, f, ctx);
-                } else {
-                    GlobalFetch<T> f;
-                    v = Ev::template eval<GlobalFetch<T>>(x, f, ctx);
-                }
-                a.out[i] = v;
+        for (int j = tid; j < cnt; j += kThreads) {
+            const long long i = first + j;
+            ctx.index = i;
+            const T x[3] = {spts[3 * j], spts[3 * j + 1], spts[3 * j + 2]};
+            T v;
+            if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) {
+                v = T(NAN);
+            } else if (staged) {
+                TileFetch<T> f;
+                f.tile = tile;
+                v = Ev::template eval<TileFetch<T>>(x, f, ctx);
+            } else {
+                GlobalFetch<T> f;
+                v = Ev::template eval<GlobalFetch<T>>(x, f, ctx);
             }
+            a.out[i] = v;
         }
         __syncthreads();
     }

@@ -80,17 +80,35 @@ struct TensorBSplineEval {
         bind_identity(f, *ctx.a, *ctx.geom, 0, cell);
         write_dbg(ctx.a->dbg, ctx.index, 1, 0, 0, cell);
         T acc = T(0);
+        if constexpr (F::kIsTile) {
+            // staged tile, identity frame: rows along the contiguous axis, immediate offsets
+            const T* p = f.tile + (f.a0 - DEG * (f.c0 + f.c1 + 1));
 #pragma unroll
-        for (int a0 = 0; a0 <= DEG; ++a0) {
-            T acc1 = T(0);
+            for (int a0 = 0; a0 <= DEG; ++a0) {
+                T acc1 = T(0);
 #pragma unroll
-            for (int a1 = 0; a1 <= DEG; ++a1) {
-                T acc2 = T(0);
+                for (int a1 = 0; a1 <= DEG; ++a1) {
+                    const T* row = p + a0 * f.c0 + a1 * f.c1;
+                    T acc2 = T(0);
 #pragma unroll
-                for (int a2 = 0; a2 <= DEG; ++a2) acc2 = fma(w[2][a2], f.get(a0 - DEG, a1 - DEG, a2 - DEG), acc2);
-                acc1 = fma(w[1][a1], acc2, acc1);
+                    for (int a2 = 0; a2 <= DEG; ++a2) acc2 = fma(w[2][a2], row[a2], acc2);
+                    acc1 = fma(w[1][a1], acc2, acc1);
+                }
+                acc = fma(w[0][a0], acc1, acc);
             }
-            acc = fma(w[0][a0], acc1, acc);
+        } else {
+#pragma unroll
+            for (int a0 = 0; a0 <= DEG; ++a0) {
+                T acc1 = T(0);
+#pragma unroll
+                for (int a1 = 0; a1 <= DEG; ++a1) {
+                    T acc2 = T(0);
+#pragma unroll
+                    for (int a2 = 0; a2 <= DEG; ++a2) acc2 = fma(w[2][a2], f.get(a0 - DEG, a1 - DEG, a2 - DEG), acc2);
+                    acc1 = fma(w[1][a1], acc2, acc1);
+                }
+                acc = fma(w[0][a0], acc1, acc);
+            }
         }
         return acc;
     }

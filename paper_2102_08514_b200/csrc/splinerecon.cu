@@ -418,7 +418,19 @@ int sp_eval_launch_count(const sp_plan* plan, int64_t n) { return (plan && n > 0
 
 namespace {
 
-constexpr int kTileBytes = 32 * 1024;
+constexpr int kTileBytes = 40 * 1024;
+
+// Points per thread per chunk from the point density: aim for ~256 unit cells per chunk so
+// the staged box (+ halo) stays small; 1..kMaxPPT.
+int choose_ppt(const sp_plan* p, const sp_grid_desc* g, int64_t n) {
+    double cells = 1.0;
+    for (int i = 0; i < 3; ++i) cells *= (double)g->extent[0][i] * p->diag[i];
+    const double density = (double)n / std::max(cells, 1.0);
+    const double want = 256.0 * density / sp::kThreads;
+    int ppt = 1;
+    while (ppt < sp::kMaxPPT && ppt * 2 <= want) ppt *= 2;
+    return ppt;
+}
 
 template <typename T>
 int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, void* out, int32_t* dbg,
@@ -452,8 +464,17 @@ int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     a.tables = p->d_tables;
     a.table_bytes = p->table_bytes;
     a.tile_cap = kTileBytes / (int)sizeof(T);
-    const size_t smem = (size_t)((p->table_bytes + 15) & ~15) + kTileBytes;
-    const long long nchunks = (n + sp::kChunk - 1) / sp::kChunk;
+    a.ppt = choose_ppt(p, g, n);
+    bool shifted = false;
+    for (int k = 0; k < p->M; ++k)
+        for (int i = 0; i < 3; ++i) shifted |= p->shifts[k][i] != 0;
+    // float32 points: x - l is exact in float64 and floor((x-l)/d) == floordiv(floor(x)-l, d);
+    // float64 points may round x - l, so keep one cell of slack around the staged box.
+    a.margin = (sizeof(T) == 8 && shifted) ? 1 : 0;
+    const int chunk_pts = sp::kThreads * a.ppt;
+    const size_t smem = (size_t)((p->table_bytes + 15) & ~15) + (size_t)((chunk_pts * 3 * sizeof(T) + 15) & ~15) +
+                        kTileBytes;
+    const long long nchunks = (n + chunk_pts - 1) / chunk_pts;
 
     cudaError_t e = cudaSuccess;
     int per_sm = 1;

@@ -60,7 +60,7 @@ def make(name: str, seed: int):
     ref = import_reference()
     from splineplan.lattice import decompose_cartesian, named_lattice
     from splineplan.plancompile import deserialize_plan
-    from splineplan.runtime import CoefficientGrid, PlanInterpreter, eval_bruteforce
+    from splineplan.runtime import CoefficientGrid, PlanInterpreter, eval_bruteforce, eval_bruteforce_exact
 
     t0 = time.time()
     text = open(os.path.join(PLANS, f"{name}.plan.json")).read()
@@ -113,12 +113,17 @@ def make(name: str, seed: int):
     sub = np.arange(0, n_uni, max(1, n_uni // 48))[:48]
     scalar = np.array([interp.eval(grids["zero"], list(map(float, p64[i]))) for i in sub])
     brute = np.full(sub.shape, np.nan)
+    exact = np.full(sub.shape, np.nan)
     sol = _sol(name, ref)
     if sol is not None:
         from fractions import Fraction
 
         brute = np.array(
             [eval_bruteforce(sol, grids["zero"], [Fraction(float(v)) for v in p64[i]]) for i in sub]
+        )
+        # exact rational convolution sum (runtime.py:430-439), rounded once to float64
+        exact = np.array(
+            [float(eval_bruteforce_exact(sol, grids["zero"], [Fraction(float(v)) for v in p64[i]])) for i in sub]
         )
 
     payload = dict(
@@ -134,13 +139,16 @@ def make(name: str, seed: int):
         sub=sub,
         scalar=scalar,
         brute=brute,
+        exact=exact,
         numpy_version=np.array(np.__version__),
     )
     for k, a in enumerate(arrays32):
         payload[f"coset{k}"] = a
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **payload)
     err = np.nanmax(np.abs(brute - outs["zero"][sub])) if sol is not None else float("nan")
+    errx = np.nanmax(np.abs(exact - outs["zero"][sub])) if sol is not None else float("nan")
     print(f"[{name}] {pts.shape[0]} pts, grid {[a.shape for a in arrays32]}, brute-vs-batch {err:.2e}, "
+          f"exact-vs-batch {errx:.2e}, "
           f"{time.time() - t0:.1f}s", flush=True)
 
 

@@ -2,10 +2,10 @@
 numpy oracle, through the public API (PlanInterpreter.eval_batch -> sp_eval C ABI).
 
 Tolerances (north star): bit-exact class / coset-cell selection; values within 1e-5 of
-max|f| for fp32 and 1e-12 for fp64.  The reference's fp64 batch path is itself only
-~1e-11 accurate for cc_tricubic (degree-9 monomial sums and t_num/g divisions; its
-eval_bruteforce differs by 1.1e-11 on the fixtures), so fp64 parity there is checked
-against eval_bruteforce at 1e-12 and against eval_batch at 2e-11.
+max|f| for fp32 and 1e-12 for fp64, against the reference's eval_batch and against its
+exact rational convolution sum eval_bruteforce_exact (runtime.py:430-439).  (The float
+eval_bruteforce evaluates the PP pieces in global coordinates and is only ~1e-11
+accurate for cc_tricubic, so it is not used as an fp64 pin.)
 """
 import numpy as np
 import pytest
@@ -20,7 +20,6 @@ from paper_2102_08514_b200.runtime import CoefficientGrid, PlanInterpreter, Runt
 pytestmark = pytest.mark.gpu
 
 NAMES = [n for n in golden_names() if deserialize_plan((corpus.PLAN_DIR / f"{n}.plan.json").read_text()).s == 3]
-FP64_BATCH_TOL = {"cc_tricubic": 2e-11}
 
 
 def _setup(name, boundary, dtype, device):
@@ -41,12 +40,11 @@ def test_fp64_matches_reference(name, boundary, cuda):
     got = interp.eval_batch(grid, pts).cpu().numpy()
     ref = g[f"out_{boundary}"]
     scale = max(1.0, np.abs(ref).max())
-    tol = FP64_BATCH_TOL.get(name, 1e-12)
     err = np.abs(got - ref).max() / scale
-    assert err <= tol, (name, interp.kernel_name(), err)
-    if boundary == "zero" and np.isfinite(g["brute"]).all():
-        eb = np.abs(got[g["sub"]] - g["brute"]).max() / scale
-        assert eb <= 1e-12, (name, eb)
+    assert err <= 1e-12, (name, interp.kernel_name(), err)
+    if boundary == "zero" and np.isfinite(g["exact"]).all():
+        ex = np.abs(got[g["sub"]] - g["exact"]).max() / scale
+        assert ex <= 1e-12, (name, ex)
 
 
 @pytest.mark.parametrize("name", NAMES)

@@ -71,4 +71,4 @@ def test_tricubic_fp64_full_size(cuda):
     sub = pts[idx].cpu().numpy()
     ngrid = NumpyGrid(plan.diag, plan.shifts, [a.cpu().numpy() for a in grid.arrays], grid.origins, "zero")
     ref = oracle_eval(plan, ngrid, sub, PlanTables(plan))
-    assert np.abs(out[idx].cpu().numpy() - ref).max() <= 2e-11
+    assert np.abs(out[idx].cpu().numpy() - ref).max() <= 1e-12

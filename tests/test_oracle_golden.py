@@ -55,3 +55,6 @@ def test_reference_batch_agrees_with_bruteforce_and_scalar(name):
     assert np.max(np.abs(g["scalar"] - g["out_zero"][sub])) <= 1e-9 * scale
     if np.isfinite(g["brute"]).all():
         assert np.max(np.abs(g["brute"] - g["out_zero"][sub])) <= 1e-9 * scale
+    if np.isfinite(g["exact"]).all():
+        # the exact rational convolution sum rounded once: the batch path is within ~1e-15
+        assert np.max(np.abs(g["exact"] - g["out_zero"][sub])) <= 1e-14 * scale
