@@ -201,6 +201,10 @@ constexpr int kSigmaBytes = {sig_bytes};
 {chr(10).join(kfuncs)}
 template <typename T>
 struct Eval {{
+    template <typename U>
+    static constexpr int vec_width() {{
+        return 0;
+    }}
     template <class F, class Ctx>
     __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
         const EvalArgs<T>& a = *ctx.a;

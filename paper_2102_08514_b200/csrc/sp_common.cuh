@@ -43,6 +43,7 @@ struct FrameArgs {
     int shift[SP_MAX_COSETS][3];
     int reach_lo[3];  // site reach in coset cells, relative to floor((x - l_k)/d)
     int reach_hi[3];
+    int dlog2[3];     // log2(d_i) when d_i is a power of two, else -1
 };
 
 template <typename T>
@@ -67,6 +68,8 @@ struct TileGeom {
     int off[SP_MAX_COSETS];
     int lo[SP_MAX_COSETS][3];  // box origin in coset-cell coordinates
     int ex[SP_MAX_COSETS][3];  // box extents
+    unsigned fdm[SP_MAX_COSETS][3];  // fast-division magic / shift for ex[k][1], ex[k][2]
+    unsigned fds[SP_MAX_COSETS][3];
 };
 
 __device__ __forceinline__ int floordiv_i(int a, int d) {
@@ -74,15 +77,10 @@ __device__ __forceinline__ int floordiv_i(int a, int d) {
     return (a % d != 0 && ((a < 0) != (d < 0))) ? q - 1 : q;
 }
 
-template <typename T>
-__device__ __forceinline__ int clamp_cell(T v) {
-    // floor(v) as int, clamped; NaN -> 0 (such points produce NaN outputs anyway)
-    T f = floor(v);
-    if (!(f == f)) return 0;
-    if (f > T(kCellClamp)) return kCellClamp;
-    if (f < T(-kCellClamp)) return -kCellClamp;
-    return (int)f;
-}
+// floor(v) as int, clamped to +-kCellClamp.  cvt.rmi saturates out-of-range values and maps
+// NaN to 0, so this is branch-free (non-finite points are masked out by the callers).
+__device__ __forceinline__ int clamp_cell(float v) { return min(max(__float2int_rd(v), -kCellClamp), kCellClamp); }
+__device__ __forceinline__ int clamp_cell(double v) { return min(max(__double2int_rd(v), -kCellClamp), kCellClamp); }
 
 __device__ __forceinline__ int mirror_index(int v, int n) {
     // runtime.py:191-196 (period 2n-2)
@@ -139,10 +137,11 @@ __device__ __noinline__ T policy_read_slow(const T* data, int e0, int e1, int e2
 // offsets (s0,s1,s2)/d reads coset cell  base_i + tau_i * s[rho_i].  Generated kernels call
 // get() with compile-time offsets, so the address arithmetic folds to IMADs.
 
-template <typename T>
+template <typename T, typename V = T>
 struct TileFetch {
     static constexpr bool kIsTile = true;
     const T* tile;
+    const V* vtile;  // row-vector copy of the tile (evaluators with vec_width > 0)
     int a0;
     int c0, c1, c2;
 
@@ -234,22 +233,66 @@ __device__ __forceinline__ void cp_async_elem(void* smem_dst, const void* gsrc, 
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Fast unsigned division by a runtime divisor (Granlund-Montgomery), valid for n < 2^31.
-struct FastDiv {
-    unsigned d, m, s;
-    __device__ __forceinline__ void init(unsigned div) {
-        d = div;
-        s = 0;
-        while ((1u << s) < div) ++s;
-        m = (unsigned)((((unsigned long long)1 << 32) * ((1ull << s) - div)) / div + 1);
+__device__ __forceinline__ void fastdiv_magic(unsigned div, unsigned& m, unsigned& s) {
+    s = 0;
+    while ((1u << s) < div) ++s;
+    m = (unsigned)((((unsigned long long)1 << 32) * ((1ull << s) - div)) / div + 1);
+}
+__device__ __forceinline__ unsigned fastdiv(unsigned n, unsigned m, unsigned s) { return (__umulhi(n, m) + n) >> s; }
+
+__device__ __forceinline__ int floordiv_d(int a, int d, int dlog2) {
+    return dlog2 >= 0 ? (a >> dlog2) : floordiv_i(a, d);
+}
+
+// Stage coset box [lo, lo+ex) (coset-cell coordinates) into dst with cp.async; the boundary
+// policy is resolved here (POLICY is warp-uniform), so the evaluators read unchecked.
+template <int POLICY, typename T>
+__device__ __forceinline__ void stage_box(T* dst, const T* __restrict__ base, int vol, int e1, int e2, unsigned m2,
+                                          unsigned s2, unsigned m1, unsigned s1, int z0b, int z1b, int z2b, int g0,
+                                          int g1, int g2, int tid) {
+#pragma unroll 2
+    for (int e = tid; e < vol; e += kThreads) {
+        const int r = (int)fastdiv((unsigned)e, m2, s2);
+        const int i2 = e - r * e2;
+        const int i0 = (int)fastdiv((unsigned)r, m1, s1);
+        const int i1 = r - i0 * e1;
+        int z0 = z0b + i0, z1 = z1b + i1, z2 = z2b + i2;
+        int bytes = (int)sizeof(T);
+        const bool in = (unsigned)z0 < (unsigned)g0 && (unsigned)z1 < (unsigned)g1 && (unsigned)z2 < (unsigned)g2;
+        if (POLICY == SP_ZERO) {
+            bytes = in ? bytes : 0;
+            z0 = in ? z0 : 0;
+            z1 = in ? z1 : 0;
+            z2 = in ? z2 : 0;
+        } else if (POLICY == SP_CLAMP) {
+            z0 = min(max(z0, 0), g0 - 1);
+            z1 = min(max(z1, 0), g1 - 1);
+            z2 = min(max(z2, 0), g2 - 1);
+        } else if (!in) {
+            z0 = mirror_index(z0, g0);
+            z1 = mirror_index(z1, g1);
+            z2 = mirror_index(z2, g2);
+        }
+        cp_async_elem<sizeof(T)>(dst + e, base + ((long long)z0 * g1 + z1) * (long long)g2 + z2, bytes);
     }
-    __device__ __forceinline__ unsigned div(unsigned n) const { return (__umulhi(n, m) + n) >> s; }
-};
+}
+
+template <typename T, int V>
+struct VecT;
+template <>
+struct VecT<float, 2> { using type = float2; };
+template <>
+struct VecT<float, 4> { using type = float4; };
+template <typename T>
+struct VecT<T, 0> { using type = T; };
 
 template <typename T, class Ev>
 __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ TileGeom geom;
     __shared__ int red[6];
+    constexpr int kVec = Ev::template vec_width<T>();
+    using V = typename VecT<T, kVec>::type;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -262,8 +305,10 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
     }
     const int ppt = a.ppt;
     const int chunk_pts = kThreads * ppt;
-    T* spts = reinterpret_cast<T*>(smem + tb);                        // [chunk_pts * 3]
-    T* tile = spts + ((chunk_pts * 3 * (int)sizeof(T) + 15) & ~15) / (int)sizeof(T);
+    T* spts = reinterpret_cast<T*>(smem + tb);  // [chunk_pts * 3]
+    T* tile = reinterpret_cast<T*>(smem + tb + ((chunk_pts * 3 * (int)sizeof(T) + 15) & ~15));
+    V* vtile = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(tile) +
+                                    (((a.tile_cap + 4) * (int)sizeof(T) + 15) & ~15));
 
     const long long n = a.n;
     const long long nchunks = (n + chunk_pts - 1) / chunk_pts;
@@ -276,13 +321,13 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
         {
             const T* src = a.pts + 3 * first;
             const int nel = 3 * cnt;
-            constexpr int kVec = 16 / (int)sizeof(T);
+            constexpr int kPer = 16 / (int)sizeof(T);
             if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-                const int nvec = nel / kVec;
+                const int nvec = nel / kPer;
                 const int4* s4 = reinterpret_cast<const int4*>(src);
                 int4* d4 = reinterpret_cast<int4*>(spts);
                 for (int v = tid; v < nvec; v += kThreads) d4[v] = __ldg(s4 + v);
-                for (int e = nvec * kVec + tid; e < nel; e += kThreads) spts[e] = __ldg(src + e);
+                for (int e = nvec * kPer + tid; e < nel; e += kThreads) spts[e] = __ldg(src + e);
             } else {
                 for (int e = tid; e < nel; e += kThreads) spts[e] = __ldg(src + e);
             }
@@ -291,16 +336,15 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
         else if (tid < 6) red[tid] = INT_MIN;
         __syncthreads();
 
-        // 2. bounding box of the chunk's unit cells floor(x)
+        // 2. bounding box of the chunk's (finite) unit cells floor(x)
         int lo0 = INT_MAX, lo1 = INT_MAX, lo2 = INT_MAX, hi0 = INT_MIN, hi1 = INT_MIN, hi2 = INT_MIN;
         for (int j = tid; j < cnt; j += kThreads) {
             const T x0 = spts[3 * j], x1 = spts[3 * j + 1], x2 = spts[3 * j + 2];
-            if (isfinite(x0) && isfinite(x1) && isfinite(x2)) {
-                const int f0 = clamp_cell(x0), f1 = clamp_cell(x1), f2 = clamp_cell(x2);
-                lo0 = min(lo0, f0); hi0 = max(hi0, f0);
-                lo1 = min(lo1, f1); hi1 = max(hi1, f1);
-                lo2 = min(lo2, f2); hi2 = max(hi2, f2);
-            }
+            const bool fin = isfinite(x0) && isfinite(x1) && isfinite(x2);
+            const int f0 = clamp_cell(x0), f1 = clamp_cell(x1), f2 = clamp_cell(x2);
+            lo0 = fin ? min(lo0, f0) : lo0; hi0 = fin ? max(hi0, f0) : hi0;
+            lo1 = fin ? min(lo1, f1) : lo1; hi1 = fin ? max(hi1, f1) : hi1;
+            lo2 = fin ? min(lo2, f2) : lo2; hi2 = fin ? max(hi2, f2) : hi2;
         }
         lo0 = __reduce_min_sync(0xffffffffu, lo0);
         lo1 = __reduce_min_sync(0xffffffffu, lo1);
@@ -313,75 +357,84 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
             atomicMax(&red[3], hi0); atomicMax(&red[4], hi1); atomicMax(&red[5], hi2);
         }
         __syncthreads();
-        if (tid == 0) {
-            bool ok = red[0] <= red[3] && a.tile_cap > 0;
-            long long total = 0;
-            for (int k = 0; k < M && ok; ++k) {
-                long long vol = 1;
-                for (int i = 0; i < 3; ++i) {
-                    const int d = a.fr.diag[i], l = a.fr.shift[k][i];
-                    const long long b0 = (long long)floordiv_i(red[i] - l, d) + a.fr.reach_lo[i] - a.margin;
-                    const long long b1 = (long long)floordiv_i(red[3 + i] - l, d) + a.fr.reach_hi[i] + a.margin;
-                    const long long e = b1 - b0 + 1;
-                    vol *= e;
-                    if (vol > a.tile_cap) { ok = false; break; }
-                    geom.lo[k][i] = (int)b0;
-                    geom.ex[k][i] = (int)e;
+
+        // 3. staging geometry, one lane per (coset, axis) of warp 0
+        if (tid < 32) {
+            const bool any = red[0] <= red[3];
+            long long e = 1;
+            int k = 0, i = 0;
+            if (lane < 3 * M && any) {
+                k = lane / 3;
+                i = lane - 3 * k;
+                const int d = a.fr.diag[i], l = a.fr.shift[k][i], dl = a.fr.dlog2[i];
+                const long long b0 = (long long)floordiv_d(red[i] - l, d, dl) + a.fr.reach_lo[i] - a.margin;
+                const long long b1 = (long long)floordiv_d(red[3 + i] - l, d, dl) + a.fr.reach_hi[i] + a.margin;
+                e = min(b1 - b0 + 1, (long long)(1 << 20));
+                geom.lo[k][i] = (int)b0;
+                geom.ex[k][i] = (int)e;
+                if (i > 0) {
+                    unsigned m, sh;
+                    fastdiv_magic((unsigned)e, m, sh);
+                    geom.fdm[k][i] = m;
+                    geom.fds[k][i] = sh;
                 }
-                geom.off[k] = (int)total;
-                total += vol;
-                if (total > a.tile_cap) ok = false;
             }
-            geom.staged = ok ? 1 : 0;
-            geom.total = ok ? (int)total : 0;
+            const long long e1 = __shfl_down_sync(0xffffffffu, e, 1);
+            const long long e2 = __shfl_down_sync(0xffffffffu, e, 2);
+            const long long vol = e * e1 * e2;  // meaningful on lanes 3k
+            long long total = 0, mine = 0;
+            for (int kk = 0; kk < M; ++kk) {
+                const long long v = __shfl_sync(0xffffffffu, vol, 3 * kk);
+                if (lane == 3 * kk) mine = total;
+                total += v;
+            }
+            const bool ok = any && a.tile_cap > 0 && total <= a.tile_cap;
+            if (lane < 3 * M && i == 0) geom.off[k] = (int)mine;
+            if (lane == 0) {
+                geom.staged = ok ? 1 : 0;
+                geom.total = ok ? (int)total : 0;
+            }
         }
         __syncthreads();
         const bool staged = geom.staged != 0;
 
-        // 3. stage the coefficient box (+ halo) with cp.async, boundary policy applied here
+        // 4. stage the coefficient box (+ halo) with cp.async, boundary policy applied here
         if (staged) {
             for (int k = 0; k < M; ++k) {
                 const int e1 = geom.ex[k][1], e2 = geom.ex[k][2];
                 const int vol = geom.ex[k][0] * e1 * e2;
-                T* dst = tile + geom.off[k];
                 const int z0b = geom.lo[k][0] - a.grid.org[k][0];
                 const int z1b = geom.lo[k][1] - a.grid.org[k][1];
                 const int z2b = geom.lo[k][2] - a.grid.org[k][2];
                 const int g0 = a.grid.ext[k][0], g1 = a.grid.ext[k][1], g2 = a.grid.ext[k][2];
+                T* dst = tile + geom.off[k];
                 const T* base = a.grid.data[k];
-                FastDiv fd2, fd1;
-                fd2.init((unsigned)e2);
-                fd1.init((unsigned)e1);
-#pragma unroll 4
-                for (int e = tid; e < vol; e += kThreads) {
-                    const int r = (int)fd2.div((unsigned)e);
-                    const int i2 = e - r * e2;
-                    const int i0 = (int)fd1.div((unsigned)r);
-                    const int i1 = r - i0 * e1;
-                    int z0 = z0b + i0, z1 = z1b + i1, z2 = z2b + i2;
-                    int bytes = (int)sizeof(T);
-                    if (!((unsigned)z0 < (unsigned)g0 && (unsigned)z1 < (unsigned)g1 && (unsigned)z2 < (unsigned)g2)) {
-                        if (a.grid.boundary == SP_ZERO) {
-                            bytes = 0;
-                            z0 = z1 = z2 = 0;
-                        } else if (a.grid.boundary == SP_CLAMP) {
-                            z0 = min(max(z0, 0), g0 - 1);
-                            z1 = min(max(z1, 0), g1 - 1);
-                            z2 = min(max(z2, 0), g2 - 1);
-                        } else {
-                            z0 = mirror_index(z0, g0);
-                            z1 = mirror_index(z1, g1);
-                            z2 = mirror_index(z2, g2);
-                        }
-                    }
-                    cp_async_elem<sizeof(T)>(dst + e, base + ((long long)z0 * g1 + z1) * (long long)g2 + z2, bytes);
-                }
+                const unsigned m2 = geom.fdm[k][2], s2 = geom.fds[k][2], m1 = geom.fdm[k][1], s1 = geom.fds[k][1];
+                if (a.grid.boundary == SP_ZERO)
+                    stage_box<SP_ZERO>(dst, base, vol, e1, e2, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+                else if (a.grid.boundary == SP_CLAMP)
+                    stage_box<SP_CLAMP>(dst, base, vol, e1, e2, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+                else
+                    stage_box<SP_MIRROR>(dst, base, vol, e1, e2, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
             }
             cp_async_wait_all();
+            if constexpr (kVec > 0) {
+                // row-vector layout: vtile[e] = (tile[e], ..., tile[e+kVec-1]) so a point's
+                // row of kVec taps along the contiguous axis is ONE shared-memory load
+                __syncthreads();
+                const int total = geom.total;
+                for (int e = tid; e < total; e += kThreads) {
+                    V v;
+                    T* pv = reinterpret_cast<T*>(&v);
+#pragma unroll
+                    for (int q = 0; q < kVec; ++q) pv[q] = tile[e + q];
+                    vtile[e] = v;
+                }
+            }
         }
         __syncthreads();
 
-        // 4. evaluate
+        // 5. evaluate
         EvalCtx<T, Ev> ctx;
         ctx.a = &a;
         ctx.tables = smem;
@@ -395,9 +448,10 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
             if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) {
                 v = T(NAN);
             } else if (staged) {
-                TileFetch<T> f;
+                TileFetch<T, V> f;
                 f.tile = tile;
-                v = Ev::template eval<TileFetch<T>>(x, f, ctx);
+                f.vtile = vtile;
+                v = Ev::template eval<TileFetch<T, V>>(x, f, ctx);
             } else {
                 GlobalFetch<T> f;
                 v = Ev::template eval<GlobalFetch<T>>(x, f, ctx);
@@ -409,8 +463,8 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
 }
 
 // Frame setup helpers used by the evaluators: bind a fetcher to (coset k, base, rho, tau).
-template <typename T>
-__device__ __forceinline__ void bind(TileFetch<T>& f, const EvalArgs<T>& a, const TileGeom& g, int k,
+template <typename T, typename V>
+__device__ __forceinline__ void bind(TileFetch<T, V>& f, const EvalArgs<T>& a, const TileGeom& g, int k,
                                      const int base[3], const int rho[3], const int tau[3]) {
     f.frame(g, k, base, rho, tau);
 }
@@ -419,8 +473,8 @@ __device__ __forceinline__ void bind(GlobalFetch<T>& f, const EvalArgs<T>& a, co
                                      const int base[3], const int rho[3], const int tau[3]) {
     f.frame(a.grid, k, base, rho, tau);
 }
-template <typename T>
-__device__ __forceinline__ void bind_identity(TileFetch<T>& f, const EvalArgs<T>& a, const TileGeom& g, int k,
+template <typename T, typename V>
+__device__ __forceinline__ void bind_identity(TileFetch<T, V>& f, const EvalArgs<T>& a, const TileGeom& g, int k,
                                               const int base[3]) {
     f.frame_identity(g, k, base);
 }

@@ -67,6 +67,11 @@ struct BWeights<3> {
 
 template <typename T, int DEG>
 struct TensorBSplineEval {
+    // fp32: rows of DEG+1 taps are one LDS.64 / LDS.128 from the row-vector tile
+    template <typename U>
+    static constexpr int vec_width() {
+        return sizeof(U) == 4 ? (DEG == 1 ? 2 : 4) : 0;
+    }
     template <class F, class Ctx>
     __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {
         int cell[3];
@@ -80,7 +85,24 @@ struct TensorBSplineEval {
         bind_identity(f, *ctx.a, *ctx.geom, 0, cell);
         write_dbg(ctx.a->dbg, ctx.index, 1, 0, 0, cell);
         T acc = T(0);
-        if constexpr (F::kIsTile) {
+        if constexpr (F::kIsTile && vec_width<T>() > 0) {
+            // staged row-vector tile: one vector load per (a0, a1) row
+            const auto* p = f.vtile + (f.a0 - DEG * (f.c0 + f.c1 + 1));
+#pragma unroll
+            for (int a0 = 0; a0 <= DEG; ++a0) {
+                T acc1 = T(0);
+#pragma unroll
+                for (int a1 = 0; a1 <= DEG; ++a1) {
+                    const auto q = p[a0 * f.c0 + a1 * f.c1];
+                    const T* qv = reinterpret_cast<const T*>(&q);
+                    T acc2 = T(0);
+#pragma unroll
+                    for (int a2 = 0; a2 <= DEG; ++a2) acc2 = fma(w[2][a2], qv[a2], acc2);
+                    acc1 = fma(w[1][a1], acc2, acc1);
+                }
+                acc = fma(w[0][a0], acc1, acc);
+            }
+        } else if constexpr (F::kIsTile) {
             // staged tile, identity frame: rows along the contiguous axis, immediate offsets
             const T* p = f.tile + (f.a0 - DEG * (f.c0 + f.c1 + 1));
 #pragma unroll
@@ -154,6 +176,10 @@ __device__ __forceinline__ T generic_poly(const GenericTables& gt, int p, const 
 
 template <typename T>
 struct GenericEval {
+    template <typename U>
+    static constexpr int vec_width() {
+        return 0;
+    }
     template <class F, class Ctx>
     __device__ static T eval(const T x[3], F& f, const Ctx& ctx) {
         const EvalArgs<T>& a = *ctx.a;

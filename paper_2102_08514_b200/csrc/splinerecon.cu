@@ -451,6 +451,9 @@ int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     a.fr.M = p->M;
     for (int i = 0; i < 3; ++i) {
         a.fr.diag[i] = p->diag[i];
+        a.fr.dlog2[i] = -1;
+        for (int b = 0; b < 30; ++b)
+            if ((1 << b) == p->diag[i]) a.fr.dlog2[i] = b;
         a.fr.reach_lo[i] = p->reach_lo[i];
         a.fr.reach_hi[i] = p->reach_hi[i];
     }
@@ -463,7 +466,9 @@ int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     a.err = err;
     a.tables = p->d_tables;
     a.table_bytes = p->table_bytes;
-    a.tile_cap = kTileBytes / (int)sizeof(T);
+    // row-vector tile (fp32 tensor-product kernels): +kVec*sizeof(T) bytes per tile element
+    const int vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
+    a.tile_cap = kTileBytes / (int)(sizeof(T) * (1 + vec));
     a.ppt = choose_ppt(p, g, n);
     bool shifted = false;
     for (int k = 0; k < p->M; ++k)
@@ -473,7 +478,8 @@ int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     a.margin = (sizeof(T) == 8 && shifted) ? 1 : 0;
     const int chunk_pts = sp::kThreads * a.ppt;
     const size_t smem = (size_t)((p->table_bytes + 15) & ~15) + (size_t)((chunk_pts * 3 * sizeof(T) + 15) & ~15) +
-                        kTileBytes;
+                        (size_t)((((size_t)a.tile_cap + 4) * sizeof(T) + 15) & ~(size_t)15) +
+                        (size_t)a.tile_cap * vec * sizeof(T);
     const long long nchunks = (n + chunk_pts - 1) / chunk_pts;
 
     cudaError_t e = cudaSuccess;
