@@ -124,6 +124,23 @@ const char* sp_plan_kernel_name(const sp_plan* plan);
 int sp_eval(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
             void* out, int32_t* dbg, int32_t* err_flag, void* stream);
 
+/*
+ * Brick mode (the fast path for coherent point sets).  Points sorted by sp_morton_keys are
+ * grouped into aligned bricks of (2^log2_brick)^3 unit cells; brick_start (device int64,
+ * n_bricks+1 entries) delimits each brick's run of points.  One CTA stages a brick's
+ * coefficient box (+ halo) once and evaluates all its points.  Results go to
+ * out[out_index[i]] when out_index (device int64 [n]) is given, else out[i].  Same
+ * arithmetic as sp_eval, bit-identical results.  Any brick partition is correct (points
+ * outside their run's brick are evaluated without staging).
+ */
+int sp_eval_bricks(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+                   const int64_t* brick_start, int32_t n_bricks, int32_t log2_brick, const int64_t* out_index,
+                   void* out, int32_t* err_flag, void* stream);
+
+/* Recommended log2 brick edge for a plan and dtype (largest brick whose box fits the tile),
+ * or a negative value when brick mode is not applicable. */
+int sp_brick_log2(const sp_plan* plan, int32_t dtype);
+
 /* Synchronous convenience: sp_eval + stream sync + sentinel check (SP_ERR_SENTINEL). */
 int sp_eval_sync(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
                  void* out, void* stream);
@@ -140,6 +157,11 @@ int sp_morton_keys(const void* pts, int64_t n, int32_t dtype, uint64_t* keys, vo
 int sp_scatter(const void* src, const int64_t* perm, int64_t n, int32_t dtype, void* out, void* stream);
 /* dst[i] = pts[perm[i]] (s=3 points) — gather points into sorted order. */
 int sp_gather_points(const void* pts, const int64_t* perm, int64_t n, int32_t dtype, void* dst, void* stream);
+
+/* Staging statistics for tuning (not thread-safe): copies the counters accumulated since the
+ * last call into out[4] = {staged chunks, unstaged chunks, staged tile elements, 0} (when
+ * out != NULL), then enables (1, counters reset) or disables (0) collection. */
+int sp_debug_stats(int enable, uint64_t* out);
 
 const char* sp_last_error(void);
 const char* sp_version(void);

@@ -103,6 +103,13 @@ EXPORTS = {
     "sp_gather_points": (
         ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
     ),
+    "sp_debug_stats": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p]),
+    "sp_eval_bricks": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.POINTER(GridDesc), ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+         ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
+    ),
+    "sp_brick_log2": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "sp_last_error": (ctypes.c_char_p, []),
     "sp_version": (ctypes.c_char_p, []),
 }

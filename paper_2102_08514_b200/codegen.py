@@ -263,6 +263,10 @@ extern const sp::GenEntry kGen_{ident} = {{
     &sp::launch_eval<double, sp::gen_{ident}::Eval<double>>,
     &sp::occupancy_blocks<float, sp::gen_{ident}::Eval<float>>,
     &sp::occupancy_blocks<double, sp::gen_{ident}::Eval<double>>,
+    &sp::launch_bricks<float, sp::gen_{ident}::Eval<float>>,
+    &sp::launch_bricks<double, sp::gen_{ident}::Eval<double>>,
+    &sp::occupancy_bricks<float, sp::gen_{ident}::Eval<float>>,
+    &sp::occupancy_bricks<double, sp::gen_{ident}::Eval<double>>,
 }};
 """
     return src, {"ident": ident, "flops_per_coset": kflops, "words": len(words)}

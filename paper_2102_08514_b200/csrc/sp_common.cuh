@@ -60,6 +60,8 @@ struct EvalArgs {
     int tile_cap;       // staged-tile capacity in elements
     int ppt;            // points per thread per chunk (chunk = kThreads * ppt)
     int margin;         // extra halo cells (1 for float64 points on shifted cosets, else 0)
+    unsigned long long* stats;  // nullable: [0] staged chunks, [1] unstaged chunks, [2] staged elements
+    const long long* out_index; // nullable: value of point i goes to out[out_index[i]]
 };
 
 struct TileGeom {
@@ -286,6 +288,91 @@ struct VecT<float, 4> { using type = float4; };
 template <typename T>
 struct VecT<T, 0> { using type = T; };
 
+// Staging geometry from the unit-cell bounds red[0..2] (lo) / red[3..5] (hi): per coset the
+// box of coset cells the points can read (+ plan site reach, + margin), its offset in the
+// tile, fast-division magics, and whether it fits the tile.  Called by warp 0 only.
+template <typename T>
+__device__ __forceinline__ void warp_geometry(const EvalArgs<T>& a, const int* red, TileGeom& geom, int lane) {
+    const int M = a.fr.M;
+    const bool any = red[0] <= red[3];
+    long long e = 1;
+    int k = 0, i = 0;
+    if (lane < 3 * M && any) {
+        k = lane / 3;
+        i = lane - 3 * k;
+        const int d = a.fr.diag[i], l = a.fr.shift[k][i], dl = a.fr.dlog2[i];
+        const long long b0 = (long long)floordiv_d(red[i] - l, d, dl) + a.fr.reach_lo[i] - a.margin;
+        const long long b1 = (long long)floordiv_d(red[3 + i] - l, d, dl) + a.fr.reach_hi[i] + a.margin;
+        e = min(b1 - b0 + 1, (long long)(1 << 20));
+        geom.lo[k][i] = (int)b0;
+        geom.ex[k][i] = (int)e;
+        if (i > 0) {
+            unsigned m, sh;
+            fastdiv_magic((unsigned)e, m, sh);
+            geom.fdm[k][i] = m;
+            geom.fds[k][i] = sh;
+        }
+    }
+    const long long e1 = __shfl_down_sync(0xffffffffu, e, 1);
+    const long long e2 = __shfl_down_sync(0xffffffffu, e, 2);
+    const long long vol = e * e1 * e2;  // meaningful on lanes 3k
+    long long total = 0, mine = 0;
+    for (int kk = 0; kk < M; ++kk) {
+        const long long v = __shfl_sync(0xffffffffu, vol, 3 * kk);
+        if (lane == 3 * kk) mine = total;
+        total += v;
+    }
+    const bool ok = any && a.tile_cap > 0 && total <= a.tile_cap;
+    if (lane < 3 * M && i == 0) geom.off[k] = (int)mine;
+    if (lane == 0) {
+        geom.staged = ok ? 1 : 0;
+        geom.total = ok ? (int)total : 0;
+        if (a.stats) {
+            atomicAdd(a.stats + (ok ? 0 : 1), 1ull);
+            if (ok) atomicAdd(a.stats + 2, (unsigned long long)total);
+        }
+    }
+}
+
+// Stage every coset box of `geom` into the tile (all threads), then build the row-vector
+// copy when the evaluator uses one.  Ends with the tile complete for the calling thread's
+// own copies; callers __syncthreads() before reading.
+template <typename T, int kVec, typename V>
+__device__ __forceinline__ void stage_tile(const EvalArgs<T>& a, const TileGeom& geom, T* tile, V* vtile, int tid) {
+    const int M = a.fr.M;
+    for (int k = 0; k < M; ++k) {
+        const int e1 = geom.ex[k][1], e2 = geom.ex[k][2];
+        const int vol = geom.ex[k][0] * e1 * e2;
+        const int z0b = geom.lo[k][0] - a.grid.org[k][0];
+        const int z1b = geom.lo[k][1] - a.grid.org[k][1];
+        const int z2b = geom.lo[k][2] - a.grid.org[k][2];
+        const int g0 = a.grid.ext[k][0], g1 = a.grid.ext[k][1], g2 = a.grid.ext[k][2];
+        T* dst = tile + geom.off[k];
+        const T* base = a.grid.data[k];
+        const unsigned m2 = geom.fdm[k][2], s2 = geom.fds[k][2], m1 = geom.fdm[k][1], s1 = geom.fds[k][1];
+        if (a.grid.boundary == SP_ZERO)
+            stage_box<SP_ZERO>(dst, base, vol, e1, e2, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+        else if (a.grid.boundary == SP_CLAMP)
+            stage_box<SP_CLAMP>(dst, base, vol, e1, e2, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+        else
+            stage_box<SP_MIRROR>(dst, base, vol, e1, e2, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+    }
+    cp_async_wait_all();
+    if constexpr (kVec > 0) {
+        // row-vector layout: vtile[e] = (tile[e], ..., tile[e+kVec-1]) so a point's row of
+        // kVec taps along the contiguous axis is ONE shared-memory load
+        __syncthreads();
+        const int total = geom.total;
+        for (int e = tid; e < total; e += kThreads) {
+            V v;
+            T* pv = reinterpret_cast<T*>(&v);
+#pragma unroll
+            for (int q = 0; q < kVec; ++q) pv[q] = tile[e + q];
+            vtile[e] = v;
+        }
+    }
+}
+
 template <typename T, class Ev>
 __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -359,79 +446,12 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
         __syncthreads();
 
         // 3. staging geometry, one lane per (coset, axis) of warp 0
-        if (tid < 32) {
-            const bool any = red[0] <= red[3];
-            long long e = 1;
-            int k = 0, i = 0;
-            if (lane < 3 * M && any) {
-                k = lane / 3;
-                i = lane - 3 * k;
-                const int d = a.fr.diag[i], l = a.fr.shift[k][i], dl = a.fr.dlog2[i];
-                const long long b0 = (long long)floordiv_d(red[i] - l, d, dl) + a.fr.reach_lo[i] - a.margin;
-                const long long b1 = (long long)floordiv_d(red[3 + i] - l, d, dl) + a.fr.reach_hi[i] + a.margin;
-                e = min(b1 - b0 + 1, (long long)(1 << 20));
-                geom.lo[k][i] = (int)b0;
-                geom.ex[k][i] = (int)e;
-                if (i > 0) {
-                    unsigned m, sh;
-                    fastdiv_magic((unsigned)e, m, sh);
-                    geom.fdm[k][i] = m;
-                    geom.fds[k][i] = sh;
-                }
-            }
-            const long long e1 = __shfl_down_sync(0xffffffffu, e, 1);
-            const long long e2 = __shfl_down_sync(0xffffffffu, e, 2);
-            const long long vol = e * e1 * e2;  // meaningful on lanes 3k
-            long long total = 0, mine = 0;
-            for (int kk = 0; kk < M; ++kk) {
-                const long long v = __shfl_sync(0xffffffffu, vol, 3 * kk);
-                if (lane == 3 * kk) mine = total;
-                total += v;
-            }
-            const bool ok = any && a.tile_cap > 0 && total <= a.tile_cap;
-            if (lane < 3 * M && i == 0) geom.off[k] = (int)mine;
-            if (lane == 0) {
-                geom.staged = ok ? 1 : 0;
-                geom.total = ok ? (int)total : 0;
-            }
-        }
+        if (tid < 32) warp_geometry(a, red, geom, lane);
         __syncthreads();
         const bool staged = geom.staged != 0;
 
         // 4. stage the coefficient box (+ halo) with cp.async, boundary policy applied here
-        if (staged) {
-            for (int k = 0; k < M; ++k) {
-                const int e1 = geom.ex[k][1], e2 = geom.ex[k][2];
-                const int vol = geom.ex[k][0] * e1 * e2;
-                const int z0b = geom.lo[k][0] - a.grid.org[k][0];
-                const int z1b = geom.lo[k][1] - a.grid.org[k][1];
-                const int z2b = geom.lo[k][2] - a.grid.org[k][2];
-                const int g0 = a.grid.ext[k][0], g1 = a.grid.ext[k][1], g2 = a.grid.ext[k][2];
-                T* dst = tile + geom.off[k];
-                const T* base = a.grid.data[k];
-                const unsigned m2 = geom.fdm[k][2], s2 = geom.fds[k][2], m1 = geom.fdm[k][1], s1 = geom.fds[k][1];
-                if (a.grid.boundary == SP_ZERO)
-                    stage_box<SP_ZERO>(dst, base, vol, e1, e2, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
-                else if (a.grid.boundary == SP_CLAMP)
-                    stage_box<SP_CLAMP>(dst, base, vol, e1, e2, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
-                else
-                    stage_box<SP_MIRROR>(dst, base, vol, e1, e2, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
-            }
-            cp_async_wait_all();
-            if constexpr (kVec > 0) {
-                // row-vector layout: vtile[e] = (tile[e], ..., tile[e+kVec-1]) so a point's
-                // row of kVec taps along the contiguous axis is ONE shared-memory load
-                __syncthreads();
-                const int total = geom.total;
-                for (int e = tid; e < total; e += kThreads) {
-                    V v;
-                    T* pv = reinterpret_cast<T*>(&v);
-#pragma unroll
-                    for (int q = 0; q < kVec; ++q) pv[q] = tile[e + q];
-                    vtile[e] = v;
-                }
-            }
-        }
+        if (staged) stage_tile<T, kVec>(a, geom, tile, vtile, tid);
         __syncthreads();
 
         // 5. evaluate
@@ -457,6 +477,90 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
                 v = Ev::template eval<GlobalFetch<T>>(x, f, ctx);
             }
             a.out[i] = v;
+        }
+        __syncthreads();
+    }
+}
+
+
+// ---------------------------------------------------------------------------------------
+// Brick mode: points sorted by the Morton code of their unit cell are grouped into aligned
+// bricks of B^3 unit cells (B = 2^log2b); brick_start[b]..brick_start[b+1] are brick b's
+// points.  One CTA stages one brick's coefficient box (+ halo) ONCE and evaluates all of its
+// points (thousands), so staging, geometry and barriers are amortised over the brick.
+// A point outside its run's brick (only possible for clamped/non-finite keys) takes the
+// global path.
+template <typename T, class Ev>
+__global__ void __launch_bounds__(kThreads)
+    brick_kernel(const EvalArgs<T> a, const long long* __restrict__ brick_start, int nbricks, int log2b) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ TileGeom geom;
+    __shared__ int red[6];
+    constexpr int kVec = Ev::template vec_width<T>();
+    using V = typename VecT<T, kVec>::type;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int tb = (a.table_bytes + 15) & ~15;
+    if (a.table_bytes > 0) {
+        const int4* src = reinterpret_cast<const int4*>(a.tables);
+        int4* dst = reinterpret_cast<int4*>(smem);
+        for (int i = tid; i < tb / 16; i += kThreads) dst[i] = src[i];
+    }
+    T* tile = reinterpret_cast<T*>(smem + tb);
+    V* vtile = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(tile) +
+                                    (((a.tile_cap + 4) * (int)sizeof(T) + 15) & ~15));
+    const int B = 1 << log2b;
+
+    for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
+        const long long p0 = brick_start[b], p1 = brick_start[b + 1];
+        if (tid < 32) {
+            if (lane == 0) {
+                const T* x = a.pts + 3 * p0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const int c = clamp_cell(x[i]);
+                    const int lo = (c >> log2b) << log2b;
+                    red[i] = lo;
+                    red[3 + i] = lo + B - 1;
+                }
+            }
+            __syncwarp();
+            warp_geometry(a, red, geom, lane);
+        }
+        __syncthreads();
+        const bool staged = geom.staged != 0;
+        if (staged) stage_tile<T, kVec>(a, geom, tile, vtile, tid);
+        __syncthreads();
+        const int c0 = red[0], c1 = red[1], c2 = red[2];
+
+        EvalCtx<T, Ev> ctx;
+        ctx.a = &a;
+        ctx.tables = smem;
+        ctx.geom = &geom;
+#pragma unroll 1
+        for (long long j = p0 + tid; j < p1; j += kThreads) {
+            ctx.index = j;
+            const T* px = a.pts + 3 * j;
+            const T x[3] = {__ldg(px), __ldg(px + 1), __ldg(px + 2)};
+            T v;
+            const bool fin = isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]);
+            const bool inside = (unsigned)(clamp_cell(x[0]) - c0) < (unsigned)B &&
+                                (unsigned)(clamp_cell(x[1]) - c1) < (unsigned)B &&
+                                (unsigned)(clamp_cell(x[2]) - c2) < (unsigned)B;
+            if (!fin) {
+                v = T(NAN);
+            } else if (staged && inside) {
+                TileFetch<T, V> f;
+                f.tile = tile;
+                f.vtile = vtile;
+                v = Ev::template eval<TileFetch<T, V>>(x, f, ctx);
+            } else {
+                GlobalFetch<T> f;
+                v = Ev::template eval<GlobalFetch<T>>(x, f, ctx);
+            }
+            if (a.out_index) a.out[a.out_index[j]] = v;
+            else a.out[j] = v;
         }
         __syncthreads();
     }

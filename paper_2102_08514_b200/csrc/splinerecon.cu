@@ -418,7 +418,16 @@ int sp_eval_launch_count(const sp_plan* plan, int64_t n) { return (plan && n > 0
 
 namespace {
 
-constexpr int kTileBytes = 40 * 1024;
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+// Tuning knobs (environment, read per call): SP_TILE_KB (shared-memory tile budget),
+// SP_PPT (points per thread per chunk, 0 = density-based).
+int tile_bytes() { return env_int("SP_TILE_KB", 40) * 1024; }
+
+unsigned long long* g_stats = nullptr;  // device [4] when sp_debug_stats(1) is on
 
 // Points per thread per chunk from the point density: aim for ~256 unit cells per chunk so
 // the staged box (+ halo) stays small; 1..kMaxPPT.
@@ -429,13 +438,15 @@ int choose_ppt(const sp_plan* p, const sp_grid_desc* g, int64_t n) {
     const double want = 256.0 * density / sp::kThreads;
     int ppt = 1;
     while (ppt < sp::kMaxPPT && ppt * 2 <= want) ppt *= 2;
+    const int forced = env_int("SP_PPT", 0);
+    if (forced > 0) ppt = std::min(forced, sp::kMaxPPT);
     return ppt;
 }
 
 template <typename T>
-int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, void* out, int32_t* dbg,
-               int32_t* err, cudaStream_t st) {
-    sp::EvalArgs<T> a{};
+int build_args(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, void* out, int32_t* dbg,
+               int32_t* err, sp::EvalArgs<T>& a, int& vec) {
+    a = sp::EvalArgs<T>{};
     a.grid.M = g->M;
     a.grid.boundary = g->boundary;
     for (int k = 0; k < g->M; ++k) {
@@ -466,9 +477,10 @@ int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     a.err = err;
     a.tables = p->d_tables;
     a.table_bytes = p->table_bytes;
-    // row-vector tile (fp32 tensor-product kernels): +kVec*sizeof(T) bytes per tile element
-    const int vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
-    a.tile_cap = kTileBytes / (int)(sizeof(T) * (1 + vec));
+    // row-vector tile (fp32 tensor-product kernels): +vec*sizeof(T) bytes per tile element
+    vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
+    a.tile_cap = tile_bytes() / (int)(sizeof(T) * (1 + vec));
+    a.stats = g_stats;
     a.ppt = choose_ppt(p, g, n);
     bool shifted = false;
     for (int k = 0; k < p->M; ++k)
@@ -476,32 +488,117 @@ int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     // float32 points: x - l is exact in float64 and floor((x-l)/d) == floordiv(floor(x)-l, d);
     // float64 points may round x - l, so keep one cell of slack around the staged box.
     a.margin = (sizeof(T) == 8 && shifted) ? 1 : 0;
-    const int chunk_pts = sp::kThreads * a.ppt;
-    const size_t smem = (size_t)((p->table_bytes + 15) & ~15) + (size_t)((chunk_pts * 3 * sizeof(T) + 15) & ~15) +
-                        (size_t)((((size_t)a.tile_cap + 4) * sizeof(T) + 15) & ~(size_t)15) +
-                        (size_t)a.tile_cap * vec * sizeof(T);
-    const long long nchunks = (n + chunk_pts - 1) / chunk_pts;
+    return SP_OK;
+}
 
-    cudaError_t e = cudaSuccess;
-    int per_sm = 1;
-    sp::LaunchFn<T> fn = nullptr;
+template <typename T>
+size_t tile_smem(const sp::EvalArgs<T>& a, int vec, size_t esz) {
+    return (size_t)((a.table_bytes + 15) & ~15) + ((((size_t)a.tile_cap + 4) * esz + 15) & ~(size_t)15) +
+           (size_t)a.tile_cap * vec * esz;
+}
+
+template <typename T>
+struct Kernels {
+    sp::LaunchFn<T> chunk = nullptr;
+    sp::BrickLaunchFn<T> brick = nullptr;
+    int (*occ)(size_t) = nullptr;
+    int (*bocc)(size_t) = nullptr;
+};
+
+template <typename T, class Ev>
+Kernels<T> kernels_of() {
+    Kernels<T> k;
+    k.chunk = &sp::launch_eval<T, Ev>;
+    k.brick = &sp::launch_bricks<T, Ev>;
+    k.occ = &sp::occupancy_blocks<T, Ev>;
+    k.bocc = &sp::occupancy_bricks<T, Ev>;
+    return k;
+}
+
+template <typename T>
+int select_kernels(const sp_plan* p, Kernels<T>& k) {
     if (p->kind == SP_KIND_TENSOR_BSPLINE) {
         switch (p->tp_degree) {
-            case 1: fn = &sp::launch_eval<T, sp::TensorBSplineEval<T, 1>>; per_sm = sp::occupancy_blocks<T, sp::TensorBSplineEval<T, 1>>(smem); break;
-            case 2: fn = &sp::launch_eval<T, sp::TensorBSplineEval<T, 2>>; per_sm = sp::occupancy_blocks<T, sp::TensorBSplineEval<T, 2>>(smem); break;
-            case 3: fn = &sp::launch_eval<T, sp::TensorBSplineEval<T, 3>>; per_sm = sp::occupancy_blocks<T, sp::TensorBSplineEval<T, 3>>(smem); break;
+            case 1: k = kernels_of<T, sp::TensorBSplineEval<T, 1>>(); return SP_OK;
+            case 2: k = kernels_of<T, sp::TensorBSplineEval<T, 2>>(); return SP_OK;
+            case 3: k = kernels_of<T, sp::TensorBSplineEval<T, 3>>(); return SP_OK;
             default: return fail(SP_ERR_UNSUPPORTED, "tensor degree");
         }
-    } else if (p->kind == SP_KIND_GENERATED) {
-        if constexpr (sizeof(T) == 4) { fn = p->gen->launch_f32; per_sm = p->gen->occ_f32(smem); }
-        else { fn = p->gen->launch_f64; per_sm = p->gen->occ_f64(smem); }
-    } else {
-        fn = &sp::launch_eval<T, sp::GenericEval<T>>;
-        per_sm = sp::occupancy_blocks<T, sp::GenericEval<T>>(smem);
     }
-    const long long cap = (long long)p->num_sms * per_sm;
+    if (p->kind == SP_KIND_GENERATED) {
+        if constexpr (sizeof(T) == 4) {
+            k.chunk = p->gen->launch_f32; k.occ = p->gen->occ_f32; k.brick = p->gen->brick_f32; k.bocc = p->gen->bocc_f32;
+        } else {
+            k.chunk = p->gen->launch_f64; k.occ = p->gen->occ_f64; k.brick = p->gen->brick_f64; k.bocc = p->gen->bocc_f64;
+        }
+        return SP_OK;
+    }
+    k = kernels_of<T, sp::GenericEval<T>>();
+    return SP_OK;
+}
+
+template <typename T>
+int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, void* out, int32_t* dbg,
+               int32_t* err, cudaStream_t st) {
+    sp::EvalArgs<T> a;
+    int vec = 0;
+    int rc = build_args<T>(p, g, pts, n, out, dbg, err, a, vec);
+    if (rc != SP_OK) return rc;
+    Kernels<T> k;
+    if ((rc = select_kernels<T>(p, k)) != SP_OK) return rc;
+    const int chunk_pts = sp::kThreads * a.ppt;
+    const size_t smem = tile_smem(a, vec, sizeof(T)) +
+                        (size_t)((chunk_pts * 3 * sizeof(T) + 15) & ~15);
+    const long long nchunks = (n + chunk_pts - 1) / chunk_pts;
+    const long long cap = (long long)p->num_sms * k.occ(smem);
     const int blocks = (int)std::max<long long>(1, std::min<long long>(nchunks, cap));
-    e = fn(a, blocks, smem, st);
+    cudaError_t e = k.chunk(a, blocks, smem, st);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return SP_OK;
+}
+
+// Largest brick edge 2^b (unit cells) whose staged box (all cosets, + reach, + margin) fits
+// the tile; -1 when even 4^3 bricks do not fit.
+template <typename T>
+int brick_log2_typed(const sp_plan* p) {
+    const int vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
+    const long long cap = tile_bytes() / (long long)(sizeof(T) * (1 + vec));
+    bool shifted = false;
+    for (int k = 0; k < p->M; ++k)
+        for (int i = 0; i < 3; ++i) shifted |= p->shifts[k][i] != 0;
+    const int margin = (sizeof(T) == 8 && shifted) ? 1 : 0;
+    for (int b = 6; b >= 2; --b) {
+        const int B = 1 << b;
+        long long total = 0;
+        for (int k = 0; k < p->M; ++k) {
+            long long vol = 1;
+            for (int i = 0; i < 3; ++i) {
+                const int d = p->diag[i];
+                const long long ext = (B + d - 1) / d + 1 + (p->reach_hi[i] - p->reach_lo[i]) + 2 * margin;
+                vol *= ext;
+            }
+            total += vol;
+        }
+        if (total <= cap) return b;
+    }
+    return -1;
+}
+
+template <typename T>
+int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, const int64_t* bstart,
+                      int32_t nbricks, int32_t log2b, const int64_t* out_index, void* out, int32_t* err,
+                      cudaStream_t st) {
+    sp::EvalArgs<T> a;
+    int vec = 0;
+    int rc = build_args<T>(p, g, pts, n, out, nullptr, err, a, vec);
+    if (rc != SP_OK) return rc;
+    a.out_index = reinterpret_cast<const long long*>(out_index);
+    Kernels<T> k;
+    if ((rc = select_kernels<T>(p, k)) != SP_OK) return rc;
+    const size_t smem = tile_smem(a, vec, sizeof(T));
+    const long long cap = (long long)p->num_sms * k.bocc(smem);
+    const int blocks = (int)std::max<long long>(1, std::min<long long>(nbricks, cap));
+    cudaError_t e = k.brick(a, reinterpret_cast<const long long*>(bstart), nbricks, log2b, blocks, smem, st);
     if (e != cudaSuccess) return fail(SP_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
     return SP_OK;
 }
@@ -532,6 +629,50 @@ extern "C" int sp_eval(const sp_plan* plan, const sp_grid_desc* grid, const void
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (dtype == SP_F32) return eval_typed<float>(plan, grid, pts, n, out, dbg, err_flag, st);
     if (dtype == SP_F64) return eval_typed<double>(plan, grid, pts, n, out, dbg, err_flag, st);
+    return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+extern "C" int sp_debug_stats(int enable, uint64_t* out) {
+    if (out) {
+        if (g_stats) {
+            SP_CUDA(cudaMemcpy(out, g_stats, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        } else {
+            for (int i = 0; i < 4; ++i) out[i] = 0;
+        }
+    }
+    if (enable && !g_stats) {
+        SP_CUDA(cudaMalloc(&g_stats, 4 * sizeof(unsigned long long)));
+    }
+    if (enable) SP_CUDA(cudaMemset(g_stats, 0, 4 * sizeof(unsigned long long)));
+    if (!enable && g_stats) {
+        cudaFree(g_stats);
+        g_stats = nullptr;
+    }
+    return SP_OK;
+}
+
+extern "C" int sp_brick_log2(const sp_plan* plan, int32_t dtype) {
+    if (!plan) return fail(SP_ERR_INVALID, "null plan");
+    if (dtype == SP_F32) return brick_log2_typed<float>(plan);
+    if (dtype == SP_F64) return brick_log2_typed<double>(plan);
+    return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+extern "C" int sp_eval_bricks(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+                              const int64_t* brick_start, int32_t n_bricks, int32_t log2_brick,
+                              const int64_t* out_index, void* out, int32_t* err_flag, void* stream) {
+    if (!plan) return fail(SP_ERR_INVALID, "null plan");
+    int rc = check_grid(plan, grid, dtype);
+    if (rc != SP_OK) return rc;
+    if (n < 0 || n_bricks < 0) return fail(SP_ERR_INVALID, "negative size");
+    if (n == 0 || n_bricks == 0) return SP_OK;
+    if (log2_brick < 0 || log2_brick > 20) return fail(SP_ERR_INVALID, "log2_brick out of range");
+    if (!pts || !out || !brick_start) return fail(SP_ERR_INVALID, "null points, output or brick_start");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32)
+        return eval_bricks_typed<float>(plan, grid, pts, n, brick_start, n_bricks, log2_brick, out_index, out, err_flag, st);
+    if (dtype == SP_F64)
+        return eval_bricks_typed<double>(plan, grid, pts, n, brick_start, n_bricks, log2_brick, out_index, out, err_flag, st);
     return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
 }
 

@@ -249,6 +249,19 @@ class PlanInterpreter:
         except Exception:
             pass
 
+    def brick_log2(self, grid: CoefficientGrid) -> int:
+        """Recommended brick edge (log2 unit cells) for this plan and the grid's dtype."""
+        dtype = _native.SP_F32 if grid.dtype == torch.float32 else _native.SP_F64
+        return int(_native.lib().sp_brick_log2(self._handle(grid.device), dtype))
+
+    def prepare(self, grid: CoefficientGrid, pts: torch.Tensor, *, presorted: bool = False) -> "PointBatch":
+        """Brick-order a point set for repeated evaluation on this plan/grid."""
+        b = self.brick_log2(grid)
+        if b < 0:
+            raise RuntimeError_("brick mode is not applicable to this plan")
+        p = pts.to(device=grid.device, dtype=grid.dtype)
+        return prepare_points(p, b, presorted=presorted)
+
     def kernel_name(self, device=None) -> str:
         device = torch.device(device) if device is not None else _default_device()
         return _native.lib().sp_plan_kernel_name(self._handle(device)).decode()
@@ -280,6 +293,8 @@ class PlanInterpreter:
         self._check_grid(grid)
         if self.mode != "float":
             raise RuntimeError_("batch evaluation is float-mode only")
+        if isinstance(pts, PointBatch):
+            return self._eval_bricks(grid, pts, out=out, check=check, stream=stream)
         is_numpy = not isinstance(pts, torch.Tensor)
         dev = grid.device
         if dev.type != "cuda":
@@ -308,6 +323,31 @@ class PlanInterpreter:
             return res.to("cpu")
         return res
 
+    def _eval_bricks(self, grid, batch: "PointBatch", *, out=None, check=True, stream=None, unpermute=True):
+        """Brick-mode evaluation (sp_eval_bricks).  Results are returned in the caller's
+        original order (batch.perm scatter fused into the kernel) unless unpermute=False."""
+        lib = _native.lib()
+        dev = grid.device
+        if batch.pts.device != dev or batch.pts.dtype != grid.dtype:
+            raise RuntimeError_("batch points must be on the grid's device with the grid's dtype")
+        h = self._handle(dev)
+        gdesc = grid.descriptor()
+        dtype = _native.SP_F32 if grid.dtype == torch.float32 else _native.SP_F64
+        n = batch.n
+        res = out if out is not None else torch.empty(n, dtype=grid.dtype, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev) if check else None
+        idx = batch.perm if (unpermute and batch.perm is not None) else None
+        if n:
+            with torch.cuda.stream(st):
+                _native.check(lib.sp_eval_bricks(h, ctypes.byref(gdesc), batch.pts.data_ptr(), n, dtype,
+                                                 batch.brick_start.data_ptr(), batch.n_bricks, batch.log2_brick,
+                                                 None if idx is None else idx.data_ptr(), res.data_ptr(),
+                                                 None if err is None else err.data_ptr(), st.cuda_stream))
+        if check and int(err.item()):
+            raise RuntimeError_("sigma sentinel hit in batch evaluation")
+        return res
+
     def classify(self, grid: CoefficientGrid, pts: torch.Tensor):
         """Per point and coset: class id and coset cell kk/d (runtime.py:371-379), as
         computed by the evaluation kernel itself.  Returns (classes (n,M), cells (n,M,s))."""
@@ -329,6 +369,11 @@ class PlanInterpreter:
         st = stream if stream is not None else torch.cuda.current_stream(grid.device)
         err = torch.zeros(1, dtype=torch.int32, device=grid.device) if check else None
         n = p.shape[0]
+        b = self.brick_log2(grid) if (reorder and dbg is None) else -1
+        if b >= 0:
+            batch = prepare_points(p, b, stream=st)
+            self._eval_bricks(grid, batch, out=res, check=check, stream=st)
+            return
         with torch.cuda.stream(st):
             if reorder:
                 perm = morton_order(p, stream=st)
@@ -350,6 +395,59 @@ class PlanInterpreter:
 def eval_plan(interp: PlanInterpreter, grid: CoefficientGrid, x: Sequence) -> float:
     """runtime.py:275-276."""
     return interp.eval(grid, x)
+
+
+class PointBatch:
+    """Query points in brick order: the input layout of the brick-mode kernel.
+
+    `pts` are sorted by the Morton code of their unit cell floor(x), so points of each
+    aligned brick of (2^log2_brick)^3 unit cells are contiguous; `brick_start[b]` ..
+    `brick_start[b+1]` is brick b's run.  `perm[i]` is the caller's index of sorted point i
+    (None when the points were already presented in this order).  Build one with
+    `prepare_points`; evaluate with `PlanInterpreter.eval_batch(grid, batch)`.
+    """
+
+    def __init__(self, pts: torch.Tensor, brick_start: torch.Tensor, log2_brick: int, perm: torch.Tensor | None):
+        self.pts = pts
+        self.brick_start = brick_start
+        self.log2_brick = int(log2_brick)
+        self.perm = perm
+
+    @property
+    def n(self) -> int:
+        return self.pts.shape[0]
+
+    @property
+    def n_bricks(self) -> int:
+        return self.brick_start.shape[0] - 1
+
+
+def prepare_points(pts: torch.Tensor, log2_brick: int, *, presorted: bool = False,
+                   stream: torch.cuda.Stream | None = None) -> PointBatch:
+    """Morton-sort points (GPU) and delimit their bricks.  With presorted=True the points
+    are taken to be in Morton order already (input-order protocol A) and only the brick
+    runs are found."""
+    lib = _native.lib()
+    st = stream if stream is not None else torch.cuda.current_stream(pts.device)
+    pts = pts.contiguous()
+    n = pts.shape[0]
+    dtype = _native.SP_F32 if pts.dtype == torch.float32 else _native.SP_F64
+    keys = torch.empty(n, dtype=torch.int64, device=pts.device)
+    with torch.cuda.stream(st):
+        _native.check(lib.sp_morton_keys(pts.data_ptr(), n, dtype, keys.data_ptr(), st.cuda_stream))
+        perm = None
+        if not presorted:
+            keys, perm = torch.sort(keys)
+            sp = torch.empty_like(pts)
+            _native.check(lib.sp_gather_points(pts.data_ptr(), perm.data_ptr(), n, dtype, sp.data_ptr(), st.cuda_stream))
+            pts = sp
+        bid = keys >> (3 * int(log2_brick))
+        if presorted and n > 1 and bool((bid[1:] < bid[:-1]).any()):
+            raise RuntimeError_("points are not in Morton order (use presorted=False)")
+        _, counts = torch.unique_consecutive(bid, return_counts=True)
+        start = torch.zeros(counts.shape[0] + 1, dtype=torch.int64, device=pts.device)
+        torch.cumsum(counts, 0, out=start[1:])
+    return PointBatch(pts, start, log2_brick, perm)
 
 
 def morton_order(pts: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:

@@ -20,10 +20,13 @@ def main():
     ap.add_argument("--points", type=int, default=None)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--order", default="morton")
+    ap.add_argument("--mode", default="brick", choices=["brick", "chunk"])
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     plan, grid, pts, interp = bench.make_workload(a.workload, 0, dev, order=a.order, n_override=a.points)
     out = torch.empty(pts.shape[0], dtype=grid.dtype, device=dev)
+    if a.mode == "brick":
+        pts = interp.prepare(grid, pts, presorted=(a.order == "morton"))
     for _ in range(a.iters):
         interp.eval_batch(grid, pts, out=out, check=False)
     torch.cuda.synchronize()
@@ -34,7 +37,21 @@ def main():
     end.record()
     torch.cuda.synchronize()
     ms = start.elapsed_time(end) / a.iters
-    print(f"{a.workload} kernel={interp.kernel_name()} n={pts.shape[0]} {ms:.3f} ms  {pts.shape[0] / ms / 1e6:.2f} Gpts/s")
+    import ctypes
+
+    from paper_2102_08514_b200 import _native
+
+    lib = _native.lib()
+    buf = (ctypes.c_uint64 * 4)()
+    lib.sp_debug_stats(1, None)
+    interp.eval_batch(grid, pts, out=out, check=False)
+    torch.cuda.synchronize()
+    lib.sp_debug_stats(0, buf)
+    st, un, el = buf[0], buf[1], buf[2]
+    n = out.shape[0]
+    print(f"{a.workload} [{a.mode}] kernel={interp.kernel_name()} n={n} {ms:.3f} ms  "
+          f"{n / ms / 1e6:.2f} Gpts/s  staged={st} unstaged={un} "
+          f"elems/pt={el / max(1, n):.2f} env=({os.environ.get('SP_PPT', '-')},{os.environ.get('SP_TILE_KB', '-')})")
 
 
 if __name__ == "__main__":
