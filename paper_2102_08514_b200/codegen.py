@@ -37,8 +37,8 @@ from .plan import EvaluationPlan
 def codegen_supported(plan: EvaluationPlan) -> bool:
     if plan.s != 3 or plan.M > 8 or plan.Q > 31 or plan.K > 15:
         return False
-    if len(set(plan.diag)) != 1:
-        return False
+    if len(set(plan.diag)) != 1 or plan.diag[0] & (plan.diag[0] - 1):
+        return False  # uniform power-of-two diagonal: x * (1/d) is exact
     if plan.tensor_bspline_degree() is not None:
         return False
     recs = plan.signed_permutation_classes()
@@ -176,6 +176,8 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
         kfuncs.append("")
         kflops.append(fl)
     sig_bytes = ((plan.r * 4) + 15) & ~15
+    # occupancy hint for ptxas: light weight programs keep 4 CTAs (<= 64 regs) per SM
+    min_blocks = 4 if max(kflops) <= 64 else (2 if max(kflops) <= 700 else 1)
     planes = []
     for j, (n, off) in enumerate(plan.planes):
         planes.append(f"            q |= ({_plane_expr(n)} >= {float(off)!r}) ? {1 << j} : 0;")
@@ -196,11 +198,15 @@ namespace gen_{ident} {{
 
 constexpr int kM = {plan.M};
 constexpr int kR = {plan.r};
+constexpr double kD = {float(d)!r};
+constexpr double kInvD = {1.0 / d!r};
+__device__ constexpr double kShift[kM][3] = {{{", ".join("{" + ", ".join(repr(float(v)) for v in sh) + "}" for sh in plan.shifts)}}};
 constexpr int kSigmaBytes = {sig_bytes};
 
 {chr(10).join(kfuncs)}
 template <typename T>
 struct Eval {{
+    static constexpr int kMinBlocks = {min_blocks};
     template <typename U>
     static constexpr int vec_width() {{
         return 0;
@@ -213,8 +219,22 @@ struct Eval {{
         T total = T(0);
 #pragma unroll
         for (int k = 0; k < kM; ++k) {{
-            const CosetFrame cf = coset_frame(x, a.fr, k);
-            const double xp0 = cf.xp[0], xp1 = cf.xp[1], xp2 = cf.xp[2];
+            // coset frame, runtime.py:371-373 in float64: xl = x - l_k; kk = floor(xl/d)*d
+            // (d is a power of two here, so xl * (1/d) == xl / d exactly)
+            double xp0, xp1, xp2;
+            int cell[3];
+            {{
+                const double xl0 = (double)x[0] - kShift[k][0];
+                const double xl1 = (double)x[1] - kShift[k][1];
+                const double xl2 = (double)x[2] - kShift[k][2];
+                const double q0 = floor(xl0 * kInvD), q1 = floor(xl1 * kInvD), q2 = floor(xl2 * kInvD);
+                xp0 = xl0 - q0 * kD;
+                xp1 = xl1 - q1 * kD;
+                xp2 = xl2 - q2 * kD;
+                cell[0] = clamp_cell(q0);
+                cell[1] = clamp_cell(q1);
+                cell[2] = clamp_cell(q2);
+            }}
             int q = 0;
 {chr(10).join(planes)}
             int c = sigma[q % kR];
@@ -222,7 +242,7 @@ struct Eval {{
                 if (a.err) atomicOr(a.err, 1);
                 c = 0;
             }}
-            write_dbg(a.dbg, ctx.index, kM, k, c, cf.cell);
+            write_dbg(a.dbg, ctx.index, kM, k, c, cell);
             const uint4 rec = cls_tab[c];
             const int kern = (int)(rec.x & 15u);
             (void)kern;
@@ -237,7 +257,7 @@ struct Eval {{
                 const int ti = (int)((rec.y >> (8 * i)) & 255u) - 128;
                 const int pb = (int)((rec.z >> (8 * i)) & 255u) - 128;
                 yv[i] = sg * sel3(perm, xp0, xp1, xp2) - (double)ti;
-                base[i] = cf.cell[i] + pb;
+                base[i] = cell[i] + pb;
             }}
             const T y0 = (T)yv[0], y1 = (T)yv[1], y2 = (T)yv[2];
             bind(f, a, *ctx.geom, k, base, rho, tau);

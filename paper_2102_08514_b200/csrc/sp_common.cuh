@@ -374,7 +374,7 @@ __device__ __forceinline__ void stage_tile(const EvalArgs<T>& a, const TileGeom&
 }
 
 template <typename T, class Ev>
-__global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const EvalArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ TileGeom geom;
     __shared__ int red[6];
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const EvalArgs<T> a) {
 // A point outside its run's brick (only possible for clamped/non-finite keys) takes the
 // global path.
 template <typename T, class Ev>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     brick_kernel(const EvalArgs<T> a, const long long* __restrict__ brick_start, int nbricks, int log2b) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ TileGeom geom;
@@ -538,11 +538,24 @@ __global__ void __launch_bounds__(kThreads)
         ctx.a = &a;
         ctx.tables = smem;
         ctx.geom = &geom;
+        // software-pipelined point loads: the next point is in flight while this one is evaluated
+        T xn0 = T(0), xn1 = T(0), xn2 = T(0);
+        if (p0 + tid < p1) {
+            const T* px = a.pts + 3 * (p0 + tid);
+            xn0 = __ldg(px);
+            xn1 = __ldg(px + 1);
+            xn2 = __ldg(px + 2);
+        }
 #pragma unroll 1
         for (long long j = p0 + tid; j < p1; j += kThreads) {
             ctx.index = j;
-            const T* px = a.pts + 3 * j;
-            const T x[3] = {__ldg(px), __ldg(px + 1), __ldg(px + 2)};
+            const T x[3] = {xn0, xn1, xn2};
+            if (j + kThreads < p1) {
+                const T* px = a.pts + 3 * (j + kThreads);
+                xn0 = __ldg(px);
+                xn1 = __ldg(px + 1);
+                xn2 = __ldg(px + 2);
+            }
             T v;
             const bool fin = isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]);
             const bool inside = (unsigned)(clamp_cell(x[0]) - c0) < (unsigned)B &&
@@ -603,7 +616,8 @@ __device__ __forceinline__ CosetFrame coset_frame(const T x[3], const FrameArgs&
     for (int i = 0; i < 3; ++i) {
         const double d = (double)fr.diag[i];
         const double xl = (double)x[i] - (double)fr.shift[k][i];
-        const double q = floor(xl / d);
+        // power-of-two d: multiplying by 1/d is exact and avoids the float64 division
+        const double q = fr.dlog2[i] >= 0 ? floor(xl * ldexp(1.0, -fr.dlog2[i])) : floor(xl / d);
         const double kk = q * d;
         c.xp[i] = xl - kk;
         c.cell[i] = clamp_cell(q);

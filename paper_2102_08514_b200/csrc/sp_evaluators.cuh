@@ -67,6 +67,7 @@ struct BWeights<3> {
 
 template <typename T, int DEG>
 struct TensorBSplineEval {
+    static constexpr int kMinBlocks = sizeof(T) == 4 ? 4 : 3;  // <= 64 / 80 registers
     // fp32: rows of DEG+1 taps are one LDS.64 / LDS.128 from the row-vector tile
     template <typename U>
     static constexpr int vec_width() {
@@ -176,6 +177,7 @@ __device__ __forceinline__ T generic_poly(const GenericTables& gt, int p, const 
 
 template <typename T>
 struct GenericEval {
+    static constexpr int kMinBlocks = 1;
     template <typename U>
     static constexpr int vec_width() {
         return 0;

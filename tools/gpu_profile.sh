@@ -4,6 +4,6 @@
 W=${1:-tricubic_cc256_fp32}; TAG=${2:-prof}; P=${3:-20000000}
 mkdir -p gpurun_out
 python tools/prof_eval.py --workload $W --points $P --iters 2 > gpurun_out/${TAG}_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 2 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"eval_kernel|brick_kernel" -s 2 -c 1 \
     -o gpurun_out/${TAG} python tools/prof_eval.py --workload $W --points $P --iters 2 > gpurun_out/${TAG}_ncu.log 2>&1
 echo "profile rc=$?"
