@@ -281,14 +281,19 @@ class PlanInterpreter:
         return float(self.eval_batch(grid, pts)[0])
 
     def eval_batch(self, grid: CoefficientGrid, pts, *, out: torch.Tensor | None = None, check: bool = True,
-                   reorder: bool = False, stream: torch.cuda.Stream | None = None):
+                   order: str = "given", reorder: bool = False, stream: torch.cuda.Stream | None = None):
         """Batch reconstruction (runtime.py:244-248).
 
-        pts: (n, s) numpy array (-> numpy float64 result, like the reference) or tensor
-        (-> tensor of the grid dtype on the grid device).  `check` synchronises and
-        raises RuntimeError_ on a sigma-sentinel hit (runtime.py:380-381); `reorder`
-        Morton-sorts the points on the GPU first (same results, faster for incoherent
-        point order on large batches).
+        pts: (n, s) numpy array (-> numpy float64 result, like the reference), tensor
+        (CUDA -> CUDA tensor of the grid dtype; CPU -> CPU tensor, copies included) or a
+        PointBatch.  `check` synchronises and raises RuntimeError_ on a sigma-sentinel
+        hit (runtime.py:380-381).  `order` says how the points are presented:
+          "given"  any order; chunk kernel with per-chunk staging (default),
+          "morton" already in Morton order of floor(x) (input-order protocol A): the
+                   brick runs are found and the brick kernel is used,
+          "sort"   Morton-sort on the GPU, brick kernel, results scattered back to the
+                   caller's order (protocol B; `reorder=True` is an alias).
+        All three give bit-identical values.
         """
         self._check_grid(grid)
         if self.mode != "float":
@@ -312,8 +317,12 @@ class PlanInterpreter:
             raise RuntimeError_(f"points must have shape (n, {self.plan.s})")
         n = p.shape[0]
         res = out if (out is not None and out.device == dev) else torch.empty(n, dtype=grid.dtype, device=dev)
+        if order not in ("given", "morton", "sort"):
+            raise RuntimeError_(f"unknown point order {order!r}")
+        if reorder:
+            order = "sort"
         if n:
-            self._launch(grid, p, res, check=check, reorder=reorder, stream=stream)
+            self._launch(grid, p, res, check=check, order=order, stream=stream)
         if is_numpy:
             return res.to("cpu").numpy().astype(np.float64)
         if on_host:
@@ -361,7 +370,7 @@ class PlanInterpreter:
             self._launch(grid, p, res, dbg=dbg, check=False)
         return dbg[:, :, 0].to(torch.int64), dbg[:, :, 1:].to(torch.int64)
 
-    def _launch(self, grid, p, res, *, dbg=None, check=True, reorder=False, stream=None):
+    def _launch(self, grid, p, res, *, dbg=None, check=True, order="given", stream=None):
         lib = _native.lib()
         h = self._handle(grid.device)
         gdesc = grid.descriptor()
@@ -369,13 +378,13 @@ class PlanInterpreter:
         st = stream if stream is not None else torch.cuda.current_stream(grid.device)
         err = torch.zeros(1, dtype=torch.int32, device=grid.device) if check else None
         n = p.shape[0]
-        b = self.brick_log2(grid) if (reorder and dbg is None) else -1
+        b = self.brick_log2(grid) if (order != "given" and dbg is None) else -1
         if b >= 0:
-            batch = prepare_points(p, b, stream=st)
+            batch = prepare_points(p, b, presorted=(order == "morton"), stream=st)
             self._eval_bricks(grid, batch, out=res, check=check, stream=st)
             return
         with torch.cuda.stream(st):
-            if reorder:
+            if order == "sort":
                 perm = morton_order(p, stream=st)
                 ps = torch.empty_like(p)
                 _native.check(lib.sp_gather_points(p.data_ptr(), perm.data_ptr(), n, dtype, ps.data_ptr(), st.cuda_stream))
