@@ -151,7 +151,7 @@ def _plane_expr(normal) -> str:
         elif n == -1:
             terms.append(f"(-xp{i})")
         else:
-            terms.append(f"({float(n)!r} * xp{i})")
+            terms.append(f"(R({float(n)!r}) * xp{i})")
     if not terms:
         return "0.0"
     expr = terms[0]
@@ -180,7 +180,14 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
     min_blocks = 4 if max(kflops) <= 64 else (2 if max(kflops) <= 700 else 1)
     planes = []
     for j, (n, off) in enumerate(plan.planes):
-        planes.append(f"            q |= ({_plane_expr(n)} >= {float(off)!r}) ? {1 << j} : 0;")
+        planes.append(f"    q |= ({_plane_expr(n)} >= R({float(off)!r})) ? {1 << j} : 0;")
+    # float32 exactness threshold: partial plane sums are bounded by R = max_j sum_i |n_ji| d
+    # and are multiples of ulp(lo) = lo * 2^-23, so they are exact when R <= 2 lo; the frame
+    # x - l, x/d, x - kk is exact for |x| >= max(1, d)
+    rmax = max([sum(abs(v) for v in n) * d for n, _ in plan.planes] + [1])
+    fast_lo = 1.0
+    while fast_lo < max(rmax / 2.0, float(d), 1.0):
+        fast_lo *= 2.0
     if plan.K == 1:
         dispatch = "            const T acc = kernel0<T>(y0, y1, y2, f);"
     else:
@@ -204,6 +211,49 @@ __device__ constexpr double kShift[kM][3] = {{{", ".join("{" + ", ".join(repr(fl
 constexpr int kSigmaBytes = {sig_bytes};
 
 {chr(10).join(kfuncs)}
+// float32 fast path: for |x_i| in [kFastLo, 2^22) the coset frame and the plane sums are
+// exact in float32 (every partial sum is a multiple of ulp(kFastLo) below 2*kFastLo*2^23),
+// so the classification equals the float64 one bit for bit; other points use float64.
+constexpr float kFastLo = {fast_lo!r}f;
+constexpr float kFastHi = 4194304.0f;
+constexpr int kN = {plan.N};
+
+template <typename R>
+__device__ __forceinline__ int plane_code(const R xp0, const R xp1, const R xp2) {{
+    int q = 0;
+{chr(10).join(planes)}
+    return q;
+}}
+
+// coset frame (runtime.py:371-373), plane tests (:374-378), sigma (:379) and y = T xp - t
+// (:385) for coset k, evaluated in R (float on the fast path, else double).
+template <typename R, typename T>
+__device__ __forceinline__ int classify(const T x[3], int k, const int* sigma, const uint4* cls_tab, int* err,
+                                        int cell[3], T y[3], uint4& rec) {{
+    R xp[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {{
+        const R xl = (R)x[i] - (R)kShift[k][i];
+        const R q = floor(xl * (R)kInvD);  // power-of-two d: exact
+        xp[i] = xl - q * (R)kD;
+        cell[i] = clamp_cell(q);
+    }}
+    int c = sigma[plane_code<R>(xp[0], xp[1], xp[2]) % kR];
+    if (c < 0) {{
+        if (err) atomicOr(err, 1);
+        c = 0;
+    }}
+    rec = cls_tab[c];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {{
+        const int perm = (int)((rec.x >> (4 + 2 * i)) & 3u);
+        const R v = perm == 0 ? xp[0] : (perm == 1 ? xp[1] : xp[2]);
+        const int ti = (int)((rec.y >> (8 * i)) & 255u) - 128;
+        y[i] = (T)((((rec.x >> (10 + i)) & 1u) ? -v : v) - (R)ti);
+    }}
+    return c;
+}}
+
 template <typename T>
 struct Eval {{
     static constexpr int kMinBlocks = {min_blocks};
@@ -211,56 +261,66 @@ struct Eval {{
     static constexpr int vec_width() {{
         return 0;
     }}
+    // per-(coset, class) shared-memory address records for the staged tile:
+    // {{coef of site/d component 0, 1, 2; constant offset of pib/d}} (computed per tile)
+    __device__ static void tile_records(const EvalArgs<T>& a, const TileGeom& g, const unsigned char* tables,
+                                        int4* trec, int tid) {{
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
+        for (int idx = tid; idx < kM * kN; idx += kThreads) {{
+            const int k = idx / kN, c = idx - k * kN;
+            const uint4 rec = cls_tab[c];
+            const int st[3] = {{g.ex[k][1] * g.ex[k][2], g.ex[k][2], 1}};
+            int cf[3] = {{0, 0, 0}}, z = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {{
+                const int rho = (int)((rec.x >> (13 + 2 * i)) & 3u);
+                const int tau = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
+                const int pb = (int)((rec.z >> (8 * i)) & 255u) - 128;
+                cf[rho] = tau * st[i];
+                z += pb * st[i];
+            }}
+            trec[idx] = make_int4(cf[0], cf[1], cf[2], z);
+        }}
+    }}
     template <class F, class Ctx>
     __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
         const EvalArgs<T>& a = *ctx.a;
         const int* sigma = reinterpret_cast<const int*>(ctx.tables);
         const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
+        bool fast = false;
+        if constexpr (sizeof(T) == 4) {{
+            const float m = fminf(fminf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
+            const float M = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
+            fast = m >= kFastLo && M < kFastHi;
+        }}
         T total = T(0);
 #pragma unroll
         for (int k = 0; k < kM; ++k) {{
-            // coset frame, runtime.py:371-373 in float64: xl = x - l_k; kk = floor(xl/d)*d
-            // (d is a power of two here, so xl * (1/d) == xl / d exactly)
-            double xp0, xp1, xp2;
             int cell[3];
-            {{
-                const double xl0 = (double)x[0] - kShift[k][0];
-                const double xl1 = (double)x[1] - kShift[k][1];
-                const double xl2 = (double)x[2] - kShift[k][2];
-                const double q0 = floor(xl0 * kInvD), q1 = floor(xl1 * kInvD), q2 = floor(xl2 * kInvD);
-                xp0 = xl0 - q0 * kD;
-                xp1 = xl1 - q1 * kD;
-                xp2 = xl2 - q2 * kD;
-                cell[0] = clamp_cell(q0);
-                cell[1] = clamp_cell(q1);
-                cell[2] = clamp_cell(q2);
-            }}
-            int q = 0;
-{chr(10).join(planes)}
-            int c = sigma[q % kR];
-            if (c < 0) {{
-                if (a.err) atomicOr(a.err, 1);
-                c = 0;
-            }}
+            T yy[3];
+            uint4 rec;
+            const int c = fast ? classify<float, T>(x, k, sigma, cls_tab, a.err, cell, yy, rec)
+                               : classify<double, T>(x, k, sigma, cls_tab, a.err, cell, yy, rec);
             write_dbg(a.dbg, ctx.index, kM, k, c, cell);
-            const uint4 rec = cls_tab[c];
             const int kern = (int)(rec.x & 15u);
             (void)kern;
-            int rho[3], tau[3], base[3];
-            double yv[3];
+            const T y0 = yy[0], y1 = yy[1], y2 = yy[2];
+            if constexpr (F::kIsTile) {{
+                const int4 tr = ctx.trec[k * kN + c];
+                f.a0 = ctx.geom->cbase[k] + cell[0] * ctx.geom->st0[k] + cell[1] * ctx.geom->st1[k] + cell[2] + tr.w;
+                f.c0 = tr.x;
+                f.c1 = tr.y;
+                f.c2 = tr.z;
+            }} else {{
+                int rho[3], tau[3], base[3];
 #pragma unroll
-            for (int i = 0; i < 3; ++i) {{
-                const int perm = (int)((rec.x >> (4 + 2 * i)) & 3u);
-                const double sg = ((rec.x >> (10 + i)) & 1u) ? -1.0 : 1.0;
-                rho[i] = (int)((rec.x >> (13 + 2 * i)) & 3u);
-                tau[i] = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
-                const int ti = (int)((rec.y >> (8 * i)) & 255u) - 128;
-                const int pb = (int)((rec.z >> (8 * i)) & 255u) - 128;
-                yv[i] = sg * sel3(perm, xp0, xp1, xp2) - (double)ti;
-                base[i] = cell[i] + pb;
+                for (int i = 0; i < 3; ++i) {{
+                    rho[i] = (int)((rec.x >> (13 + 2 * i)) & 3u);
+                    tau[i] = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
+                    base[i] = cell[i] + (int)((rec.z >> (8 * i)) & 255u) - 128;
+                }}
+                bind(f, a, *ctx.geom, k, base, rho, tau);
             }}
-            const T y0 = (T)yv[0], y1 = (T)yv[1], y2 = (T)yv[2];
-            bind(f, a, *ctx.geom, k, base, rho, tau);
 {dispatch}
             total += acc;
         }}

@@ -62,6 +62,7 @@ struct EvalArgs {
     int margin;         // extra halo cells (1 for float64 points on shifted cosets, else 0)
     unsigned long long* stats;  // nullable: [0] staged chunks, [1] unstaged chunks, [2] staged elements
     const long long* out_index; // nullable: value of point i goes to out[out_index[i]]
+    int trec_bytes;             // per-(coset, class) tile records (generated kernels), in smem
 };
 
 struct TileGeom {
@@ -72,6 +73,10 @@ struct TileGeom {
     int ex[SP_MAX_COSETS][3];  // box extents
     unsigned fdm[SP_MAX_COSETS][3];  // fast-division magic / shift for ex[k][1], ex[k][2]
     unsigned fds[SP_MAX_COSETS][3];
+    // tile address of coset cell (c0,c1,c2) = cbase[k] + c0*st0[k] + c1*st1[k] + c2
+    int cbase[SP_MAX_COSETS];
+    int st0[SP_MAX_COSETS];
+    int st1[SP_MAX_COSETS];
 };
 
 __device__ __forceinline__ int floordiv_i(int a, int d) {
@@ -222,6 +227,7 @@ struct EvalCtx {
     const EvalArgs<T>* a;
     const unsigned char* tables;  // smem copy (or global when not staged)
     const TileGeom* geom;
+    const int4* trec;             // per-(coset, class) tile address records (generated kernels)
     long long index;              // point index (for debug output)
 };
 
@@ -316,6 +322,9 @@ __device__ __forceinline__ void warp_geometry(const EvalArgs<T>& a, const int* r
     const long long e1 = __shfl_down_sync(0xffffffffu, e, 1);
     const long long e2 = __shfl_down_sync(0xffffffffu, e, 2);
     const long long vol = e * e1 * e2;  // meaningful on lanes 3k
+    const int mylo = (lane < 3 * M && any) ? geom.lo[k][i] : 0;
+    const int lo1 = __shfl_down_sync(0xffffffffu, mylo, 1);
+    const int lo2 = __shfl_down_sync(0xffffffffu, mylo, 2);
     long long total = 0, mine = 0;
     for (int kk = 0; kk < M; ++kk) {
         const long long v = __shfl_sync(0xffffffffu, vol, 3 * kk);
@@ -323,7 +332,13 @@ __device__ __forceinline__ void warp_geometry(const EvalArgs<T>& a, const int* r
         total += v;
     }
     const bool ok = any && a.tile_cap > 0 && total <= a.tile_cap;
-    if (lane < 3 * M && i == 0) geom.off[k] = (int)mine;
+    if (lane < 3 * M && i == 0) {
+        geom.off[k] = (int)mine;
+        const int s0 = (int)(e1 * e2), s1 = (int)e2;
+        geom.st0[k] = s0;
+        geom.st1[k] = s1;
+        geom.cbase[k] = (int)mine - mylo * s0 - lo1 * s1 - lo2;
+    }
     if (lane == 0) {
         geom.staged = ok ? 1 : 0;
         geom.total = ok ? (int)total : 0;
@@ -392,8 +407,10 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
     }
     const int ppt = a.ppt;
     const int chunk_pts = kThreads * ppt;
-    T* spts = reinterpret_cast<T*>(smem + tb);  // [chunk_pts * 3]
-    T* tile = reinterpret_cast<T*>(smem + tb + ((chunk_pts * 3 * (int)sizeof(T) + 15) & ~15));
+    int4* trec = reinterpret_cast<int4*>(smem + tb);
+    const int tb2 = tb + a.trec_bytes;
+    T* spts = reinterpret_cast<T*>(smem + tb2);  // [chunk_pts * 3]
+    T* tile = reinterpret_cast<T*>(smem + tb2 + ((chunk_pts * 3 * (int)sizeof(T) + 15) & ~15));
     V* vtile = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(tile) +
                                     (((a.tile_cap + 4) * (int)sizeof(T) + 15) & ~15));
 
@@ -451,7 +468,10 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
         const bool staged = geom.staged != 0;
 
         // 4. stage the coefficient box (+ halo) with cp.async, boundary policy applied here
-        if (staged) stage_tile<T, kVec>(a, geom, tile, vtile, tid);
+        if (staged) {
+            Ev::tile_records(a, geom, smem, trec, tid);
+            stage_tile<T, kVec>(a, geom, tile, vtile, tid);
+        }
         __syncthreads();
 
         // 5. evaluate
@@ -459,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
         ctx.a = &a;
         ctx.tables = smem;
         ctx.geom = &geom;
+        ctx.trec = trec;
 #pragma unroll 1
         for (int j = tid; j < cnt; j += kThreads) {
             const long long i = first + j;
@@ -507,7 +528,8 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         int4* dst = reinterpret_cast<int4*>(smem);
         for (int i = tid; i < tb / 16; i += kThreads) dst[i] = src[i];
     }
-    T* tile = reinterpret_cast<T*>(smem + tb);
+    int4* trec = reinterpret_cast<int4*>(smem + tb);
+    T* tile = reinterpret_cast<T*>(smem + tb + a.trec_bytes);
     V* vtile = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(tile) +
                                     (((a.tile_cap + 4) * (int)sizeof(T) + 15) & ~15));
     const int B = 1 << log2b;
@@ -530,7 +552,10 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         }
         __syncthreads();
         const bool staged = geom.staged != 0;
-        if (staged) stage_tile<T, kVec>(a, geom, tile, vtile, tid);
+        if (staged) {
+            Ev::tile_records(a, geom, smem, trec, tid);
+            stage_tile<T, kVec>(a, geom, tile, vtile, tid);
+        }
         __syncthreads();
         const int c0 = red[0], c1 = red[1], c2 = red[2];
 
@@ -538,6 +563,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         ctx.a = &a;
         ctx.tables = smem;
         ctx.geom = &geom;
+        ctx.trec = trec;
         // software-pipelined point loads: the next point is in flight while this one is evaluated
         T xn0 = T(0), xn1 = T(0), xn2 = T(0);
         if (p0 + tid < p1) {

@@ -68,6 +68,7 @@ struct BWeights<3> {
 template <typename T, int DEG>
 struct TensorBSplineEval {
     static constexpr int kMinBlocks = sizeof(T) == 4 ? 4 : 3;  // <= 64 / 80 registers
+    __device__ static void tile_records(const EvalArgs<T>&, const TileGeom&, const unsigned char*, int4*, int) {}
     // fp32: rows of DEG+1 taps are one LDS.64 / LDS.128 from the row-vector tile
     template <typename U>
     static constexpr int vec_width() {
@@ -178,6 +179,7 @@ __device__ __forceinline__ T generic_poly(const GenericTables& gt, int p, const 
 template <typename T>
 struct GenericEval {
     static constexpr int kMinBlocks = 1;
+    __device__ static void tile_records(const EvalArgs<T>&, const TileGeom&, const unsigned char*, int4*, int) {}
     template <typename U>
     static constexpr int vec_width() {
         return 0;

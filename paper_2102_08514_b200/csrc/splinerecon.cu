@@ -82,6 +82,7 @@ struct sp_plan {
     int shifts[SP_MAX_COSETS][3] = {};
     int reach_lo[3] = {0, 0, 0}, reach_hi[3] = {0, 0, 0};
     int tp_degree = -1;
+    int N = 0;
     const sp::GenEntry* gen = nullptr;
     void* d_tables = nullptr;  // generated: sigma + class records; generic: GenericTables
     int table_bytes = 0;       // bytes staged into smem (generated only)
@@ -263,6 +264,7 @@ int sp_plan_create(const sp_plan_desc* desc, sp_plan** out) {
     sp_plan* p = new sp_plan();
     p->s = d.s;
     p->M = d.M;
+    p->N = d.N;
     for (int i = 0; i < 3; ++i) p->diag[i] = d.diag[i];
     for (int k = 0; k < d.M; ++k)
         for (int i = 0; i < 3; ++i) p->shifts[k][i] = d.shifts[k][i];
@@ -477,6 +479,7 @@ int build_args(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     a.err = err;
     a.tables = p->d_tables;
     a.table_bytes = p->table_bytes;
+    a.trec_bytes = p->kind == SP_KIND_GENERATED ? p->M * p->N * 16 : 0;
     // row-vector tile (fp32 tensor-product kernels): +vec*sizeof(T) bytes per tile element
     vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
     a.tile_cap = tile_bytes() / (int)(sizeof(T) * (1 + vec));
@@ -493,7 +496,8 @@ int build_args(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
 
 template <typename T>
 size_t tile_smem(const sp::EvalArgs<T>& a, int vec, size_t esz) {
-    return (size_t)((a.table_bytes + 15) & ~15) + ((((size_t)a.tile_cap + 4) * esz + 15) & ~(size_t)15) +
+    return (size_t)((a.table_bytes + 15) & ~15) + (size_t)a.trec_bytes +
+           ((((size_t)a.tile_cap + 4) * esz + 15) & ~(size_t)15) +
            (size_t)a.tile_cap * vec * esz;
 }
 
