@@ -217,6 +217,9 @@ constexpr int kSigmaBytes = {sig_bytes};
 constexpr float kFastLo = {fast_lo!r}f;
 constexpr float kFastHi = 4194304.0f;
 constexpr int kN = {plan.N};
+constexpr int kDI = {d};
+constexpr int kLog2D = {d.bit_length() - 1};
+__device__ constexpr int kShiftI[kM][3] = {{{", ".join("{" + ", ".join(str(int(v)) for v in sh) + "}" for sh in plan.shifts)}}};
 
 template <typename R>
 __device__ __forceinline__ int plane_code(const R xp0, const R xp1, const R xp2) {{
@@ -227,22 +230,13 @@ __device__ __forceinline__ int plane_code(const R xp0, const R xp1, const R xp2)
 
 // coset frame (runtime.py:371-373), plane tests (:374-378), sigma (:379) and y = T xp - t
 // (:385) for coset k, evaluated in R (float on the fast path, else double).
+// class lookup + y = T xp - t from the packed class record
 template <typename R, typename T>
-__device__ __forceinline__ int classify(const T x[3], int k, const int* sigma, const uint4* cls_tab, int* err,
-                                        int cell[3], T y[3], uint4& rec) {{
-    R xp[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {{
-        const R xl = (R)x[i] - (R)kShift[k][i];
-        const R q = floor(xl * (R)kInvD);  // power-of-two d: exact
-        xp[i] = xl - q * (R)kD;
-        cell[i] = clamp_cell(q);
-    }}
+__device__ __forceinline__ int class_and_y(const R xp[3], const int* sigma, const uint4* cls_tab, int& err,
+                                           T y[3], uint4& rec) {{
     int c = sigma[plane_code<R>(xp[0], xp[1], xp[2]) % kR];
-    if (c < 0) {{
-        if (err) atomicOr(err, 1);
-        c = 0;
-    }}
+    err |= c < 0;
+    c = max(c, 0);
     rec = cls_tab[c];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {{
@@ -252,6 +246,38 @@ __device__ __forceinline__ int classify(const T x[3], int k, const int* sigma, c
         y[i] = (T)((((rec.x >> (10 + i)) & 1u) ? -v : v) - (R)ti);
     }}
     return c;
+}}
+
+// float64 coset frame exactly as runtime.py:371-373 (any point)
+template <typename T>
+__device__ __forceinline__ int classify_f64(const T x[3], int k, const int* sigma, const uint4* cls_tab, int& err,
+                                            int cell[3], T y[3], uint4& rec) {{
+    double xp[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {{
+        const double xl = (double)x[i] - kShift[k][i];
+        const double q = floor(xl * kInvD);  // power-of-two d: exact
+        xp[i] = xl - q * kD;
+        cell[i] = clamp_cell(q);
+    }}
+    return class_and_y<double, T>(xp, sigma, cls_tab, err, y, rec);
+}}
+
+// float32 fast frame from X = floor(x) and frac = x - X (exact): for integer l and d = 2^j,
+// floor((x-l)/d) = (X-l) >> j and xp = frac + ((X-l) & (d-1)), exactly the float64 values
+// for |x| >= kFastLo (frac + p needs no rounding there).
+template <typename T>
+__device__ __forceinline__ int classify_fast(const float frac[3], const int X[3], int k, const int* sigma,
+                                             const uint4* cls_tab, int& err, int cell[3], T y[3], uint4& rec) {{
+    float xp[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {{
+        const int xm = X[i] - kShiftI[k][i];
+        cell[i] = xm >> kLog2D;
+        const int p = xm & (kDI - 1);
+        xp[i] = kDI == 1 ? frac[i] : (kDI == 2 ? (p ? frac[i] + 1.0f : frac[i]) : frac[i] + (float)p);
+    }}
+    return class_and_y<float, T>(xp, sigma, cls_tab, err, y, rec);
 }}
 
 template <typename T>
@@ -288,10 +314,13 @@ struct Eval {{
         const int* sigma = reinterpret_cast<const int*>(ctx.tables);
         const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
         bool fast = false;
+        float frac[3] = {{0.f, 0.f, 0.f}};
         if constexpr (sizeof(T) == 4) {{
             const float m = fminf(fminf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
             const float M = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
             fast = m >= kFastLo && M < kFastHi;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) frac[i] = (float)x[i] - floorf((float)x[i]);
         }}
         T total = T(0);
 #pragma unroll
@@ -299,8 +328,8 @@ struct Eval {{
             int cell[3];
             T yy[3];
             uint4 rec;
-            const int c = fast ? classify<float, T>(x, k, sigma, cls_tab, a.err, cell, yy, rec)
-                               : classify<double, T>(x, k, sigma, cls_tab, a.err, cell, yy, rec);
+            const int c = fast ? classify_fast<T>(frac, ctx.X, k, sigma, cls_tab, ctx.err, cell, yy, rec)
+                               : classify_f64<T>(x, k, sigma, cls_tab, ctx.err, cell, yy, rec);
             write_dbg(a.dbg, ctx.index, kM, k, c, cell);
             const int kern = (int)(rec.x & 15u);
             (void)kern;

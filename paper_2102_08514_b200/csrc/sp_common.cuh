@@ -229,6 +229,8 @@ struct EvalCtx {
     const TileGeom* geom;
     const int4* trec;             // per-(coset, class) tile address records (generated kernels)
     long long index;              // point index (for debug output)
+    int X[3];                     // floor(x) of the current point (clamped), computed once
+    mutable int err;              // sigma-sentinel hits, flushed with one atomic per thread
 };
 
 // cp.async (LDGSTS) element copy global -> shared; src_bytes = 0 zero-fills (boundary 'zero').
@@ -480,11 +482,15 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
         ctx.tables = smem;
         ctx.geom = &geom;
         ctx.trec = trec;
+        ctx.err = 0;
 #pragma unroll 1
         for (int j = tid; j < cnt; j += kThreads) {
             const long long i = first + j;
             ctx.index = i;
             const T x[3] = {spts[3 * j], spts[3 * j + 1], spts[3 * j + 2]};
+            ctx.X[0] = clamp_cell(x[0]);
+            ctx.X[1] = clamp_cell(x[1]);
+            ctx.X[2] = clamp_cell(x[2]);
             T v;
             if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) {
                 v = T(NAN);
@@ -499,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
             }
             a.out[i] = v;
         }
+        if (ctx.err && a.err) atomicOr(a.err, 1);
         __syncthreads();
     }
 }
@@ -564,6 +571,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         ctx.tables = smem;
         ctx.geom = &geom;
         ctx.trec = trec;
+        ctx.err = 0;
         // software-pipelined point loads: the next point is in flight while this one is evaluated
         T xn0 = T(0), xn1 = T(0), xn2 = T(0);
         if (p0 + tid < p1) {
@@ -584,9 +592,11 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
             }
             T v;
             const bool fin = isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]);
-            const bool inside = (unsigned)(clamp_cell(x[0]) - c0) < (unsigned)B &&
-                                (unsigned)(clamp_cell(x[1]) - c1) < (unsigned)B &&
-                                (unsigned)(clamp_cell(x[2]) - c2) < (unsigned)B;
+            ctx.X[0] = clamp_cell(x[0]);
+            ctx.X[1] = clamp_cell(x[1]);
+            ctx.X[2] = clamp_cell(x[2]);
+            const bool inside = (unsigned)(ctx.X[0] - c0) < (unsigned)B && (unsigned)(ctx.X[1] - c1) < (unsigned)B &&
+                                (unsigned)(ctx.X[2] - c2) < (unsigned)B;
             if (!fin) {
                 v = T(NAN);
             } else if (staged && inside) {
@@ -601,6 +611,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
             if (a.out_index) a.out[a.out_index[j]] = v;
             else a.out[j] = v;
         }
+        if (ctx.err && a.err) atomicOr(a.err, 1);
         __syncthreads();
     }
 }

@@ -82,7 +82,7 @@ struct TensorBSplineEval {
         for (int i = 0; i < 3; ++i) {
             const T fl = floor(x[i]);
             BWeights<DEG>::w(x[i] - fl, w[i]);
-            cell[i] = clamp_cell(x[i]);
+            cell[i] = ctx.X[i];
         }
         bind_identity(f, *ctx.a, *ctx.geom, 0, cell);
         write_dbg(ctx.a->dbg, ctx.index, 1, 0, 0, cell);
@@ -203,7 +203,7 @@ struct GenericEval {
             }
             int cls = __ldg(gt.sigma + (int)(q % gt.r));
             if (cls < 0) {
-                if (a.err) atomicOr(a.err, 1);
+                ctx.err = 1;
                 cls = 0;
             }
             write_dbg(a.dbg, ctx.index, a.fr.M, k, cls, cf.cell);
