@@ -238,12 +238,13 @@ __device__ __forceinline__ int class_and_y(const R xp[3], const int* sigma, cons
     err |= c < 0;
     c = max(c, 0);
     rec = cls_tab[c];
+    const float tt[3] = {{__uint_as_float(rec.y), __uint_as_float(rec.z), __uint_as_float(rec.w)}};
 #pragma unroll
     for (int i = 0; i < 3; ++i) {{
-        const int perm = (int)((rec.x >> (4 + 2 * i)) & 3u);
-        const R v = perm == 0 ? xp[0] : (perm == 1 ? xp[1] : xp[2]);
-        const int ti = (int)((rec.y >> (8 * i)) & 255u) - 128;
-        y[i] = (T)((((rec.x >> (10 + i)) & 1u) ? -v : v) - (R)ti);
+        const unsigned perm = (rec.x >> (4 + 2 * i)) & 3u;  // 0, 1 or 2
+        const R v01 = (perm & 1u) ? xp[1] : xp[0];
+        const R v = (perm & 2u) ? xp[2] : v01;
+        y[i] = (T)((((rec.x >> (10 + i)) & 1u) ? -v : v) - (R)tt[i]);
     }}
     return c;
 }}
@@ -301,7 +302,7 @@ struct Eval {{
             for (int i = 0; i < 3; ++i) {{
                 const int rho = (int)((rec.x >> (13 + 2 * i)) & 3u);
                 const int tau = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
-                const int pb = (int)((rec.z >> (8 * i)) & 255u) - 128;
+                const int pb = (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
                 cf[rho] = tau * st[i];
                 z += pb * st[i];
             }}
@@ -336,7 +337,7 @@ struct Eval {{
             const T y0 = yy[0], y1 = yy[1], y2 = yy[2];
             if constexpr (F::kIsTile) {{
                 const int4 tr = ctx.trec[k * kN + c];
-                f.a0 = ctx.geom->cbase[k] + cell[0] * ctx.geom->st0[k] + cell[1] * ctx.geom->st1[k] + cell[2] + tr.w;
+                f.a0 = ctx.cbase[k] + cell[0] * ctx.st0[k] + cell[1] * ctx.st1[k] + cell[2] + tr.w;
                 f.c0 = tr.x;
                 f.c1 = tr.y;
                 f.c2 = tr.z;
@@ -346,7 +347,7 @@ struct Eval {{
                 for (int i = 0; i < 3; ++i) {{
                     rho[i] = (int)((rec.x >> (13 + 2 * i)) & 3u);
                     tau[i] = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
-                    base[i] = cell[i] + (int)((rec.z >> (8 * i)) & 255u) - 128;
+                    base[i] = cell[i] + (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
                 }}
                 bind(f, a, *ctx.geom, k, base, rho, tau);
             }}

@@ -231,6 +231,19 @@ struct EvalCtx {
     long long index;              // point index (for debug output)
     int X[3];                     // floor(x) of the current point (clamped), computed once
     mutable int err;              // sigma-sentinel hits, flushed with one atomic per thread
+    int cbase[SP_MAX_COSETS];     // register copies of the tile geometry (staged path)
+    int st0[SP_MAX_COSETS];
+    int st1[SP_MAX_COSETS];
+    __device__ __forceinline__ void load_geom(const TileGeom& g, int M) {
+#pragma unroll
+        for (int k = 0; k < SP_MAX_COSETS; ++k) {
+            if (k < M) {
+                cbase[k] = g.cbase[k];
+                st0[k] = g.st0[k];
+                st1[k] = g.st1[k];
+            }
+        }
+    }
 };
 
 // cp.async (LDGSTS) element copy global -> shared; src_bytes = 0 zero-fills (boundary 'zero').
@@ -483,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
         ctx.geom = &geom;
         ctx.trec = trec;
         ctx.err = 0;
+        ctx.load_geom(geom, M);
 #pragma unroll 1
         for (int j = tid; j < cnt; j += kThreads) {
             const long long i = first + j;
@@ -572,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         ctx.geom = &geom;
         ctx.trec = trec;
         ctx.err = 0;
+        ctx.load_geom(geom, a.fr.M);
         // software-pipelined point loads: the next point is in flight while this one is evaluated
         T xn0 = T(0), xn1 = T(0), xn2 = T(0);
         if (p0 + tid < p1) {

@@ -335,20 +335,25 @@ int sp_plan_create(const sp_plan_desc* desc, sp_plan** out) {
             double A[9];
             for (int j = 0; j < 9; ++j) A[j] = d.cls_piA[9 * c + j];
             if (!signed_perm(A, rho, tau)) { delete p; return fail(SP_ERR_INVALID, "generated plan needs signed-permutation piA"); }
+            // x: kernel | perm_i << (4+2i) | (sign_i<0) << (10+i) | rho_i << (13+2i) | (tau_i<0) << (19+i)
+            //    | (pib_i/d + 4) << (22+3i);   y, z, w: t_0, t_1, t_2 as float bits
             uint32_t x = (uint32_t)d.cls_kernel[c];
-            uint32_t y = 0, z = 0;
+            float tf[3];
             for (int i = 0; i < 3; ++i) {
                 x |= (uint32_t)perm[i] << (4 + 2 * i);
                 x |= (uint32_t)(sign[i] < 0) << (10 + i);
                 x |= (uint32_t)rho[i] << (13 + 2 * i);
                 x |= (uint32_t)(tau[i] < 0) << (19 + i);
-                const int ti = (int)d.cls_t[3 * c + i];
-                if ((double)ti != d.cls_t[3 * c + i]) { delete p; return fail(SP_ERR_INVALID, "non-integral class shift t"); }
-                y |= (uint32_t)(ti + 128) << (8 * i);
-                z |= (uint32_t)(d.cls_pib[3 * c + i] / d.diag[i] + 128) << (8 * i);
+                const double ti = d.cls_t[3 * c + i];
+                if (ti != std::floor(ti) || std::fabs(ti) > 1024) { delete p; return fail(SP_ERR_INVALID, "non-integral class shift t"); }
+                tf[i] = (float)ti;
+                const int pbd = d.cls_pib[3 * c + i] / d.diag[i];
+                if (pbd < -4 || pbd > 3) { delete p; return fail(SP_ERR_UNSUPPORTED, "class offset out of range"); }
+                x |= (uint32_t)(pbd + 4) << (22 + 3 * i);
             }
             uint32_t* rec = blob.data() + sig_bytes / 4 + 4 * c;
-            rec[0] = x; rec[1] = y; rec[2] = z; rec[3] = 0;
+            rec[0] = x;
+            std::memcpy(rec + 1, tf, sizeof tf);
         }
         const uint32_t* dptr = nullptr;
         if (upload(p, blob, &dptr) != SP_OK) { delete p; return SP_ERR_CUDA; }
