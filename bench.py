@@ -368,7 +368,7 @@ def run_ours(args):
     def unsorted_step():
         interp.eval_batch(grid, shuffled, out=out, check=False, order="sort")
 
-    ms_b = measure(unsorted_step, max(2, args.steps // 4), 1, stream, dist)
+    ms_b = measure(unsorted_step, max(2, min(args.steps // 4, 10)), 1, stream, dist)
     del shuffled
     torch.cuda.empty_cache()
 
@@ -428,7 +428,7 @@ def run_ours(args):
 
             wstep()
             torch.cuda.synchronize()
-            msw = measure(wstep, max(3, args.steps // 2), args.warmup, stream, dist)
+            msw = measure(wstep, max(3, min(args.steps, 40)), args.warmup, stream, dist)
             es = grid_w.arrays[0].element_size()
             bw = algorithmic_bytes(nw, grid_w, es)
             others[wname] = {
@@ -453,7 +453,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default=HEADLINE, choices=sorted(WORKLOADS))

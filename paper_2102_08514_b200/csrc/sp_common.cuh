@@ -525,6 +525,12 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
 }
 
 
+template <typename T>
+__device__ __forceinline__ void store_out(const EvalArgs<T>& a, long long j, T v) {
+    if (a.out_index) a.out[a.out_index[j]] = v;
+    else a.out[j] = v;
+}
+
 // ---------------------------------------------------------------------------------------
 // Brick mode: points sorted by the Morton code of their unit cell are grouped into aligned
 // bricks of B^3 unit cells (B = 2^log2b); brick_start[b]..brick_start[b+1] are brick b's
@@ -587,6 +593,77 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         ctx.trec = trec;
         ctx.err = 0;
         ctx.load_geom(geom, a.fr.M);
+        if constexpr (Ev::kPairRuns) {
+            if (staged && a.dbg == nullptr) {
+                // Register reuse for Morton-sorted points: each thread walks a contiguous
+                // segment of the brick's points and evaluates consecutive same-cell points in
+                // pairs against ONE set of row loads (shared-memory wavefronts per point drop
+                // from 2 towards 1).  Same arithmetic per point as the single-point path.
+                const long long cnt = p1 - p0;
+                const long long L = (cnt + kThreads - 1) / kThreads;
+                long long j = p0 + (long long)tid * L;
+                const long long e = min(p1, j + L);
+                T xa[3] = {T(0), T(0), T(0)};
+                if (j < e) {
+                    xa[0] = __ldg(a.pts + 3 * j);
+                    xa[1] = __ldg(a.pts + 3 * j + 1);
+                    xa[2] = __ldg(a.pts + 3 * j + 2);
+                }
+#pragma unroll 1
+                while (j < e) {
+                    const bool havb = j + 1 < e;
+                    T xb[3] = {T(0), T(0), T(0)};
+                    if (havb) {
+                        xb[0] = __ldg(a.pts + 3 * j + 3);
+                        xb[1] = __ldg(a.pts + 3 * j + 4);
+                        xb[2] = __ldg(a.pts + 3 * j + 5);
+                    }
+                    int Xa[3], Xb[3];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        Xa[i] = clamp_cell(xa[i]);
+                        Xb[i] = clamp_cell(xb[i]);
+                    }
+                    const bool oka = isfinite(xa[0]) && isfinite(xa[1]) && isfinite(xa[2]) &&
+                                     (unsigned)(Xa[0] - c0) < (unsigned)B && (unsigned)(Xa[1] - c1) < (unsigned)B &&
+                                     (unsigned)(Xa[2] - c2) < (unsigned)B;
+                    const bool pair = oka && havb && isfinite(xb[0]) && isfinite(xb[1]) && isfinite(xb[2]) &&
+                                      Xa[0] == Xb[0] && Xa[1] == Xb[1] && Xa[2] == Xb[2];
+                    T va, vb;
+                    if (oka) {
+                        TileFetch<T, V> f;
+                        f.tile = tile;
+                        f.vtile = vtile;
+                        Ev::run_pair(xa, xb, Xa, pair, f, ctx, va, vb);
+                    } else {
+                        ctx.index = j;
+                        ctx.X[0] = Xa[0];
+                        ctx.X[1] = Xa[1];
+                        ctx.X[2] = Xa[2];
+                        const bool fin = isfinite(xa[0]) && isfinite(xa[1]) && isfinite(xa[2]);
+                        GlobalFetch<T> f;
+                        va = fin ? Ev::template eval<GlobalFetch<T>>(xa, f, ctx) : T(NAN);
+                    }
+                    store_out(a, j, va);
+                    if (pair) store_out(a, j + 1, vb);
+                    const long long step = pair ? 2 : 1;
+                    j += step;
+                    if (pair) {
+                        if (j < e) {
+                            xa[0] = __ldg(a.pts + 3 * j);
+                            xa[1] = __ldg(a.pts + 3 * j + 1);
+                            xa[2] = __ldg(a.pts + 3 * j + 2);
+                        }
+                    } else {
+                        xa[0] = xb[0];
+                        xa[1] = xb[1];
+                        xa[2] = xb[2];
+                    }
+                }
+                __syncthreads();
+                continue;
+            }
+        }
         // software-pipelined point loads: the next point is in flight while this one is evaluated
         T xn0 = T(0), xn1 = T(0), xn2 = T(0);
         if (p0 + tid < p1) {
