@@ -26,6 +26,7 @@ namespace sp {
 
 constexpr int kThreads = 256;
 constexpr int kMaxPPT = 8;                    // points per thread per chunk (runtime <= this)
+constexpr int kPairQueue = 1024;              // leftover queue of split pairs (brick mode)
 constexpr int kCellClamp = 1 << 30;           // |cell| clamp (mirror exact below this)
 
 template <typename T>
@@ -531,6 +532,24 @@ __device__ __forceinline__ void store_out(const EvalArgs<T>& a, long long j, T v
     else a.out[j] = v;
 }
 
+// One point in brick mode (ctx.X = floor(x) already set): staged tile when the point lies in
+// the staged brick, else the global (policy-checked) path.
+template <typename T, class Ev, typename V>
+__device__ __forceinline__ T eval_one(const T x[3], bool staged, int c0, int c1, int c2, int B, const T* tile,
+                                      const V* vtile, const EvalCtx<T, Ev>& ctx) {
+    if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) return T(NAN);
+    const bool inside = (unsigned)(ctx.X[0] - c0) < (unsigned)B && (unsigned)(ctx.X[1] - c1) < (unsigned)B &&
+                        (unsigned)(ctx.X[2] - c2) < (unsigned)B;
+    if (staged && inside) {
+        TileFetch<T, V> f;
+        f.tile = tile;
+        f.vtile = vtile;
+        return Ev::template eval<TileFetch<T, V>>(x, f, ctx);
+    }
+    GlobalFetch<T> f;
+    return Ev::template eval<GlobalFetch<T>>(x, f, ctx);
+}
+
 // ---------------------------------------------------------------------------------------
 // Brick mode: points sorted by the Morton code of their unit cell are grouped into aligned
 // bricks of B^3 unit cells (B = 2^log2b); brick_start[b]..brick_start[b+1] are brick b's
@@ -544,6 +563,8 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ TileGeom geom;
     __shared__ int red[6];
+    __shared__ int pq_count;
+    __shared__ int pq[Ev::kPairRuns ? kPairQueue : 1];
     constexpr int kVec = Ev::template vec_width<T>();
     using V = typename VecT<T, kVec>::type;
 
@@ -595,28 +616,27 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         ctx.load_geom(geom, a.fr.M);
         if constexpr (Ev::kPairRuns) {
             if (staged && a.dbg == nullptr) {
-                // Register reuse for Morton-sorted points: each thread walks a contiguous
-                // segment of the brick's points and evaluates consecutive same-cell points in
-                // pairs against ONE set of row loads (shared-memory wavefronts per point drop
-                // from 2 towards 1).  Same arithmetic per point as the single-point path.
+                // Register reuse for Morton-sorted points: thread q takes the consecutive pair
+                // (2q, 2q+1) of the brick (a warp covers 64 consecutive points, so lanes stay
+                // spatially coherent).  When both points lie in the same cell (the common case
+                // at several points per cell) they are evaluated against ONE set of row loads;
+                // otherwise the second point is queued and evaluated in a coherent leftover
+                // pass.  Same arithmetic per point as the single-point path.
+                if (tid == 0) pq_count = 0;
+                __syncthreads();
                 const long long cnt = p1 - p0;
-                const long long L = (cnt + kThreads - 1) / kThreads;
-                long long j = p0 + (long long)tid * L;
-                const long long e = min(p1, j + L);
-                T xa[3] = {T(0), T(0), T(0)};
-                if (j < e) {
-                    xa[0] = __ldg(a.pts + 3 * j);
-                    xa[1] = __ldg(a.pts + 3 * j + 1);
-                    xa[2] = __ldg(a.pts + 3 * j + 2);
-                }
+                const long long npairs = (cnt + 1) / 2;
 #pragma unroll 1
-                while (j < e) {
-                    const bool havb = j + 1 < e;
+                for (long long q = tid; q < npairs; q += kThreads) {
+                    const long long j = p0 + 2 * q;
+                    const bool havb = j + 1 < p1;
+                    const T* px = a.pts + 3 * j;
+                    const T xa[3] = {__ldg(px), __ldg(px + 1), __ldg(px + 2)};
                     T xb[3] = {T(0), T(0), T(0)};
                     if (havb) {
-                        xb[0] = __ldg(a.pts + 3 * j + 3);
-                        xb[1] = __ldg(a.pts + 3 * j + 4);
-                        xb[2] = __ldg(a.pts + 3 * j + 5);
+                        xb[0] = __ldg(px + 3);
+                        xb[1] = __ldg(px + 4);
+                        xb[2] = __ldg(px + 5);
                     }
                     int Xa[3], Xb[3];
 #pragma unroll
@@ -627,38 +647,57 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
                     const bool oka = isfinite(xa[0]) && isfinite(xa[1]) && isfinite(xa[2]) &&
                                      (unsigned)(Xa[0] - c0) < (unsigned)B && (unsigned)(Xa[1] - c1) < (unsigned)B &&
                                      (unsigned)(Xa[2] - c2) < (unsigned)B;
-                    const bool pair = oka && havb && isfinite(xb[0]) && isfinite(xb[1]) && isfinite(xb[2]) &&
+                    const bool same = oka && havb && isfinite(xb[0]) && isfinite(xb[1]) && isfinite(xb[2]) &&
                                       Xa[0] == Xb[0] && Xa[1] == Xb[1] && Xa[2] == Xb[2];
                     T va, vb;
                     if (oka) {
                         TileFetch<T, V> f;
                         f.tile = tile;
                         f.vtile = vtile;
-                        Ev::run_pair(xa, xb, Xa, pair, f, ctx, va, vb);
+                        Ev::run_pair(xa, xb, Xa, same, f, ctx, va, vb);
                     } else {
                         ctx.index = j;
                         ctx.X[0] = Xa[0];
                         ctx.X[1] = Xa[1];
                         ctx.X[2] = Xa[2];
-                        const bool fin = isfinite(xa[0]) && isfinite(xa[1]) && isfinite(xa[2]);
-                        GlobalFetch<T> f;
-                        va = fin ? Ev::template eval<GlobalFetch<T>>(xa, f, ctx) : T(NAN);
+                        va = eval_one<T, Ev, V>(xa, staged, c0, c1, c2, B, tile, vtile, ctx);
                     }
                     store_out(a, j, va);
-                    if (pair) store_out(a, j + 1, vb);
-                    const long long step = pair ? 2 : 1;
-                    j += step;
-                    if (pair) {
-                        if (j < e) {
-                            xa[0] = __ldg(a.pts + 3 * j);
-                            xa[1] = __ldg(a.pts + 3 * j + 1);
-                            xa[2] = __ldg(a.pts + 3 * j + 2);
+                    if (same) store_out(a, j + 1, vb);
+                    // queue the second point of a split pair (warp-aggregated slot allocation)
+                    const bool need = havb && !same;
+                    const unsigned m = __ballot_sync(__activemask(), need);
+                    if (need) {
+                        const int leader = __ffs(m) - 1;
+                        int base = 0;
+                        if (lane == leader) base = atomicAdd(&pq_count, __popc(m));
+                        base = __shfl_sync(m, base, leader);
+                        const int pos = base + __popc(m & ((1u << lane) - 1));
+                        if (pos < kPairQueue) {
+                            pq[pos] = (int)(j + 1 - p0);
+                        } else {
+                            const T* pb = a.pts + 3 * (j + 1);
+                            const T x1[3] = {__ldg(pb), __ldg(pb + 1), __ldg(pb + 2)};
+                            ctx.index = j + 1;
+                            ctx.X[0] = clamp_cell(x1[0]);
+                            ctx.X[1] = clamp_cell(x1[1]);
+                            ctx.X[2] = clamp_cell(x1[2]);
+                            store_out(a, j + 1, eval_one<T, Ev, V>(x1, staged, c0, c1, c2, B, tile, vtile, ctx));
                         }
-                    } else {
-                        xa[0] = xb[0];
-                        xa[1] = xb[1];
-                        xa[2] = xb[2];
                     }
+                }
+                __syncthreads();
+                const int nq = min(pq_count, kPairQueue);
+#pragma unroll 1
+                for (int t = tid; t < nq; t += kThreads) {
+                    const long long j = p0 + pq[t];
+                    const T* pb = a.pts + 3 * j;
+                    const T x1[3] = {__ldg(pb), __ldg(pb + 1), __ldg(pb + 2)};
+                    ctx.index = j;
+                    ctx.X[0] = clamp_cell(x1[0]);
+                    ctx.X[1] = clamp_cell(x1[1]);
+                    ctx.X[2] = clamp_cell(x1[2]);
+                    store_out(a, j, eval_one<T, Ev, V>(x1, staged, c0, c1, c2, B, tile, vtile, ctx));
                 }
                 __syncthreads();
                 continue;
