@@ -26,7 +26,6 @@ namespace sp {
 
 constexpr int kThreads = 256;
 constexpr int kMaxPPT = 8;                    // points per thread per chunk (runtime <= this)
-constexpr int kPairQueue = 1024;              // leftover queue of split pairs (brick mode)
 constexpr int kCellClamp = 1 << 30;           // |cell| clamp (mirror exact below this)
 
 template <typename T>
@@ -64,6 +63,7 @@ struct EvalArgs {
     unsigned long long* stats;  // nullable: [0] staged chunks, [1] unstaged chunks, [2] staged elements
     const long long* out_index; // nullable: value of point i goes to out[out_index[i]]
     int trec_bytes;             // per-(coset, class) tile records (generated kernels), in smem
+    int pair_queue;             // brick mode, pair evaluators: leftover-queue capacity (points)
 };
 
 struct TileGeom {
@@ -564,7 +564,6 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     __shared__ TileGeom geom;
     __shared__ int red[6];
     __shared__ int pq_count;
-    __shared__ int pq[Ev::kPairRuns ? kPairQueue : 1];
     constexpr int kVec = Ev::template vec_width<T>();
     using V = typename VecT<T, kVec>::type;
 
@@ -580,6 +579,8 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     T* tile = reinterpret_cast<T*>(smem + tb + a.trec_bytes);
     V* vtile = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(tile) +
                                     (((a.tile_cap + 4) * (int)sizeof(T) + 15) & ~15));
+    // pair-mode leftover queue (brick-relative point offsets) after the tiles
+    int* pq = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(vtile) + (size_t)a.tile_cap * kVec * sizeof(T));
     const int B = 1 << log2b;
 
     for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
@@ -615,21 +616,25 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         ctx.err = 0;
         ctx.load_geom(geom, a.fr.M);
         if constexpr (Ev::kPairRuns) {
-            if (staged && a.dbg == nullptr) {
+            if (staged && a.dbg == nullptr && p1 - p0 <= (long long)a.pair_queue) {
                 // Register reuse for Morton-sorted points: thread q takes the consecutive pair
                 // (2q, 2q+1) of the brick (a warp covers 64 consecutive points, so lanes stay
                 // spatially coherent).  When both points lie in the same cell (the common case
-                // at several points per cell) they are evaluated against ONE set of row loads;
-                // otherwise the second point is queued and evaluated in a coherent leftover
-                // pass.  Same arithmetic per point as the single-point path.
+                // at several points per cell) they are evaluated against ONE set of row loads.
+                // Every other point (second point of a split pair, points outside the brick,
+                // non-finite points) is queued and evaluated in a leftover pass; the queue holds
+                // a whole brick, so it cannot overflow.  Same arithmetic per point as the
+                // single-point path.
                 if (tid == 0) pq_count = 0;
                 __syncthreads();
                 const long long cnt = p1 - p0;
                 const long long npairs = (cnt + 1) / 2;
 #pragma unroll 1
-                for (long long q = tid; q < npairs; q += kThreads) {
-                    const long long j = p0 + 2 * q;
-                    const bool havb = j + 1 < p1;
+                for (long long qb = 0; qb < npairs; qb += kThreads) {  // block-uniform trip count
+                    const long long q = qb + tid;
+                    const bool act = q < npairs;
+                    const long long j = p0 + 2 * (act ? q : 0);
+                    const bool havb = act && j + 1 < p1;
                     const T* px = a.pts + 3 * j;
                     const T xa[3] = {__ldg(px), __ldg(px + 1), __ldg(px + 2)};
                     T xb[3] = {T(0), T(0), T(0)};
@@ -644,50 +649,44 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
                         Xa[i] = clamp_cell(xa[i]);
                         Xb[i] = clamp_cell(xb[i]);
                     }
-                    const bool oka = isfinite(xa[0]) && isfinite(xa[1]) && isfinite(xa[2]) &&
+                    const bool oka = act && isfinite(xa[0]) && isfinite(xa[1]) && isfinite(xa[2]) &&
                                      (unsigned)(Xa[0] - c0) < (unsigned)B && (unsigned)(Xa[1] - c1) < (unsigned)B &&
                                      (unsigned)(Xa[2] - c2) < (unsigned)B;
                     const bool same = oka && havb && isfinite(xb[0]) && isfinite(xb[1]) && isfinite(xb[2]) &&
                                       Xa[0] == Xb[0] && Xa[1] == Xb[1] && Xa[2] == Xb[2];
-                    T va, vb;
-                    if (oka) {
+                    {
                         TileFetch<T, V> f;
                         f.tile = tile;
                         f.vtile = vtile;
-                        Ev::run_pair(xa, xb, Xa, same, f, ctx, va, vb);
-                    } else {
-                        ctx.index = j;
-                        ctx.X[0] = Xa[0];
-                        ctx.X[1] = Xa[1];
-                        ctx.X[2] = Xa[2];
-                        va = eval_one<T, Ev, V>(xa, staged, c0, c1, c2, B, tile, vtile, ctx);
+                        T va, vb;
+                        // (for !oka lanes the tile address is clamped into range; result unused)
+                        int Xs[3];
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) Xs[i] = oka ? Xa[i] : (i == 0 ? c0 : (i == 1 ? c1 : c2));
+                        Ev::run_pair(xa, xb, Xs, same, f, ctx, va, vb);
+                        if (oka) store_out(a, j, va);
+                        if (same) store_out(a, j + 1, vb);
                     }
-                    store_out(a, j, va);
-                    if (same) store_out(a, j + 1, vb);
-                    // queue the second point of a split pair (warp-aggregated slot allocation)
-                    const bool need = havb && !same;
-                    const unsigned m = __ballot_sync(__activemask(), need);
-                    if (need) {
-                        const int leader = __ffs(m) - 1;
-                        int base = 0;
-                        if (lane == leader) base = atomicAdd(&pq_count, __popc(m));
-                        base = __shfl_sync(m, base, leader);
-                        const int pos = base + __popc(m & ((1u << lane) - 1));
-                        if (pos < kPairQueue) {
-                            pq[pos] = (int)(j + 1 - p0);
-                        } else {
-                            const T* pb = a.pts + 3 * (j + 1);
-                            const T x1[3] = {__ldg(pb), __ldg(pb + 1), __ldg(pb + 2)};
-                            ctx.index = j + 1;
-                            ctx.X[0] = clamp_cell(x1[0]);
-                            ctx.X[1] = clamp_cell(x1[1]);
-                            ctx.X[2] = clamp_cell(x1[2]);
-                            store_out(a, j + 1, eval_one<T, Ev, V>(x1, staged, c0, c1, c2, B, tile, vtile, ctx));
-                        }
+                    // queue what was not evaluated (warp-aggregated slot allocation)
+                    const int na = (act && !oka) ? 1 : 0;
+                    const int nb = (havb && !same) ? 1 : 0;
+                    int mine = na + nb;
+                    int incl = mine;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += v;
                     }
+                    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                    int base = 0;
+                    if (lane == 31 && tot) base = atomicAdd(&pq_count, tot);
+                    base = __shfl_sync(0xffffffffu, base, 31);
+                    int pos = base + incl - mine;
+                    if (na) pq[pos++] = (int)(j - p0);
+                    if (nb) pq[pos] = (int)(j + 1 - p0);
                 }
                 __syncthreads();
-                const int nq = min(pq_count, kPairQueue);
+                const int nq = pq_count;
 #pragma unroll 1
                 for (int t = tid; t < nq; t += kThreads) {
                     const long long j = p0 + pq[t];

@@ -351,6 +351,7 @@ class PlanInterpreter:
             with torch.cuda.stream(st):
                 _native.check(lib.sp_eval_bricks(h, ctypes.byref(gdesc), batch.pts.data_ptr(), n, dtype,
                                                  batch.brick_start.data_ptr(), batch.n_bricks, batch.log2_brick,
+                                                 min(batch.max_brick, 2**31 - 1),
                                                  None if idx is None else idx.data_ptr(), res.data_ptr(),
                                                  None if err is None else err.data_ptr(), st.cuda_stream))
         if check and int(err.item()):
@@ -416,11 +417,15 @@ class PointBatch:
     `prepare_points`; evaluate with `PlanInterpreter.eval_batch(grid, batch)`.
     """
 
-    def __init__(self, pts: torch.Tensor, brick_start: torch.Tensor, log2_brick: int, perm: torch.Tensor | None):
+    def __init__(self, pts: torch.Tensor, brick_start: torch.Tensor, log2_brick: int, perm: torch.Tensor | None,
+                 max_brick: int | None = None):
         self.pts = pts
         self.brick_start = brick_start
         self.log2_brick = int(log2_brick)
         self.perm = perm
+        if max_brick is None:
+            max_brick = int((brick_start[1:] - brick_start[:-1]).max().item()) if brick_start.numel() > 1 else 0
+        self.max_brick = int(max_brick)
 
     @property
     def n(self) -> int:
@@ -456,7 +461,8 @@ def prepare_points(pts: torch.Tensor, log2_brick: int, *, presorted: bool = Fals
         _, counts = torch.unique_consecutive(bid, return_counts=True)
         start = torch.zeros(counts.shape[0] + 1, dtype=torch.int64, device=pts.device)
         torch.cumsum(counts, 0, out=start[1:])
-    return PointBatch(pts, start, log2_brick, perm)
+        max_brick = int(counts.max().item()) if counts.numel() else 0
+    return PointBatch(pts, start, log2_brick, perm, max_brick)
 
 
 def morton_order(pts: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
