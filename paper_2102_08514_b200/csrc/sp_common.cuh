@@ -64,6 +64,7 @@ struct EvalArgs {
     const long long* out_index; // nullable: value of point i goes to out[out_index[i]]
     int trec_bytes;             // per-(coset, class) tile records (generated kernels), in smem
     int pair_queue;             // brick mode, pair evaluators: leftover-queue capacity (points)
+    int vec_cap;                // row-vector tile capacity in elements (0: no row-vector tile)
 };
 
 struct TileGeom {
@@ -78,6 +79,10 @@ struct TileGeom {
     int cbase[SP_MAX_COSETS];
     int st0[SP_MAX_COSETS];
     int st1[SP_MAX_COSETS];
+    // row-vector tile (coset 0): padded pitches vx, vy (vx = 6 mod 8, vy = 2 mod 4 makes the
+    // 16-byte rows of any 2x2x2 cell block fall in distinct bank groups), address base
+    int vx, vy, vtotal, vbase;
+    unsigned vfm_x, vfs_x, vfm_y, vfs_y;
 };
 
 __device__ __forceinline__ int floordiv_i(int a, int d) {
@@ -235,7 +240,11 @@ struct EvalCtx {
     int cbase[SP_MAX_COSETS];     // register copies of the tile geometry (staged path)
     int st0[SP_MAX_COSETS];
     int st1[SP_MAX_COSETS];
+    int vbase, vst0, vst1;        // row-vector tile (coset 0)
     __device__ __forceinline__ void load_geom(const TileGeom& g, int M) {
+        vbase = g.vbase;
+        vst0 = g.vx * g.vy;
+        vst1 = g.vx;
 #pragma unroll
         for (int k = 0; k < SP_MAX_COSETS; ++k) {
             if (k < M) {
@@ -355,6 +364,27 @@ __device__ __forceinline__ void warp_geometry(const EvalArgs<T>& a, const int* r
         geom.st1[k] = s1;
         geom.cbase[k] = (int)mine - mylo * s0 - lo1 * s1 - lo2;
     }
+    if (lane == 0 && a.vec_cap > 0 && any) {
+        // padded pitches for the row-vector tile of coset 0 (dense when they do not fit)
+        const int ex = (int)e2, ey = (int)e1, ez = (int)e;
+        int vx = ex + ((6 - ex % 8) + 8) % 8;
+        int vy = ey + ((2 - ey % 4) + 4) % 4;
+        if ((long long)vx * vy * ez > a.vec_cap) {
+            vx = ex;
+            vy = ey;
+        }
+        geom.vx = vx;
+        geom.vy = vy;
+        geom.vtotal = vx * vy * ez;
+        geom.vbase = -mylo * vy * vx - lo1 * vx - lo2;
+        unsigned m, sh;
+        fastdiv_magic((unsigned)vx, m, sh);
+        geom.vfm_x = m;
+        geom.vfs_x = sh;
+        fastdiv_magic((unsigned)vy, m, sh);
+        geom.vfm_y = m;
+        geom.vfs_y = sh;
+    }
     if (lane == 0) {
         geom.staged = ok ? 1 : 0;
         geom.total = ok ? (int)total : 0;
@@ -390,16 +420,25 @@ __device__ __forceinline__ void stage_tile(const EvalArgs<T>& a, const TileGeom&
     }
     cp_async_wait_all();
     if constexpr (kVec > 0) {
-        // row-vector layout: vtile[e] = (tile[e], ..., tile[e+kVec-1]) so a point's row of
-        // kVec taps along the contiguous axis is ONE shared-memory load
+        // row-vector layout (coset 0): vtile[(z*vy + y)*vx + x] = (tile[e], ..., tile[e+kVec-1])
+        // with e the dense index of (z, y, x), so a point's row of kVec taps along the
+        // contiguous axis is ONE shared-memory load; padded pitches avoid bank conflicts
         __syncthreads();
-        const int total = geom.total;
-        for (int e = tid; e < total; e += kThreads) {
-            V v;
-            T* pv = reinterpret_cast<T*>(&v);
+        const int vt = geom.vtotal, vx = geom.vx, vy = geom.vy;
+        const int ex = geom.ex[0][2], ey = geom.ex[0][1];
+        for (int e = tid; e < vt; e += kThreads) {
+            const int r = (int)fastdiv((unsigned)e, geom.vfm_x, geom.vfs_x);
+            const int x = e - r * vx;
+            const int z = (int)fastdiv((unsigned)r, geom.vfm_y, geom.vfs_y);
+            const int y = r - z * vy;
+            if (x < ex && y < ey) {
+                const int d = (z * ey + y) * ex + x;
+                V v;
+                T* pv = reinterpret_cast<T*>(&v);
 #pragma unroll
-            for (int q = 0; q < kVec; ++q) pv[q] = tile[e + q];
-            vtile[e] = v;
+                for (int q = 0; q < kVec; ++q) pv[q] = tile[d + q];
+                vtile[e] = v;
+            }
         }
     }
 }
@@ -580,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     V* vtile = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(tile) +
                                     (((a.tile_cap + 4) * (int)sizeof(T) + 15) & ~15));
     // pair-mode leftover queue (brick-relative point offsets) after the tiles
-    int* pq = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(vtile) + (size_t)a.tile_cap * kVec * sizeof(T));
+    int* pq = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(vtile) + (size_t)a.vec_cap * kVec * sizeof(T));
     const int B = 1 << log2b;
 
     for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {

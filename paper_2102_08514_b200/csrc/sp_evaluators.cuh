@@ -85,10 +85,8 @@ struct TensorBSplineEval {
             BWeights<DEG>::w(xa[i] - floor(xa[i]), wa[i]);
             BWeights<DEG>::w(xb[i] - floor(xb[i]), wb[i]);
         }
-        const TileGeom& g = *ctx.geom;
-        const int s0 = ctx.st0[0], s1 = ctx.st1[0];
-        const auto* p = f.vtile + (ctx.cbase[0] + X[0] * s0 + X[1] * s1 + X[2] - DEG * (s0 + s1 + 1));
-        (void)g;
+        const int s0 = ctx.vst0, s1 = ctx.vst1;
+        const auto* p = f.vtile + (ctx.vbase + X[0] * s0 + X[1] * s1 + X[2] - DEG * (s0 + s1 + 1));
         T acc_a = T(0), acc_b = T(0);
 #pragma unroll
         for (int a0 = 0; a0 <= DEG; ++a0) {
@@ -128,13 +126,14 @@ struct TensorBSplineEval {
         T acc = T(0);
         if constexpr (F::kIsTile && vec_width<T>() > 0) {
             // staged row-vector tile: one vector load per (a0, a1) row
-            const auto* p = f.vtile + (f.a0 - DEG * (f.c0 + f.c1 + 1));
+            const int s0 = ctx.vst0, s1 = ctx.vst1;
+            const auto* p = f.vtile + (ctx.vbase + cell[0] * s0 + cell[1] * s1 + cell[2] - DEG * (s0 + s1 + 1));
 #pragma unroll
             for (int a0 = 0; a0 <= DEG; ++a0) {
                 T acc1 = T(0);
 #pragma unroll
                 for (int a1 = 0; a1 <= DEG; ++a1) {
-                    const auto q = p[a0 * f.c0 + a1 * f.c1];
+                    const auto q = p[a0 * s0 + a1 * s1];
                     const T* qv = reinterpret_cast<const T*>(&q);
                     T acc2 = T(0);
 #pragma unroll

@@ -487,7 +487,14 @@ int build_args(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     a.trec_bytes = p->kind == SP_KIND_GENERATED ? p->M * p->N * 16 : 0;
     // row-vector tile (fp32 tensor-product kernels): +vec*sizeof(T) bytes per tile element
     vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
-    a.tile_cap = tile_bytes() / (int)(sizeof(T) * (1 + vec));
+    if (vec) {
+        // scalar staging tile + padded row-vector tile (~1.5x the scalar capacity)
+        a.tile_cap = tile_bytes() / (int)(sizeof(T) * (1 + vec * 3 / 2));
+        a.vec_cap = a.tile_cap * 3 / 2;
+    } else {
+        a.tile_cap = tile_bytes() / (int)sizeof(T);
+        a.vec_cap = 0;
+    }
     a.stats = g_stats;
     a.ppt = choose_ppt(p, g, n);
     bool shifted = false;
@@ -503,7 +510,7 @@ template <typename T>
 size_t tile_smem(const sp::EvalArgs<T>& a, int vec, size_t esz) {
     return (size_t)((a.table_bytes + 15) & ~15) + (size_t)a.trec_bytes +
            ((((size_t)a.tile_cap + 4) * esz + 15) & ~(size_t)15) +
-           (size_t)a.tile_cap * vec * esz;
+           (size_t)a.vec_cap * vec * esz;
 }
 
 template <typename T>
@@ -571,7 +578,7 @@ int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
 template <typename T>
 int brick_log2_typed(const sp_plan* p) {
     const int vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
-    const long long cap = tile_bytes() / (long long)(sizeof(T) * (1 + vec));
+    const long long cap = tile_bytes() / (long long)(sizeof(T) * (1 + vec * 3 / 2));
     bool shifted = false;
     for (int k = 0; k < p->M; ++k)
         for (int i = 0; i < 3; ++i) shifted |= p->shifts[k][i] != 0;
