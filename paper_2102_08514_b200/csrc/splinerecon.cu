@@ -589,8 +589,11 @@ int brick_log2_typed(const sp_plan* p) {
         for (int k = 0; k < p->M; ++k) {
             long long vol = 1;
             for (int i = 0; i < 3; ++i) {
-                const int d = p->diag[i];
-                const long long ext = (B + d - 1) / d + 1 + (p->reach_hi[i] - p->reach_lo[i]) + 2 * margin;
+                const int d = p->diag[i], l = p->shifts[k][i];
+                auto fdiv = [](long long a, long long b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+                // coset cells covered by the unit cells [0, B-1] of an aligned brick
+                const long long cells = fdiv(B - 1 - l, d) - fdiv(-l, d) + 1;
+                const long long ext = cells + (p->reach_hi[i] - p->reach_lo[i]) + 2 * margin;
                 vol *= ext;
             }
             total += vol;
