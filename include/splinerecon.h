@@ -129,15 +129,13 @@ int sp_eval(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int6
  * grouped into aligned bricks of (2^log2_brick)^3 unit cells; brick_start (device int64,
  * n_bricks+1 entries) delimits each brick's run of points.  One CTA stages a brick's
  * coefficient box (+ halo) once and evaluates all its points.  Results go to
- * out[out_index[i]] when out_index (device int64 [n]) is given, else out[i].  max_brick (host
- * value, <= 0 if unknown) is the largest number of points in one brick; it sizes the
- * same-cell pairing queue of the fp32 tensor-product kernel.  Same arithmetic as sp_eval,
- * bit-identical results.  Any brick partition is correct (points outside their run's brick
- * are evaluated without staging).
+ * out[out_index[i]] when out_index (device int64 [n]) is given, else out[i].  Same
+ * arithmetic as sp_eval, bit-identical results.  Any brick partition is correct (points
+ * outside their run's brick are evaluated without staging).
  */
 int sp_eval_bricks(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
-                   const int64_t* brick_start, int32_t n_bricks, int32_t log2_brick, int32_t max_brick,
-                   const int64_t* out_index, void* out, int32_t* err_flag, void* stream);
+                   const int64_t* brick_start, int32_t n_bricks, int32_t log2_brick, const int64_t* out_index,
+                   void* out, int32_t* err_flag, void* stream);
 
 /* Recommended log2 brick edge for a plan and dtype (largest brick whose box fits the tile),
  * or a negative value when brick mode is not applicable. */

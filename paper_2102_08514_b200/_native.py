@@ -107,8 +107,7 @@ EXPORTS = {
     "sp_eval_bricks": (
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.POINTER(GridDesc), ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
-         ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-         ctypes.c_void_p],
+         ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
     ),
     "sp_brick_log2": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "sp_last_error": (ctypes.c_char_p, []),

@@ -352,9 +352,6 @@ __device__ __forceinline__ int classify_fast(const float frac[3], const int X[3]
 template <typename T>
 struct Eval {{
     static constexpr int kMinBlocks = {min_blocks};
-    static constexpr bool kPairRuns = false;
-    template <class F, class Ctx>
-    __device__ static void run_pair(const T*, const T*, const int*, bool, const F&, const Ctx&, T&, T&) {{}}
     template <typename U>
     static constexpr int vec_width() {{
         return 0;

@@ -63,7 +63,6 @@ struct EvalArgs {
     unsigned long long* stats;  // nullable: [0] staged chunks, [1] unstaged chunks, [2] staged elements
     const long long* out_index; // nullable: value of point i goes to out[out_index[i]]
     int trec_bytes;             // per-(coset, class) tile records (generated kernels), in smem
-    int pair_queue;             // brick mode, pair evaluators: leftover-queue capacity (points)
     int vec_cap;                // row-vector tile capacity in elements (0: no row-vector tile)
 };
 
@@ -602,7 +601,6 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ TileGeom geom;
     __shared__ int red[6];
-    __shared__ int pq_count;
     constexpr int kVec = Ev::template vec_width<T>();
     using V = typename VecT<T, kVec>::type;
 
@@ -618,8 +616,6 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     T* tile = reinterpret_cast<T*>(smem + tb + a.trec_bytes);
     V* vtile = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(tile) +
                                     (((a.tile_cap + 4) * (int)sizeof(T) + 15) & ~15));
-    // pair-mode leftover queue (brick-relative point offsets) after the tiles
-    int* pq = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(vtile) + (size_t)a.vec_cap * kVec * sizeof(T));
     const int B = 1 << log2b;
 
     for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
@@ -654,93 +650,6 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         ctx.trec = trec;
         ctx.err = 0;
         ctx.load_geom(geom, a.fr.M);
-        if constexpr (Ev::kPairRuns) {
-            if (staged && a.dbg == nullptr && p1 - p0 <= (long long)a.pair_queue) {
-                // Register reuse for Morton-sorted points: thread q takes the consecutive pair
-                // (2q, 2q+1) of the brick (a warp covers 64 consecutive points, so lanes stay
-                // spatially coherent).  When both points lie in the same cell (the common case
-                // at several points per cell) they are evaluated against ONE set of row loads.
-                // Every other point (second point of a split pair, points outside the brick,
-                // non-finite points) is queued and evaluated in a leftover pass; the queue holds
-                // a whole brick, so it cannot overflow.  Same arithmetic per point as the
-                // single-point path.
-                if (tid == 0) pq_count = 0;
-                __syncthreads();
-                const long long cnt = p1 - p0;
-                const long long npairs = (cnt + 1) / 2;
-#pragma unroll 1
-                for (long long qb = 0; qb < npairs; qb += kThreads) {  // block-uniform trip count
-                    const long long q = qb + tid;
-                    const bool act = q < npairs;
-                    const long long j = p0 + 2 * (act ? q : 0);
-                    const bool havb = act && j + 1 < p1;
-                    const T* px = a.pts + 3 * j;
-                    const T xa[3] = {__ldg(px), __ldg(px + 1), __ldg(px + 2)};
-                    T xb[3] = {T(0), T(0), T(0)};
-                    if (havb) {
-                        xb[0] = __ldg(px + 3);
-                        xb[1] = __ldg(px + 4);
-                        xb[2] = __ldg(px + 5);
-                    }
-                    int Xa[3], Xb[3];
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        Xa[i] = clamp_cell(xa[i]);
-                        Xb[i] = clamp_cell(xb[i]);
-                    }
-                    const bool oka = act && isfinite(xa[0]) && isfinite(xa[1]) && isfinite(xa[2]) &&
-                                     (unsigned)(Xa[0] - c0) < (unsigned)B && (unsigned)(Xa[1] - c1) < (unsigned)B &&
-                                     (unsigned)(Xa[2] - c2) < (unsigned)B;
-                    const bool same = oka && havb && isfinite(xb[0]) && isfinite(xb[1]) && isfinite(xb[2]) &&
-                                      Xa[0] == Xb[0] && Xa[1] == Xb[1] && Xa[2] == Xb[2];
-                    {
-                        TileFetch<T, V> f;
-                        f.tile = tile;
-                        f.vtile = vtile;
-                        T va, vb;
-                        // (for !oka lanes the tile address is clamped into range; result unused)
-                        int Xs[3];
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) Xs[i] = oka ? Xa[i] : (i == 0 ? c0 : (i == 1 ? c1 : c2));
-                        Ev::run_pair(xa, xb, Xs, same, f, ctx, va, vb);
-                        if (oka) store_out(a, j, va);
-                        if (same) store_out(a, j + 1, vb);
-                    }
-                    // queue what was not evaluated (warp-aggregated slot allocation)
-                    const int na = (act && !oka) ? 1 : 0;
-                    const int nb = (havb && !same) ? 1 : 0;
-                    int mine = na + nb;
-                    int incl = mine;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += v;
-                    }
-                    const int tot = __shfl_sync(0xffffffffu, incl, 31);
-                    int base = 0;
-                    if (lane == 31 && tot) base = atomicAdd(&pq_count, tot);
-                    base = __shfl_sync(0xffffffffu, base, 31);
-                    int pos = base + incl - mine;
-                    if (na) pq[pos++] = (int)(j - p0);
-                    if (nb) pq[pos] = (int)(j + 1 - p0);
-                }
-                __syncthreads();
-                const int nq = pq_count;
-#pragma unroll 1
-                for (int t = tid; t < nq; t += kThreads) {
-                    const long long j = p0 + pq[t];
-                    const T* pb = a.pts + 3 * j;
-                    const T x1[3] = {__ldg(pb), __ldg(pb + 1), __ldg(pb + 2)};
-                    ctx.index = j;
-                    ctx.X[0] = clamp_cell(x1[0]);
-                    ctx.X[1] = clamp_cell(x1[1]);
-                    ctx.X[2] = clamp_cell(x1[2]);
-                    store_out(a, j, eval_one<T, Ev, V>(x1, staged, c0, c1, c2, B, tile, vtile, ctx));
-                }
-                __syncthreads();
-                continue;
-            }
-        }
         // software-pipelined point loads: the next point is in flight while this one is evaluated
         T xn0 = T(0), xn1 = T(0), xn2 = T(0);
         if (p0 + tid < p1) {

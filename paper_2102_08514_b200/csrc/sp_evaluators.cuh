@@ -68,49 +68,12 @@ struct BWeights<3> {
 template <typename T, int DEG>
 struct TensorBSplineEval {
     static constexpr int kMinBlocks = sizeof(T) == 4 ? 4 : 3;  // <= 64 / 80 registers
-    static constexpr bool kPairRuns = sizeof(T) == 4;          // brick-mode same-cell pairs
     __device__ static void tile_records(const EvalArgs<T>&, const TileGeom&, const unsigned char*, int4*, int) {}
     // fp32: rows of DEG+1 taps are one LDS.64 / LDS.128 from the row-vector tile
     template <typename U>
     static constexpr int vec_width() {
         return sizeof(U) == 4 ? (DEG == 1 ? 2 : 4) : 0;
     }
-    // Point a (and point b when `pair`, same cell) on the staged row-vector tile.
-    template <class F, class Ctx>
-    __device__ __forceinline__ static void run_pair(const T xa[3], const T xb[3], const int X[3], bool pair,
-                                                    const F& f, const Ctx& ctx, T& va, T& vb) {
-        T wa[3][DEG + 1], wb[3][DEG + 1];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            BWeights<DEG>::w(xa[i] - floor(xa[i]), wa[i]);
-            BWeights<DEG>::w(xb[i] - floor(xb[i]), wb[i]);
-        }
-        const int s0 = ctx.vst0, s1 = ctx.vst1;
-        const auto* p = f.vtile + (ctx.vbase + X[0] * s0 + X[1] * s1 + X[2] - DEG * (s0 + s1 + 1));
-        T acc_a = T(0), acc_b = T(0);
-#pragma unroll
-        for (int a0 = 0; a0 <= DEG; ++a0) {
-            T s1a = T(0), s1b = T(0);
-#pragma unroll
-            for (int a1 = 0; a1 <= DEG; ++a1) {
-                const auto q = p[a0 * s0 + a1 * s1];
-                const T* qv = reinterpret_cast<const T*>(&q);
-                T s2a = T(0), s2b = T(0);
-#pragma unroll
-                for (int a2 = 0; a2 <= DEG; ++a2) {
-                    s2a = fma(wa[2][a2], qv[a2], s2a);
-                    s2b = fma(wb[2][a2], qv[a2], s2b);
-                }
-                s1a = fma(wa[1][a1], s2a, s1a);
-                s1b = fma(wb[1][a1], s2b, s1b);
-            }
-            acc_a = fma(wa[0][a0], s1a, acc_a);
-            acc_b = fma(wb[0][a0], s1b, acc_b);
-        }
-        va = acc_a;
-        vb = pair ? acc_b : T(0);
-    }
-
     template <class F, class Ctx>
     __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {
         int cell[3];
@@ -217,9 +180,7 @@ __device__ __forceinline__ T generic_poly(const GenericTables& gt, int p, const 
 template <typename T>
 struct GenericEval {
     static constexpr int kMinBlocks = 1;
-    static constexpr bool kPairRuns = false;
-    template <class F, class Ctx>
-    __device__ static void run_pair(const T*, const T*, const int*, bool, const F&, const Ctx&, T&, T&) {}
+
     __device__ static void tile_records(const EvalArgs<T>&, const TileGeom&, const unsigned char*, int4*, int) {}
     template <typename U>
     static constexpr int vec_width() {

@@ -606,7 +606,7 @@ int brick_log2_typed(const sp_plan* p) {
 template <typename T>
 int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, const int64_t* bstart,
                       int32_t nbricks, int32_t log2b, const int64_t* out_index, void* out, int32_t* err,
-                      cudaStream_t st, int max_brick) {
+                      cudaStream_t st) {
     sp::EvalArgs<T> a;
     int vec = 0;
     int rc = build_args<T>(p, g, pts, n, out, nullptr, err, a, vec);
@@ -614,10 +614,7 @@ int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, 
     a.out_index = reinterpret_cast<const long long*>(out_index);
     Kernels<T> k;
     if ((rc = select_kernels<T>(p, k)) != SP_OK) return rc;
-    // pair mode (fp32 tensor-product): leftover queue sized for the largest brick, capped
-    const bool pairs = p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4 && max_brick > 0;
-    a.pair_queue = pairs ? std::min(max_brick, 8192) : 0;
-    const size_t smem = tile_smem(a, vec, sizeof(T)) + (size_t)a.pair_queue * sizeof(int);
+    const size_t smem = tile_smem(a, vec, sizeof(T));
     const long long cap = (long long)p->num_sms * k.bocc(smem);
     const int blocks = (int)std::max<long long>(1, std::min<long long>(nbricks, cap));
     cudaError_t e = k.brick(a, reinterpret_cast<const long long*>(bstart), nbricks, log2b, blocks, smem, st);
@@ -681,7 +678,7 @@ extern "C" int sp_brick_log2(const sp_plan* plan, int32_t dtype) {
 }
 
 extern "C" int sp_eval_bricks(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
-                              const int64_t* brick_start, int32_t n_bricks, int32_t log2_brick, int32_t max_brick,
+                              const int64_t* brick_start, int32_t n_bricks, int32_t log2_brick,
                               const int64_t* out_index, void* out, int32_t* err_flag, void* stream) {
     if (!plan) return fail(SP_ERR_INVALID, "null plan");
     int rc = check_grid(plan, grid, dtype);
@@ -693,10 +690,10 @@ extern "C" int sp_eval_bricks(const sp_plan* plan, const sp_grid_desc* grid, con
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (dtype == SP_F32)
         return eval_bricks_typed<float>(plan, grid, pts, n, brick_start, n_bricks, log2_brick, out_index, out, err_flag,
-                                        st, max_brick);
+                                        st);
     if (dtype == SP_F64)
         return eval_bricks_typed<double>(plan, grid, pts, n, brick_start, n_bricks, log2_brick, out_index, out, err_flag,
-                                         st, max_brick);
+                                         st);
     return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
 }
 

@@ -351,7 +351,6 @@ class PlanInterpreter:
             with torch.cuda.stream(st):
                 _native.check(lib.sp_eval_bricks(h, ctypes.byref(gdesc), batch.pts.data_ptr(), n, dtype,
                                                  batch.brick_start.data_ptr(), batch.n_bricks, batch.log2_brick,
-                                                 min(batch.max_brick, 2**31 - 1),
                                                  None if idx is None else idx.data_ptr(), res.data_ptr(),
                                                  None if err is None else err.data_ptr(), st.cuda_stream))
         if check and int(err.item()):
