@@ -489,8 +489,10 @@ int build_args(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
     if (vec) {
         // scalar staging tile + padded row-vector tile (~1.5x the scalar capacity)
-        a.tile_cap = tile_bytes() / (int)(sizeof(T) * (1 + vec * 3 / 2));
-        a.vec_cap = a.tile_cap * 3 / 2;
+        // SP_VPAD=1: bank-conflict-padded row-vector tile (tuning knob; dense measured faster)
+        const bool pad = env_int("SP_VPAD", 0) != 0;
+        a.tile_cap = tile_bytes() / (int)(sizeof(T) * (1 + (pad ? vec * 3 / 2 : vec)));
+        a.vec_cap = pad ? a.tile_cap * 3 / 2 : a.tile_cap;
     } else {
         a.tile_cap = tile_bytes() / (int)sizeof(T);
         a.vec_cap = 0;
