@@ -158,6 +158,19 @@ int sp_scatter(const void* src, const int64_t* perm, int64_t n, int32_t dtype, v
 /* dst[i] = pts[perm[i]] (s=3 points) — gather points into sorted order. */
 int sp_gather_points(const void* pts, const int64_t* perm, int64_t n, int32_t dtype, void* dst, void* stream);
 
+/*
+ * Hardware-texture-filtered variant (the paper's GPU fetch path),
+ * reported separately from the exact kernels because texture filtering weights are 9-bit
+ * fixed point: 3-D CUDA array copy of a single-coset float32 grid with linear filtering
+ * (boundary zero -> border, clamp -> clamp; mirror is not expressible: the hardware mirror
+ * period is 2n, runtime.py:191-196 uses 2n-2).  Tensor-product plans of degree 1 (one
+ * filtered fetch per point) and 3 (eight fetches per point).
+ */
+typedef struct sp_texture sp_texture;
+int sp_texture_create(const sp_grid_desc* grid, sp_texture** out);
+void sp_texture_destroy(sp_texture* tex);
+int sp_eval_texture(const sp_plan* plan, const sp_texture* tex, const void* pts, int64_t n, void* out, void* stream);
+
 /* Staging statistics for tuning (not thread-safe): copies the counters accumulated since the
  * last call into out[4] = {staged chunks, unstaged chunks, staged tile elements, 0} (when
  * out != NULL), then enables (1, counters reset) or disables (0) collection. */

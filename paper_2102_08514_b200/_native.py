@@ -110,6 +110,11 @@ EXPORTS = {
          ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
     ),
     "sp_brick_log2": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
+    "sp_texture_create": (ctypes.c_int, [ctypes.POINTER(GridDesc), ctypes.POINTER(ctypes.c_void_p)]),
+    "sp_texture_destroy": (None, [ctypes.c_void_p]),
+    "sp_eval_texture": (
+        ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+    ),
     "sp_last_error": (ctypes.c_char_p, []),
     "sp_version": (ctypes.c_char_p, []),
 }

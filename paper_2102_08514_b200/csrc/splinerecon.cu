@@ -74,6 +74,10 @@ bool signed_perm(const double* m, int perm[3], int sign[3]) {
 
 }  // namespace
 
+namespace sp {
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace sp
+
 struct sp_plan {
     sp_kernel_kind kind = SP_KIND_GENERIC;
     std::string name;

@@ -244,6 +244,8 @@ class PlanInterpreter:
         try:
             lib = _native._lib
             if lib is not None:
+                for t in self.__dict__.get("_tex", {}).values():
+                    lib.sp_texture_destroy(t)
                 for h in self._handles.values():
                     lib.sp_plan_destroy(h)
         except Exception:
@@ -355,6 +357,37 @@ class PlanInterpreter:
                                                  None if err is None else err.data_ptr(), st.cuda_stream))
         if check and int(err.item()):
             raise RuntimeError_("sigma sentinel hit in batch evaluation")
+        return res
+
+    def eval_batch_texture(self, grid: CoefficientGrid, pts: torch.Tensor, *, out: torch.Tensor | None = None,
+                           stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """Hardware-texture-filtered variant (sp_eval_texture): the paper's GPU fetch path with
+        9-bit texture filtering weights — NOT within the exact tolerances; reported
+        separately with its measured error.  fp32 single-coset grids, TP degree 1 or 3."""
+        self._check_grid(grid)
+        lib = _native.lib()
+        h = self._handle(grid.device)
+        key = (id(grid), tuple(a.data_ptr() for a in grid.arrays))
+        cache = self.__dict__.setdefault("_tex", {})
+        tex = cache.get(key)
+        if tex is None:
+            for old in cache.values():
+                lib.sp_texture_destroy(old)
+            cache.clear()
+            gd = grid.descriptor()
+            hnd = ctypes.c_void_p()
+            code = lib.sp_texture_create(ctypes.byref(gd), ctypes.byref(hnd))
+            if code == _native.SP_ERR_UNSUPPORTED:
+                raise NotImplementedError(lib.sp_last_error().decode())
+            _native.check(code)
+            tex = cache[key] = hnd.value
+        p = pts.to(device=grid.device, dtype=torch.float32).contiguous()
+        res = out if out is not None else torch.empty(p.shape[0], dtype=torch.float32, device=grid.device)
+        st = stream if stream is not None else torch.cuda.current_stream(grid.device)
+        code = lib.sp_eval_texture(h, tex, p.data_ptr(), p.shape[0], res.data_ptr(), st.cuda_stream)
+        if code == _native.SP_ERR_UNSUPPORTED:
+            raise NotImplementedError(lib.sp_last_error().decode())
+        _native.check(code)
         return res
 
     def classify(self, grid: CoefficientGrid, pts: torch.Tensor):

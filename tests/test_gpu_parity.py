@@ -179,3 +179,20 @@ def test_brick_mode_matches_chunk_mode(name, dtype, cuda):
     presorted = interp.prepare(grid, sorted_pts, presorted=True)
     c = interp.eval_batch(grid, presorted)
     torch.testing.assert_close(interp.eval_batch(grid, sorted_pts), c, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("name,deg", [("cc_trilinear", 1), ("cc_tricubic", 3)])
+def test_texture_variant_error_is_bounded(name, deg, cuda):
+    """The hardware-filtered variant is NOT exact (9-bit filtering weights); it is reported
+    separately.  Check it tracks the exact kernel to ~1e-2 of max|f| and is not exact."""
+    g, plan, grid = _setup(name, "zero", torch.float32, cuda)
+    interp = PlanInterpreter(plan)
+    pts = torch.from_numpy(g["pts"]).to(cuda)
+    exact = interp.eval_batch(grid, pts)
+    tex = interp.eval_batch_texture(grid, pts)
+    ok = torch.isfinite(exact)
+    err = (tex[ok] - exact[ok]).abs().max().item() / exact[ok].abs().max().item()
+    assert err < 2e-2
+    with pytest.raises(NotImplementedError):
+        _, p2, g2 = _setup("bcc_linear_rd", "zero", torch.float32, cuda)
+        PlanInterpreter(p2).eval_batch_texture(g2, pts)
