@@ -153,6 +153,11 @@ int sp_eval_launch_count(const sp_plan* plan, int64_t n);
  * keys device uint64 [n]. */
 int sp_morton_keys(const void* pts, int64_t n, int32_t dtype, uint64_t* keys, void* stream);
 
+/* 30-bit Morton keys of (floor(x) - lo), each axis clamped to [0, 2^bits), bits <= 10:
+ * the same order as sp_morton_keys inside the box, half the sort width. keys device int32 [n]. */
+int sp_morton_keys32(const void* pts, int64_t n, int32_t dtype, int32_t lo0, int32_t lo1, int32_t lo2, int32_t bits,
+                     int32_t* keys, void* stream);
+
 /* out[perm[i]] = src[i]  (float or double, by dtype) — unpermute results of a sorted batch. */
 int sp_scatter(const void* src, const int64_t* perm, int64_t n, int32_t dtype, void* out, void* stream);
 /* dst[i] = pts[perm[i]] (s=3 points) — gather points into sorted order. */

@@ -97,6 +97,11 @@ EXPORTS = {
     ),
     "sp_eval_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),
     "sp_morton_keys": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]),
+    "sp_morton_keys32": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+         ctypes.c_void_p, ctypes.c_void_p],
+    ),
     "sp_scatter": (
         ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
     ),

@@ -753,6 +753,20 @@ __global__ void morton_kernel(const T* __restrict__ pts, long long n, uint64_t* 
     }
 }
 
+// 30-bit Morton keys of cells relative to lo (each axis clamped to [0, 2^bits)), for fast
+// 32-bit radix sorts when the batch's bounding box is small (<= 1024 cells per axis).
+template <typename T>
+__global__ void morton32_kernel(const T* __restrict__ pts, long long n, int lo0, int lo1, int lo2, int bits,
+                                int* __restrict__ keys) {
+    const int hi = (1 << bits) - 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int c0 = min(max(sp::clamp_cell(pts[3 * i]) - lo0, 0), hi);
+        const int c1 = min(max(sp::clamp_cell(pts[3 * i + 1]) - lo1, 0), hi);
+        const int c2 = min(max(sp::clamp_cell(pts[3 * i + 2]) - lo2, 0), hi);
+        keys[i] = (int)(spread3((uint32_t)c2) | (spread3((uint32_t)c1) << 1) | (spread3((uint32_t)c0) << 2));
+    }
+}
+
 template <typename T>
 __global__ void scatter_kernel(const T* __restrict__ src, const int64_t* __restrict__ perm, long long n, T* __restrict__ out) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -781,6 +795,18 @@ extern "C" int sp_morton_keys(const void* pts, int64_t n, int32_t dtype, uint64_
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (dtype == SP_F32) morton_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, n, keys);
     else if (dtype == SP_F64) morton_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, n, keys);
+    else return fail(SP_ERR_INVALID, "unknown dtype");
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
+
+extern "C" int sp_morton_keys32(const void* pts, int64_t n, int32_t dtype, int32_t lo0, int32_t lo1, int32_t lo2,
+                                int32_t bits, int32_t* keys, void* stream) {
+    if (n <= 0) return SP_OK;
+    if (bits < 0 || bits > 10) return fail(SP_ERR_INVALID, "bits must be in [0, 10]");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32) morton32_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, n, lo0, lo1, lo2, bits, keys);
+    else if (dtype == SP_F64) morton32_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, n, lo0, lo1, lo2, bits, keys);
     else return fail(SP_ERR_INVALID, "unknown dtype");
     SP_CUDA(cudaGetLastError());
     return SP_OK;

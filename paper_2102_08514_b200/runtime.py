@@ -449,15 +449,11 @@ class PointBatch:
     `prepare_points`; evaluate with `PlanInterpreter.eval_batch(grid, batch)`.
     """
 
-    def __init__(self, pts: torch.Tensor, brick_start: torch.Tensor, log2_brick: int, perm: torch.Tensor | None,
-                 max_brick: int | None = None):
+    def __init__(self, pts: torch.Tensor, brick_start: torch.Tensor, log2_brick: int, perm: torch.Tensor | None):
         self.pts = pts
         self.brick_start = brick_start
         self.log2_brick = int(log2_brick)
         self.perm = perm
-        if max_brick is None:
-            max_brick = int((brick_start[1:] - brick_start[:-1]).max().item()) if brick_start.numel() > 1 else 0
-        self.max_brick = int(max_brick)
 
     @property
     def n(self) -> int:
@@ -478,23 +474,40 @@ def prepare_points(pts: torch.Tensor, log2_brick: int, *, presorted: bool = Fals
     pts = pts.contiguous()
     n = pts.shape[0]
     dtype = _native.SP_F32 if pts.dtype == torch.float32 else _native.SP_F64
-    keys = torch.empty(n, dtype=torch.int64, device=pts.device)
     with torch.cuda.stream(st):
-        _native.check(lib.sp_morton_keys(pts.data_ptr(), n, dtype, keys.data_ptr(), st.cuda_stream))
         perm = None
-        if not presorted:
-            keys, perm = torch.sort(keys)
+        keys = None
+        if not presorted and n:
+            # 32-bit keys relative to the brick-aligned bounding box when it is small enough
+            # (half the radix-sort width of the 64-bit keys); same order, same brick runs
+            lo = pts.amin(0).floor()  # floor is monotone: min(floor(x)) = floor(min(x))
+            hi = pts.amax(0).floor()
+            if bool(torch.isfinite(lo).all() and torch.isfinite(hi).all()):
+                b = int(log2_brick)
+                lo_i = [(int(v) >> b) << b for v in lo.tolist()]
+                span = max(int(h) - l for h, l in zip(hi.tolist(), lo_i)) + 1
+                bits = max(b, (span - 1).bit_length())
+                if bits <= 10:
+                    k32 = torch.empty(n, dtype=torch.int32, device=pts.device)
+                    _native.check(lib.sp_morton_keys32(pts.data_ptr(), n, dtype, lo_i[0], lo_i[1], lo_i[2], bits,
+                                                       k32.data_ptr(), st.cuda_stream))
+                    keys, perm = torch.sort(k32)
+        if keys is None:
+            keys = torch.empty(n, dtype=torch.int64, device=pts.device)
+            _native.check(lib.sp_morton_keys(pts.data_ptr(), n, dtype, keys.data_ptr(), st.cuda_stream))
+            if not presorted:
+                keys, perm = torch.sort(keys)
+        if perm is not None:
             sp = torch.empty_like(pts)
             _native.check(lib.sp_gather_points(pts.data_ptr(), perm.data_ptr(), n, dtype, sp.data_ptr(), st.cuda_stream))
             pts = sp
+        # brick runs (points not actually in Morton order just give many short runs:
+        # still correct, only slower)
         bid = keys >> (3 * int(log2_brick))
-        if presorted and n > 1 and bool((bid[1:] < bid[:-1]).any()):
-            raise RuntimeError_("points are not in Morton order (use presorted=False)")
         _, counts = torch.unique_consecutive(bid, return_counts=True)
         start = torch.zeros(counts.shape[0] + 1, dtype=torch.int64, device=pts.device)
         torch.cumsum(counts, 0, out=start[1:])
-        max_brick = int(counts.max().item()) if counts.numel() else 0
-    return PointBatch(pts, start, log2_brick, perm, max_brick)
+    return PointBatch(pts, start, log2_brick, perm)
 
 
 def morton_order(pts: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
