@@ -209,80 +209,6 @@ def _kernel_function(plan: EvaluationPlan, kidx: int, d: int) -> tuple:
     return out, ops[0]
 
 
-def _lit2(q: Fraction) -> str:
-    return f"f2_bc((float){float(q)!r})"
-
-
-def _kernel_function_x2(plan: EvaluationPlan, kidx: int, d: int) -> list:
-    """The same weight program as _kernel_function, as packed float32 pairs (two points per
-    thread, FFMA2/FMUL2/FADD2): operation for operation identical, so bit-identical."""
-    kern = plan.kernels[kidx]
-    polys = [g.g for g in kern.groups] + [t for g in kern.groups for t in g.t_nums]
-    mono_lines, have, _ = _monomial_program(polys)
-    mono_lines = [ln.replace("const T ", "const F2 ").replace(" * y", ", y") for ln in mono_lines]
-    mono_lines = [_x2_mul(ln) for ln in mono_lines]
-    out = [
-        "template <class FA, class FB>",
-        f"__device__ __forceinline__ F2 kernel{kidx}_x2(const F2 y0, const F2 y1, const F2 y2, const FA& fa, const FB& fb) {{",
-        "    (void)y0; (void)y1; (void)y2;",
-    ]
-    out += [f"    {ln}" for ln in mono_lines]
-    out.append("    F2 acc = f2_bc(0.0f);")
-    for gi, g in enumerate(kern.groups):
-        body_lines = []
-        gname = _poly_expr_x2(g.g, have, body_lines, f"g{gi}")
-        tnames = [_poly_expr_x2(t, have, body_lines, f"tn{gi}_{j}") for j, t in enumerate(g.t_nums)]
-        body = ["    {"] + [f"        {ln}" for ln in body_lines]
-        sd = [tuple(v // d for v in site) for site in g.sites]
-        ns = len(g.span_axes)
-
-        def get(c):
-            a = f"{sd[c][0]}, {sd[c][1]}, {sd[c][2]}"
-            return f"f2_pack(fa.get({a}), fb.get({a}))"
-
-        if ns == 0:
-            body.append(f"        acc = f2_fma({gname}, {get(0)}, acc);")
-        elif ns == 1:
-            body.append(f"        const F2 c0 = {get(0)};")
-            body.append(f"        const F2 c1 = {get(1)};")
-            body.append(f"        acc = f2_fma({gname}, c0, acc);")
-            body.append(f"        acc = f2_fma({tnames[0]}, f2_sub(c1, c0), acc);")
-        else:
-            raise ValueError("x2 kernels support 1- and 2-site groups")
-        body.append("    }")
-        out.extend(body)
-    out.append("    return acc;")
-    out.append("}")
-    return out
-
-
-def _x2_mul(line: str) -> str:
-    # "const F2 m_xyz = m_parent, y1;" -> "const F2 m_xyz = f2_mul(m_parent, y1);"
-    if "=" in line and "," in line:
-        lhs, rhs = line.split("=", 1)
-        return f"{lhs}= f2_mul({rhs.strip().rstrip(';')});"
-    return line
-
-
-def _poly_expr_x2(poly, have, lines, tag) -> str:
-    terms = sorted(poly.terms.items(), key=lambda kv: (-sum(kv[0]), kv[0]))
-    if not terms:
-        return "f2_bc(0.0f)"
-    const = poly.terms.get((0, 0, 0))
-    var_terms = [(e, c) for e, c in terms if sum(e)]
-    if not var_terms:
-        return _lit2(const)
-    acc = _lit2(const) if const is not None else None
-    for e, c in var_terms:
-        m = have[tuple(e)]
-        if acc is None:
-            acc = f"f2_mul({_lit2(c)}, {m})" if c != 1 else m
-        else:
-            acc = f"f2_fma({_lit2(c)}, {m}, {acc})"
-    lines.append(f"const F2 {tag} = {acc};")
-    return tag
-
-
 def _plane_expr(normal) -> str:
     terms = []
     for i, n in enumerate(normal):
@@ -312,18 +238,14 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
     words = canonical_words(pack_plan(plan))
     kfuncs = []
     kflops = []
-    pair2 = all(len(g.span_axes) <= 1 for k in plan.kernels for g in k.groups)
     for kidx in range(plan.K):
         lines, fl = _kernel_function(plan, kidx, d)
         kfuncs.extend(lines)
         kfuncs.append("")
         kflops.append(fl)
-        if pair2:
-            kfuncs.extend(_kernel_function_x2(plan, kidx, d))
-            kfuncs.append("")
     sig_bytes = ((plan.r * 4) + 15) & ~15
     # occupancy hint for ptxas: light weight programs keep 4 CTAs (<= 64 regs) per SM
-    min_blocks = 4 if max(kflops) <= 64 else (2 if max(kflops) <= 300 else 1)
+    min_blocks = 4 if max(kflops) <= 64 else (2 if max(kflops) <= 700 else 1)
     planes = []
     for j, (n, off) in enumerate(plan.planes):
         planes.append(f"    q |= ({_plane_expr(n)} >= R({float(off)!r})) ? {1 << j} : 0;")
@@ -334,29 +256,6 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
     fast_lo = 1.0
     while fast_lo < max(rmax / 2.0, float(d), 1.0):
         fast_lo *= 2.0
-    if plan.K == 1:
-        dispatch2 = "            const F2 acc = kernel0_x2(p0, p1, p2, fa, fb);"
-    else:
-        c2 = "\n".join(
-            f"                    case {k}: acc = kernel{k}_x2(p0, p1, p2, fa, fb); break;" for k in range(plan.K)
-        )
-        ca = "\n".join(
-            f"                    case {k}: va = kernel{k}<T>(ya[0], ya[1], ya[2], fa); break;" for k in range(plan.K)
-        )
-        cb = "\n".join(
-            f"                    case {k}: vb = kernel{k}<T>(yb[0], yb[1], yb[2], fb); break;" for k in range(plan.K)
-        )
-        dispatch2 = (
-            "            F2 acc = f2_bc(0.0f);\n"
-            "            if (kern_a == kern_b) {\n"
-            f"                switch (kern_a) {{\n{c2}\n                }}\n"
-            "            } else {\n"
-            "                T va = T(0), vb = T(0);\n"
-            f"                switch (kern_a) {{\n{ca}\n                }}\n"
-            f"                switch (kern_b) {{\n{cb}\n                }}\n"
-            "                acc = f2_pack(va, vb);\n"
-            "            }"
-        )
     if plan.K == 1:
         dispatch = "            const T acc = kernel0<T>(y0, y1, y2, f);"
     else:
@@ -453,7 +352,6 @@ __device__ __forceinline__ int classify_fast(const float frac[3], const int X[3]
 template <typename T>
 struct Eval {{
     static constexpr int kMinBlocks = {min_blocks};
-    static constexpr bool kPair2 = {"true" if pair2 else "false"};
     template <typename U>
     static constexpr int vec_width() {{
         return 0;
@@ -479,62 +377,6 @@ struct Eval {{
             trec[idx] = make_int4(cf[0], cf[1], cf[2], z);
         }}
     }}
-    // tile frame of one point for coset k / class c (staged tile only)
-    template <class F, class Ctx>
-    __device__ __forceinline__ static void tile_frame(F& f, const Ctx& ctx, int k, int c, const int cell[3]) {{
-        const int4 tr = ctx.trec[k * kN + c];
-        f.a0 = ctx.cbase[k] + cell[0] * ctx.st0[k] + cell[1] * ctx.st1[k] + cell[2] + tr.w;
-        f.c0 = tr.x;
-        f.c1 = tr.y;
-        f.c2 = tr.z;
-    }}
-
-    // two points (staged tile, no debug output): scalar classification per point, packed
-    // FFMA2 weight programs; bit-identical to two eval() calls
-    template <class F, class Ctx>
-    __device__ __forceinline__ static void eval2(const T xa[3], const T xb[3], const int Xa[3], const int Xb[3],
-                                                 F& fa, F& fb, Ctx& ctx, T& out_a, T& out_b) {{
-        if constexpr (kPair2 && sizeof(T) == 4) {{
-            const int* sigma = reinterpret_cast<const int*>(ctx.tables);
-            const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
-            const float ma = fminf(fminf(fabsf(xa[0]), fabsf(xa[1])), fabsf(xa[2]));
-            const float Ma = fmaxf(fmaxf(fabsf(xa[0]), fabsf(xa[1])), fabsf(xa[2]));
-            const float mb = fminf(fminf(fabsf(xb[0]), fabsf(xb[1])), fabsf(xb[2]));
-            const float Mb = fmaxf(fmaxf(fabsf(xb[0]), fabsf(xb[1])), fabsf(xb[2]));
-            const bool fast_a = ma >= kFastLo && Ma < kFastHi, fast_b = mb >= kFastLo && Mb < kFastHi;
-            float frac_a[3], frac_b[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {{
-                frac_a[i] = (float)xa[i] - floorf((float)xa[i]);
-                frac_b[i] = (float)xb[i] - floorf((float)xb[i]);
-            }}
-            F2 total = f2_bc(0.0f);
-#pragma unroll
-            for (int k = 0; k < kM; ++k) {{
-                int cell_a[3], cell_b[3];
-                T ya[3], yb[3];
-                uint4 rec_a, rec_b;
-                const int ca = fast_a ? classify_fast<T>(frac_a, Xa, k, sigma, cls_tab, ctx.err, cell_a, ya, rec_a)
-                                      : classify_f64<T>(xa, k, sigma, cls_tab, ctx.err, cell_a, ya, rec_a);
-                const int cb = fast_b ? classify_fast<T>(frac_b, Xb, k, sigma, cls_tab, ctx.err, cell_b, yb, rec_b)
-                                      : classify_f64<T>(xb, k, sigma, cls_tab, ctx.err, cell_b, yb, rec_b);
-                const int kern_a = (int)(rec_a.x & 15u), kern_b = (int)(rec_b.x & 15u);
-                (void)kern_a;
-                (void)kern_b;
-                tile_frame(fa, ctx, k, ca, cell_a);
-                tile_frame(fb, ctx, k, cb, cell_b);
-                const F2 p0 = f2_pack(ya[0], yb[0]), p1 = f2_pack(ya[1], yb[1]), p2 = f2_pack(ya[2], yb[2]);
-                (void)p0;
-                (void)p1;
-                (void)p2;
-{dispatch2}
-                total = f2_add(total, acc);
-            }}
-            out_a = f2_lo(total);
-            out_b = f2_hi(total);
-        }}
-    }}
-
     template <class F, class Ctx>
     __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
         const EvalArgs<T>& a = *ctx.a;

@@ -264,49 +264,6 @@ __device__ __forceinline__ void cp_async_elem(void* smem_dst, const void* gsrc, 
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// Packed float32 pairs for the sm_100 FFMA2 / FMUL2 / FADD2 datapath: one instruction
-// performs the same IEEE operation on two independent points (bit-identical to the scalar
-// instructions), halving the issue slots of the weight programs.
-struct F2 {
-    unsigned long long v;
-};
-__device__ __forceinline__ F2 f2_pack(float lo, float hi) {
-    F2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
-    return r;
-}
-__device__ __forceinline__ F2 f2_bc(float c) { return f2_pack(c, c); }
-__device__ __forceinline__ float f2_lo(F2 x) {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x.v));
-    return lo;
-}
-__device__ __forceinline__ float f2_hi(F2 x) {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x.v));
-    return hi;
-}
-__device__ __forceinline__ F2 f2_fma(F2 a, F2 b, F2 c) {
-    F2 r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-    return r;
-}
-__device__ __forceinline__ F2 f2_mul(F2 a, F2 b) {
-    F2 r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ F2 f2_add(F2 a, F2 b) {
-    F2 r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-__device__ __forceinline__ F2 f2_sub(F2 a, F2 b) {
-    F2 r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
-    return r;
-}
-
 // Fast unsigned division by a runtime divisor (Granlund-Montgomery), valid for n < 2^31.
 __device__ __forceinline__ void fastdiv_magic(unsigned div, unsigned& m, unsigned& s) {
     s = 0;
@@ -631,31 +588,6 @@ __device__ __forceinline__ T eval_one(const T x[3], bool staged, int c0, int c1,
     return Ev::template eval<GlobalFetch<T>>(x, f, ctx);
 }
 
-// Out-of-line single-point evaluation for the pair loop's rare cases (non-finite points,
-// points outside their run's brick).  Arguments come through shared memory (a copy of the
-// kernel arguments), so taking their address does not spill the parameter block.
-template <typename T, class Ev, typename V>
-__device__ __noinline__ T eval_one_ool(const EvalArgs<T>* sa, const TileGeom* geom, const unsigned char* tables,
-                                       const int4* trec, const T* tile, const V* vtile, long long j, bool staged,
-                                       int c0, int c1, int c2, int B) {
-    EvalCtx<T, Ev> ctx;
-    ctx.a = sa;
-    ctx.tables = tables;
-    ctx.geom = geom;
-    ctx.trec = trec;
-    ctx.err = 0;
-    ctx.index = j;
-    ctx.load_geom(*geom, sa->fr.M);
-    const T* px = sa->pts + 3 * j;
-    const T x[3] = {px[0], px[1], px[2]};
-    ctx.X[0] = clamp_cell(x[0]);
-    ctx.X[1] = clamp_cell(x[1]);
-    ctx.X[2] = clamp_cell(x[2]);
-    const T v = eval_one<T, Ev, V>(x, staged, c0, c1, c2, B, tile, vtile, ctx);
-    if (ctx.err && sa->err) atomicOr(sa->err, 1);
-    return v;
-}
-
 // ---------------------------------------------------------------------------------------
 // Brick mode: points sorted by the Morton code of their unit cell are grouped into aligned
 // bricks of B^3 unit cells (B = 2^log2b); brick_start[b]..brick_start[b+1] are brick b's
@@ -669,8 +601,6 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ TileGeom geom;
     __shared__ int red[6];
-    __shared__ EvalArgs<T> sargs;  // argument copy for the out-of-line rare path
-    if (threadIdx.x == 0) sargs = a;
     constexpr int kVec = Ev::template vec_width<T>();
     using V = typename VecT<T, kVec>::type;
 
@@ -720,52 +650,6 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         ctx.trec = trec;
         ctx.err = 0;
         ctx.load_geom(geom, a.fr.M);
-        if constexpr (Ev::kPair2 && sizeof(T) == 4) {
-            if (staged && a.dbg == nullptr) {
-                // Two consecutive points per thread, their weight programs run as packed
-                // FFMA2/FMUL2 pairs (one instruction, two points); each point keeps its own
-                // classification and fetch frame.  Rare cases go out of line.
-                const long long cnt = p1 - p0;
-                const long long npairs = cnt / 2;
-#pragma unroll 1
-                for (long long q = tid; q < npairs; q += kThreads) {
-                    const long long j = p0 + 2 * q;
-                    const T* px = a.pts + 3 * j;
-                    const T xa[3] = {__ldg(px), __ldg(px + 1), __ldg(px + 2)};
-                    const T xb[3] = {__ldg(px + 3), __ldg(px + 4), __ldg(px + 5)};
-                    int Xa[3], Xb[3];
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        Xa[i] = clamp_cell(xa[i]);
-                        Xb[i] = clamp_cell(xb[i]);
-                    }
-                    const bool ok = isfinite(xa[0]) && isfinite(xa[1]) && isfinite(xa[2]) && isfinite(xb[0]) &&
-                                    isfinite(xb[1]) && isfinite(xb[2]) && (unsigned)(Xa[0] - c0) < (unsigned)B &&
-                                    (unsigned)(Xa[1] - c1) < (unsigned)B && (unsigned)(Xa[2] - c2) < (unsigned)B &&
-                                    (unsigned)(Xb[0] - c0) < (unsigned)B && (unsigned)(Xb[1] - c1) < (unsigned)B &&
-                                    (unsigned)(Xb[2] - c2) < (unsigned)B;
-                    T va, vb;
-                    if (ok) {
-                        TileFetch<T, V> fa, fb;
-                        fa.tile = fb.tile = tile;
-                        fa.vtile = fb.vtile = vtile;
-                        Ev::eval2(xa, xb, Xa, Xb, fa, fb, ctx, va, vb);
-                    } else {
-                        va = eval_one_ool<T, Ev, V>(&sargs, &geom, smem, trec, tile, vtile, j, staged, c0, c1, c2, B);
-                        vb = eval_one_ool<T, Ev, V>(&sargs, &geom, smem, trec, tile, vtile, j + 1, staged, c0, c1, c2,
-                                                    B);
-                    }
-                    store_out(a, j, va);
-                    store_out(a, j + 1, vb);
-                }
-                if ((cnt & 1) && tid == 0)
-                    store_out(a, p1 - 1,
-                              eval_one_ool<T, Ev, V>(&sargs, &geom, smem, trec, tile, vtile, p1 - 1, staged, c0, c1, c2, B));
-                if (ctx.err && a.err) atomicOr(a.err, 1);
-                __syncthreads();
-                continue;
-            }
-        }
         // software-pipelined point loads: the next point is in flight while this one is evaluated
         T xn0 = T(0), xn1 = T(0), xn2 = T(0);
         if (p0 + tid < p1) {

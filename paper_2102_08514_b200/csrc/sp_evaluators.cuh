@@ -68,9 +68,6 @@ struct BWeights<3> {
 template <typename T, int DEG>
 struct TensorBSplineEval {
     static constexpr int kMinBlocks = sizeof(T) == 4 ? 4 : 3;  // <= 64 / 80 registers
-    static constexpr bool kPair2 = false;
-    template <class F, class Ctx>
-    __device__ static void eval2(const T*, const T*, const int*, const int*, F&, F&, Ctx&, T&, T&) {}
     __device__ static void tile_records(const EvalArgs<T>&, const TileGeom&, const unsigned char*, int4*, int) {}
     // fp32: rows of DEG+1 taps are one LDS.64 / LDS.128 from the row-vector tile
     template <typename U>
@@ -183,9 +180,6 @@ __device__ __forceinline__ T generic_poly(const GenericTables& gt, int p, const 
 template <typename T>
 struct GenericEval {
     static constexpr int kMinBlocks = 1;
-    static constexpr bool kPair2 = false;
-    template <class F, class Ctx>
-    __device__ static void eval2(const T*, const T*, const int*, const int*, F&, F&, Ctx&, T&, T&) {}
 
     __device__ static void tile_records(const EvalArgs<T>&, const TileGeom&, const unsigned char*, int4*, int) {}
     template <typename U>
