@@ -196,3 +196,46 @@ def test_texture_variant_error_is_bounded(name, deg, cuda):
     with pytest.raises(NotImplementedError):
         _, p2, g2 = _setup("bcc_linear_rd", "zero", torch.float32, cuda)
         PlanInterpreter(p2).eval_batch_texture(g2, pts)
+
+
+def test_arbitrary_brick_partitions_are_correct(cuda):
+    """sp_eval_bricks is correct for ANY brick partition: unsorted points in one 'brick', or
+    random run boundaries, go through the global path where they leave the staged brick."""
+    from paper_2102_08514_b200.runtime import PointBatch
+
+    g, plan, grid = _setup("bcc_quintic_rd", "clamp", torch.float32, cuda)
+    interp = PlanInterpreter(plan)
+    pts = torch.from_numpy(g["pts"]).to(cuda)
+    ref = interp.eval_batch(grid, pts)
+    n = pts.shape[0]
+    one = PointBatch(pts, torch.tensor([0, n], dtype=torch.int64, device=cuda), 3, None)
+    torch.testing.assert_close(interp.eval_batch(grid, one), ref, rtol=0, atol=0)
+    cuts = torch.sort(torch.randint(1, n, (37,), generator=torch.Generator().manual_seed(3))).values
+    starts = torch.cat([torch.tensor([0]), cuts, torch.tensor([n])]).to(cuda)
+    rnd = PointBatch(pts, starts, 2, None)
+    torch.testing.assert_close(interp.eval_batch(grid, rnd), ref, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("name", ["bcc_linear_rd", "fcc_cubic", "cc_tricubic"])
+def test_float64_ties_and_large_coordinates(name, cuda):
+    """float64 points one ulp around coset-cell faces / plane ties (where x - l rounds) and
+    large |x| with the clamp policy: classification bit-exact, values vs the oracle."""
+    from oracle.plan_numpy import NumpyGrid, PlanTables, classify_batch, eval_batch as oracle_eval
+
+    g, plan, grid = _setup(name, "clamp", torch.float64, cuda)
+    rng = np.random.default_rng(17)
+    base = np.round(rng.uniform(-3, 14, size=(600, 3)) * 2) / 2
+    ulp = np.spacing(np.abs(base) + 1.0)
+    pts = np.concatenate([base, base + ulp, base - ulp, base + 2 ** -52, base - 2 ** -52,
+                          rng.uniform(-1e7, 1e7, size=(64, 3)), np.array([[1 - 2 ** -53, -1 + 2 ** -53, 2 ** -60]])])
+    interp = PlanInterpreter(plan)
+    t = torch.from_numpy(pts).to(cuda)
+    cls, cells = interp.classify(grid, t)
+    rcls, rcells = classify_batch(plan, pts)
+    np.testing.assert_array_equal(cls.cpu().numpy(), rcls)
+    np.testing.assert_array_equal(cells.cpu().numpy(), rcells)
+    ngrid = NumpyGrid(plan.diag, plan.shifts, [a.cpu().numpy() for a in grid.arrays], grid.origins, "clamp")
+    ref = oracle_eval(plan, ngrid, pts, PlanTables(plan))
+    for order in ("given", "sort"):
+        got = interp.eval_batch(grid, t, order=order).cpu().numpy()
+        assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), order
