@@ -1,0 +1,170 @@
+// sp_tma.cuh — brick kernel with TMA (cp.async.bulk.tensor) double-buffered staging.
+//
+// For single-coset tensor-product plans with the 'zero' boundary policy the staged brick box
+// has the same shape for every brick, so one tensor map (box = brick + site reach, padded to
+// 16 bytes) covers all of them: one elected thread issues the 3-D bulk tensor copy of the
+// NEXT brick into the other shared-memory buffer (mbarrier complete_tx) while the CTA
+// evaluates the current one; out-of-range texels are zero-filled by the TMA unit, which is
+// exactly the 'zero' policy (runtime.py:155-161).  No per-element staging instructions.
+#pragma once
+
+#include <cuda.h>
+
+#include "sp_common.cuh"
+#include "sp_evaluators.cuh"
+
+namespace sp {
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, unsigned long long* bar, int c0, int c1,
+                                            int c2) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(d),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(b)
+        : "memory");
+}
+
+// Single-coset (M = 1) brick kernel, T = float, evaluators with a row-vector tile.
+// box = (bz, by, bx) coset cells; bx is a multiple of 4 (16-byte TMA rows).
+template <typename T, class Ev>
+__global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
+    brick_kernel_tma(const EvalArgs<T> a, const __grid_constant__ CUtensorMap tmap,
+                     const long long* __restrict__ brick_start, int nbricks, int log2b, int bx, int by, int bz) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ TileGeom geom;
+    __shared__ __align__(8) unsigned long long mbar[2];
+    __shared__ int corner[2][3];
+    constexpr int kVec = Ev::template vec_width<T>();
+    using V = typename VecT<T, kVec>::type;
+    static_assert(kVec > 0, "TMA brick path is for row-vector evaluators");
+
+    const int tid = threadIdx.x;
+    const int boxv = bx * by * bz;
+    const int buf_bytes = (boxv * (int)sizeof(T) + 127) & ~127;
+    T* buf[2] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem + buf_bytes)};
+    V* vtile = reinterpret_cast<V*>(smem + 2 * buf_bytes);
+    const int B = 1 << log2b;
+
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // thread 0: brick corner from its first point, then the bulk tensor copy of its box
+    auto issue = [&](int b, int slot) {
+        const T* x = a.pts + 3 * brick_start[b];
+        int c[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            c[i] = (clamp_cell(x[i]) >> log2b) << log2b;
+            corner[slot][i] = c[i];
+        }
+        // array index of the box origin (may be negative: TMA zero-fills out of range)
+        const int z0 = c[0] + a.fr.reach_lo[0] - a.grid.org[0][0];
+        const int z1 = c[1] + a.fr.reach_lo[1] - a.grid.org[0][1];
+        const int z2 = c[2] + a.fr.reach_lo[2] - a.grid.org[0][2];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[slot], (unsigned)(boxv * sizeof(T)));
+        tma_load_3d(buf[slot], &tmap, &mbar[slot], z2, z1, z0);
+    };
+
+    if (tid == 0 && (int)blockIdx.x < nbricks) issue(blockIdx.x, 0);
+    unsigned phase[2] = {0u, 0u};
+    int it = 0;
+    for (int b = blockIdx.x; b < nbricks; b += gridDim.x, ++it) {
+        const int cur = it & 1;
+        const int nb = b + gridDim.x;
+        if (tid == 0 && nb < nbricks) issue(nb, cur ^ 1);  // overlaps this brick's evaluation
+        mbar_wait(&mbar[cur], phase[cur]);
+        phase[cur] ^= 1u;
+        const T* tile = buf[cur];
+        const int c0 = corner[cur][0], c1 = corner[cur][1], c2 = corner[cur][2];
+        const int lo0 = c0 + a.fr.reach_lo[0], lo1 = c1 + a.fr.reach_lo[1], lo2 = c2 + a.fr.reach_lo[2];
+        // row-vector copy of the box (same pitches as the TMA box)
+        for (int e = tid; e < boxv; e += kThreads) {
+            V v;
+            T* pv = reinterpret_cast<T*>(&v);
+#pragma unroll
+            for (int q = 0; q < kVec; ++q) pv[q] = e + q < boxv ? tile[e + q] : T(0);
+            vtile[e] = v;
+        }
+        if (tid == 0) {
+            geom.staged = 1;
+            geom.total = boxv;
+            geom.off[0] = 0;
+            geom.lo[0][0] = lo0;
+            geom.lo[0][1] = lo1;
+            geom.lo[0][2] = lo2;
+            geom.ex[0][0] = bz;
+            geom.ex[0][1] = by;
+            geom.ex[0][2] = bx;
+            geom.vx = bx;
+            geom.vy = by;
+            geom.vtotal = boxv;
+            geom.vbase = -lo0 * by * bx - lo1 * bx - lo2;
+            geom.st0[0] = by * bx;
+            geom.st1[0] = bx;
+            geom.cbase[0] = geom.vbase;
+        }
+        __syncthreads();
+
+        EvalCtx<T, Ev> ctx;
+        ctx.a = &a;
+        ctx.tables = smem;
+        ctx.geom = &geom;
+        ctx.trec = nullptr;
+        ctx.err = 0;
+        ctx.load_geom(geom, 1);
+        const long long p0 = brick_start[b], p1 = brick_start[b + 1];
+        T xn0 = T(0), xn1 = T(0), xn2 = T(0);
+        if (p0 + tid < p1) {
+            const T* px = a.pts + 3 * (p0 + tid);
+            xn0 = __ldg(px);
+            xn1 = __ldg(px + 1);
+            xn2 = __ldg(px + 2);
+        }
+#pragma unroll 1
+        for (long long j = p0 + tid; j < p1; j += kThreads) {
+            ctx.index = j;
+            const T x[3] = {xn0, xn1, xn2};
+            if (j + kThreads < p1) {
+                const T* px = a.pts + 3 * (j + kThreads);
+                xn0 = __ldg(px);
+                xn1 = __ldg(px + 1);
+                xn2 = __ldg(px + 2);
+            }
+            ctx.X[0] = clamp_cell(x[0]);
+            ctx.X[1] = clamp_cell(x[1]);
+            ctx.X[2] = clamp_cell(x[2]);
+            store_out(a, j, eval_one<T, Ev, V>(x, true, c0, c1, c2, B, tile, vtile, ctx));
+        }
+        if (ctx.err && a.err) atomicOr(a.err, 1);
+        __syncthreads();  // vtile / geom / this buffer are rewritten next iteration
+    }
+}
+
+}  // namespace sp

@@ -21,6 +21,7 @@
 #include "sp_common.cuh"
 #include "sp_evaluators.cuh"
 #include "sp_launch.cuh"
+#include "sp_tma.cuh"
 
 
 // generated plan kernels + kGenerated[] registry (codegen.py)
@@ -609,6 +610,75 @@ int brick_log2_typed(const sp_plan* p) {
     return -1;
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(f);
+    }
+    return fn;
+}
+
+template <int DEG>
+cudaError_t launch_tma(const sp::EvalArgs<float>& a, const CUtensorMap& map, const long long* bstart, int nbricks,
+                       int log2b, int bx, int by, int bz, size_t smem, int num_sms, cudaStream_t st) {
+    using Ev = sp::TensorBSplineEval<float, DEG>;
+    auto kern = sp::brick_kernel_tma<float, Ev>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e != cudaSuccess) return e;
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, sp::kThreads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const int blocks = std::max(1, std::min(nbricks, num_sms * per_sm));
+    kern<<<blocks, sp::kThreads, smem, st>>>(a, map, bstart, nbricks, log2b, bx, by, bz);
+    return cudaGetLastError();
+}
+
+// TMA-staged brick path: fp32 single-coset tensor-product plans, 'zero' boundary, 16-byte
+// aligned rows.  Returns 1 when launched, 0 when not applicable, < 0 on error.
+int try_bricks_tma(const sp_plan* p, const sp_grid_desc* g, const sp::EvalArgs<float>& a, const int64_t* bstart,
+                   int nbricks, int log2b, cudaStream_t st) {
+    if (env_int("SP_TMA", 1) == 0) return 0;
+    if (p->kind != SP_KIND_TENSOR_BSPLINE || g->M != 1 || g->boundary != SP_ZERO || a.margin != 0) return 0;
+    if (p->tp_degree != 1 && p->tp_degree != 3) return 0;
+    const long long e0 = g->extent[0][0], e1 = g->extent[0][1], e2 = g->extent[0][2];
+    if ((e2 * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(g->data[0]) & 15) != 0) return 0;
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return 0;
+    const int B = 1 << log2b;
+    const int span[3] = {B + p->reach_hi[0] - p->reach_lo[0], B + p->reach_hi[1] - p->reach_lo[1],
+                         B + p->reach_hi[2] - p->reach_lo[2]};
+    const int bx = (span[2] + 3) & ~3, by = span[1], bz = span[0];
+    if (bx > 256 || by > 256 || bz > 256) return 0;
+    const int boxv = bx * by * bz;
+    const int vec = p->tp_degree == 1 ? 2 : 4;
+    const size_t smem = 2 * (size_t)((boxv * 4 + 127) & ~127) + (size_t)boxv * vec * 4;
+    if (smem > 100 * 1024) return 0;
+    CUtensorMap map;
+    const cuuint64_t dims[3] = {(cuuint64_t)e2, (cuuint64_t)e1, (cuuint64_t)e0};
+    const cuuint64_t strides[2] = {(cuuint64_t)(e2 * 4), (cuuint64_t)(e2 * e1 * 4)};
+    const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(g->data[0]), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return 0;
+    const long long* bs = reinterpret_cast<const long long*>(bstart);
+    cudaError_t e = p->tp_degree == 1 ? launch_tma<1>(a, map, bs, nbricks, log2b, bx, by, bz, smem, p->num_sms, st)
+                                      : launch_tma<3>(a, map, bs, nbricks, log2b, bx, by, bz, smem, p->num_sms, st);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "TMA brick kernel launch: %s", cudaGetErrorString(e));
+    return 1;
+}
+
 template <typename T>
 int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, const int64_t* bstart,
                       int32_t nbricks, int32_t log2b, const int64_t* out_index, void* out, int32_t* err,
@@ -618,6 +688,10 @@ int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, 
     int rc = build_args<T>(p, g, pts, n, out, nullptr, err, a, vec);
     if (rc != SP_OK) return rc;
     a.out_index = reinterpret_cast<const long long*>(out_index);
+    if constexpr (sizeof(T) == 4) {
+        const int t = try_bricks_tma(p, g, a, bstart, nbricks, log2b, st);
+        if (t != 0) return t > 0 ? SP_OK : t;
+    }
     Kernels<T> k;
     if ((rc = select_kernels<T>(p, k)) != SP_OK) return rc;
     const size_t smem = tile_smem(a, vec, sizeof(T));

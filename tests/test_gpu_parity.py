@@ -164,10 +164,12 @@ def test_two_dimensional_plans_not_implemented(cuda):
 
 @pytest.mark.parametrize("name", NAMES)
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-def test_brick_mode_matches_chunk_mode(name, dtype, cuda):
-    """Brick mode (sorted points, per-brick staging, fused unpermute) is bit-identical to the
+@pytest.mark.parametrize("boundary", ["zero", "mirror"])
+def test_brick_mode_matches_chunk_mode(name, dtype, boundary, cuda):
+    """Brick mode (sorted points, per-brick staging — TMA bulk tensor copies for fp32
+    tensor-product plans with the zero policy — fused unpermute) is bit-identical to the
     chunk kernel and therefore inherits its parity with the reference."""
-    g, plan, grid = _setup(name, "mirror", dtype, cuda)
+    g, plan, grid = _setup(name, boundary, dtype, cuda)
     interp = PlanInterpreter(plan)
     pts = torch.from_numpy(g["pts"]).to(cuda, dtype)
     a = interp.eval_batch(grid, pts)
