@@ -47,7 +47,8 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 }
 
 // Single-coset (M = 1) brick kernel, T = float, evaluators with a row-vector tile.
-// box = (bz, by, bx) coset cells; bx is a multiple of 4 (16-byte TMA rows).
+// box = (bz, by, bx) coset cells; bx is a multiple of 4 (16-byte TMA rows) and 3 wider than
+// needed, because the box's innermost start coordinate must be 16-byte aligned.
 template <typename T, class Ev>
 __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     brick_kernel_tma(const EvalArgs<T> a, const __grid_constant__ CUtensorMap tmap,
@@ -83,10 +84,12 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
             c[i] = (clamp_cell(x[i]) >> log2b) << log2b;
             corner[slot][i] = c[i];
         }
-        // array index of the box origin (may be negative: TMA zero-fills out of range)
+        // array index of the box origin (may be negative: TMA zero-fills out of range); the
+        // innermost coordinate must be 16-byte aligned, so it is rounded down to 4 floats
+        // (the host widens the box by 3 to cover it)
         const int z0 = c[0] + a.fr.reach_lo[0] - a.grid.org[0][0];
         const int z1 = c[1] + a.fr.reach_lo[1] - a.grid.org[0][1];
-        const int z2 = c[2] + a.fr.reach_lo[2] - a.grid.org[0][2];
+        const int z2 = (c[2] + a.fr.reach_lo[2] - a.grid.org[0][2]) & ~3;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&mbar[slot], (unsigned)(boxv * sizeof(T)));
         tma_load_3d(buf[slot], &tmap, &mbar[slot], z2, z1, z0);
@@ -103,7 +106,8 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         phase[cur] ^= 1u;
         const T* tile = buf[cur];
         const int c0 = corner[cur][0], c1 = corner[cur][1], c2 = corner[cur][2];
-        const int lo0 = c0 + a.fr.reach_lo[0], lo1 = c1 + a.fr.reach_lo[1], lo2 = c2 + a.fr.reach_lo[2];
+        const int lo0 = c0 + a.fr.reach_lo[0], lo1 = c1 + a.fr.reach_lo[1];
+        const int lo2 = ((c2 + a.fr.reach_lo[2] - a.grid.org[0][2]) & ~3) + a.grid.org[0][2];
         // row-vector copy of the box (same pitches as the TMA box)
         for (int e = tid; e < boxv; e += kThreads) {
             V v;

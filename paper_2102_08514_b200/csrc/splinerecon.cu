@@ -657,7 +657,8 @@ int try_bricks_tma(const sp_plan* p, const sp_grid_desc* g, const sp::EvalArgs<f
     const int B = 1 << log2b;
     const int span[3] = {B + p->reach_hi[0] - p->reach_lo[0], B + p->reach_hi[1] - p->reach_lo[1],
                          B + p->reach_hi[2] - p->reach_lo[2]};
-    const int bx = (span[2] + 3) & ~3, by = span[1], bz = span[0];
+    // innermost TMA start coordinate must be 16-byte aligned: start rounded down, box widened
+    const int bx = (span[2] + 3 + 3) & ~3, by = span[1], bz = span[0];
     if (bx > 256 || by > 256 || bz > 256) return 0;
     const int boxv = bx * by * bz;
     const int vec = p->tp_degree == 1 ? 2 : 4;
