@@ -302,9 +302,9 @@ __device__ __forceinline__ int plane_code(const R xp0, const R xp1, const R xp2)
 template <typename R, typename T>
 __device__ __forceinline__ int class_and_y(const R xp[3], const int* sigma, const uint4* cls_tab, int& err,
                                            T y[3], uint4& rec) {{
-    int c = sigma[plane_code<R>(xp[0], xp[1], xp[2]) % kR];
-    err |= c < 0;
-    c = max(c, 0);
+    const int raw = sigma[plane_code<R>(xp[0], xp[1], xp[2]) % kR];
+    err |= raw < 0;  // sigma sentinel (runtime.py:380-381): flagged, evaluated as class 0
+    const int c = max(raw, 0);
     rec = cls_tab[c];
     const float tt[3] = {{__uint_as_float(rec.y), __uint_as_float(rec.z), __uint_as_float(rec.w)}};
 #pragma unroll
@@ -314,7 +314,7 @@ __device__ __forceinline__ int class_and_y(const R xp[3], const int* sigma, cons
         const R v = (perm & 2u) ? xp[2] : v01;
         y[i] = (T)((((rec.x >> (10 + i)) & 1u) ? -v : v) - (R)tt[i]);
     }}
-    return c;
+    return raw;
 }}
 
 // float64 coset frame exactly as runtime.py:371-373 (any point)
@@ -397,9 +397,10 @@ struct Eval {{
             int cell[3];
             T yy[3];
             uint4 rec;
-            const int c = fast ? classify_fast<T>(frac, ctx.X, k, sigma, cls_tab, ctx.err, cell, yy, rec)
-                               : classify_f64<T>(x, k, sigma, cls_tab, ctx.err, cell, yy, rec);
-            write_dbg(a.dbg, ctx.index, kM, k, c, cell);
+            const int raw = fast ? classify_fast<T>(frac, ctx.X, k, sigma, cls_tab, ctx.err, cell, yy, rec)
+                                 : classify_f64<T>(x, k, sigma, cls_tab, ctx.err, cell, yy, rec);
+            write_dbg(a.dbg, ctx.index, kM, k, raw, cell);  // raw class: -1 for the sentinel
+            const int c = max(raw, 0);
             const int kern = (int)(rec.x & 15u);
             (void)kern;
             const T y0 = yy[0], y1 = yy[1], y2 = yy[2];

@@ -204,11 +204,11 @@ struct GenericEval {
                 if (dot >= __ldg(gt.offsets + j)) q |= 1LL << j;
             }
             int cls = __ldg(gt.sigma + (int)(q % gt.r));
+            write_dbg(a.dbg, ctx.index, a.fr.M, k, cls, cf.cell);  // raw class: -1 for the sentinel
             if (cls < 0) {
                 ctx.err = 1;
                 cls = 0;
             }
-            write_dbg(a.dbg, ctx.index, a.fr.M, k, cls, cf.cell);
             T y[3];
 #pragma unroll
             for (int i = 0; i < 3; ++i) {

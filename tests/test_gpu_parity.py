@@ -236,8 +236,15 @@ def test_float64_ties_and_large_coordinates(name, cuda):
     rcls, rcells = classify_batch(plan, pts)
     np.testing.assert_array_equal(cls.cpu().numpy(), rcls)
     np.testing.assert_array_equal(cells.cpu().numpy(), rcells)
+    # float64 ties can land on unrealised plane codes: the reference raises there
+    # (runtime.py:380-381) and so does eval_batch; compare values on the other points
+    sentinel = (rcls < 0).any(axis=1)
+    if sentinel.any():
+        with pytest.raises(RuntimeError_):
+            interp.eval_batch(grid, t)
+    keep = ~sentinel
     ngrid = NumpyGrid(plan.diag, plan.shifts, [a.cpu().numpy() for a in grid.arrays], grid.origins, "clamp")
-    ref = oracle_eval(plan, ngrid, pts, PlanTables(plan))
+    ref = oracle_eval(plan, ngrid, pts[keep], PlanTables(plan))
     for order in ("given", "sort"):
-        got = interp.eval_batch(grid, t, order=order).cpu().numpy()
+        got = interp.eval_batch(grid, t[torch.from_numpy(keep).to(cuda)], order=order).cpu().numpy()
         assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), order
