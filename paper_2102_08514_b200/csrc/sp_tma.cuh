@@ -48,11 +48,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 
 // Single-coset (M = 1) brick kernel, T = float, evaluators with a row-vector tile.
 // box = (bz, by, bx) coset cells; bx is a multiple of 4 (16-byte TMA rows) and 3 wider than
-// needed, because the box's innermost start coordinate must be 16-byte aligned.
+// needed, because the box's innermost start coordinate must be 16-byte aligned; the host may
+// widen bx / by further so that the row loads are bank-conflict free (choose_box_pitch).
 template <typename T, class Ev>
 __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     brick_kernel_tma(const EvalArgs<T> a, const __grid_constant__ CUtensorMap tmap,
-                     const long long* __restrict__ brick_start, int nbricks, int log2b, int bx, int by, int bz) {
+                     const long long* __restrict__ brick_start, int nbricks, int log2b, int bx, int by, int bz, int vx,
+                     int vy) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ TileGeom geom;
     __shared__ __align__(8) unsigned long long mbar[2];
@@ -64,9 +66,13 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     const int tid = threadIdx.x;
     const int boxv = bx * by * bz;
     const int buf_bytes = (boxv * (int)sizeof(T) + 127) & ~127;
-    T* buf[2] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem + buf_bytes)};
+    auto buf = [&](int slot) { return reinterpret_cast<T*>(smem + slot * buf_bytes); };
     V* vtile = reinterpret_cast<V*>(smem + 2 * buf_bytes);
     const int B = 1 << log2b;
+    const bool padded = vx != bx || vy != by;
+    unsigned mx, sx, my, sy;
+    fastdiv_magic((unsigned)bx, mx, sx);
+    fastdiv_magic((unsigned)by, my, sy);
 
     if (tid == 0) {
         mbar_init(&mbar[0], 1);
@@ -92,29 +98,35 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         const int z2 = (c[2] + a.fr.reach_lo[2] - a.grid.org[0][2]) & ~3;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&mbar[slot], (unsigned)(boxv * sizeof(T)));
-        tma_load_3d(buf[slot], &tmap, &mbar[slot], z2, z1, z0);
+        tma_load_3d(buf(slot), &tmap, &mbar[slot], z2, z1, z0);
     };
 
     if (tid == 0 && (int)blockIdx.x < nbricks) issue(blockIdx.x, 0);
-    unsigned phase[2] = {0u, 0u};
+    unsigned phase = 0u;  // bit s = mbarrier parity of buffer s
     int it = 0;
     for (int b = blockIdx.x; b < nbricks; b += gridDim.x, ++it) {
         const int cur = it & 1;
         const int nb = b + gridDim.x;
         if (tid == 0 && nb < nbricks) issue(nb, cur ^ 1);  // overlaps this brick's evaluation
-        mbar_wait(&mbar[cur], phase[cur]);
-        phase[cur] ^= 1u;
-        const T* tile = buf[cur];
+        mbar_wait(&mbar[cur], (phase >> cur) & 1u);
+        phase ^= 1u << cur;
+        const T* tile = buf(cur);
         const int c0 = corner[cur][0], c1 = corner[cur][1], c2 = corner[cur][2];
         const int lo0 = c0 + a.fr.reach_lo[0], lo1 = c1 + a.fr.reach_lo[1];
         const int lo2 = ((c2 + a.fr.reach_lo[2] - a.grid.org[0][2]) & ~3) + a.grid.org[0][2];
-        // row-vector copy of the box (same pitches as the TMA box)
+        // row-vector copy of the box: vtile[(z*vy + y)*vx + x] = tile[(z*by + y)*bx + x .. +kVec)
         for (int e = tid; e < boxv; e += kThreads) {
             V v;
             T* pv = reinterpret_cast<T*>(&v);
 #pragma unroll
             for (int q = 0; q < kVec; ++q) pv[q] = e + q < boxv ? tile[e + q] : T(0);
-            vtile[e] = v;
+            int d = e;
+            if (padded) {
+                const int r = (int)fastdiv((unsigned)e, mx, sx);  // z*by + y
+                const int z = (int)fastdiv((unsigned)r, my, sy);
+                d = (r + z * (vy - by)) * vx + (e - r * bx);
+            }
+            vtile[d] = v;
         }
         if (tid == 0) {
             geom.staged = 1;
@@ -126,13 +138,13 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
             geom.ex[0][0] = bz;
             geom.ex[0][1] = by;
             geom.ex[0][2] = bx;
-            geom.vx = bx;
-            geom.vy = by;
-            geom.vtotal = boxv;
-            geom.vbase = -lo0 * by * bx - lo1 * bx - lo2;
-            geom.st0[0] = by * bx;
+            geom.vx = vx;
+            geom.vy = vy;
+            geom.vtotal = vx * vy * bz;
+            geom.vbase = -lo0 * vy * vx - lo1 * vx - lo2;
+            geom.st0[0] = by * bx;  // scalar (TMA) tile pitches
             geom.st1[0] = bx;
-            geom.cbase[0] = geom.vbase;
+            geom.cbase[0] = -lo0 * by * bx - lo1 * bx - lo2;
         }
         __syncthreads();
 

@@ -10,6 +10,7 @@
 //   * the generic table-driven kernel.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -630,7 +631,7 @@ EncodeTiledFn encode_tiled() {
 
 template <int DEG>
 cudaError_t launch_tma(const sp::EvalArgs<float>& a, const CUtensorMap& map, const long long* bstart, int nbricks,
-                       int log2b, int bx, int by, int bz, size_t smem, int num_sms, cudaStream_t st) {
+                       int log2b, int bx, int by, int bz, int vx, int vy, size_t smem, int num_sms, cudaStream_t st) {
     using Ev = sp::TensorBSplineEval<float, DEG>;
     auto kern = sp::brick_kernel_tma<float, Ev>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
@@ -639,8 +640,47 @@ cudaError_t launch_tma(const sp::EvalArgs<float>& a, const CUtensorMap& map, con
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, sp::kThreads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     const int blocks = std::max(1, std::min(nbricks, num_sms * per_sm));
-    kern<<<blocks, sp::kThreads, smem, st>>>(a, map, bstart, nbricks, log2b, bx, by, bz);
+    kern<<<blocks, sp::kThreads, smem, st>>>(a, map, bstart, nbricks, log2b, bx, by, bz, vx, vy);
     return cudaGetLastError();
+}
+
+// Pitches of the TMA box (= the row-vector tile) that keep the row loads of Morton-adjacent
+// cells in different shared-memory bank groups: two lanes of one load phase (8 lanes for
+// LDS.128, 16 for LDS.64) reading different rows whose float offsets differ by a multiple of
+// 32 banks serialise.  Lanes hold consecutive Morton-ordered points, so the rows they read
+// belong to Morton-consecutive cells; score each candidate (bx, by) by the cell pairs at
+// Morton distance 1 and 2 inside a brick whose row offset is a multiple of the phase's slot
+// count, and take the cheapest (then smallest) box.
+void choose_box_pitch(int need_x, int need_y, int B, int slots, int xstep, int& bx, int& by) {
+    auto spread = [](int v) {
+        int o = 0;
+        for (int i = 0; i < 5; ++i) o |= ((v >> i) & 1) << (3 * i);
+        return o;
+    };
+    std::vector<std::pair<int, int>> cells;  // (morton, packed zyx)
+    for (int z = 0; z < B; ++z)
+        for (int y = 0; y < B; ++y)
+            for (int x = 0; x < B; ++x) cells.push_back({spread(x) | spread(y) << 1 | spread(z) << 2, (z << 10) | (y << 5) | x});
+    std::sort(cells.begin(), cells.end());
+    long best = -1;
+    const int bx0 = (need_x + xstep - 1) / xstep * xstep;
+    for (int cx = bx0; cx <= bx0 + 12 && cx <= 256; cx += xstep)
+        for (int cy = need_y; cy <= need_y + 4 && cy <= 256; ++cy) {
+            long cost = 0;
+            for (size_t i = 0; i < cells.size(); ++i)
+                for (size_t d = 1; d <= 2 && i + d < cells.size(); ++d) {
+                    const int a = cells[i].second, b = cells[i + d].second;
+                    const long D = (long)((b >> 10) - (a >> 10)) * cx * cy + (long)(((b >> 5) & 31) - ((a >> 5) & 31)) * cx +
+                                   ((b & 31) - (a & 31));
+                    cost += (D != 0 && D % slots == 0);
+                }
+            const long score = cost * (1l << 24) + (long)cx * cy;
+            if (best < 0 || score < best) {
+                best = score;
+                bx = cx;
+                by = cy;
+            }
+        }
 }
 
 // TMA-staged brick path: fp32 single-coset tensor-product plans, 'zero' boundary, 16-byte
@@ -658,11 +698,18 @@ int try_bricks_tma(const sp_plan* p, const sp_grid_desc* g, const sp::EvalArgs<f
     const int span[3] = {B + p->reach_hi[0] - p->reach_lo[0], B + p->reach_hi[1] - p->reach_lo[1],
                          B + p->reach_hi[2] - p->reach_lo[2]};
     // innermost TMA start coordinate must be 16-byte aligned: start rounded down, box widened
-    const int bx = (span[2] + 3 + 3) & ~3, by = span[1], bz = span[0];
+    const int vec = p->tp_degree == 1 ? 2 : 4;
+    // SP_BOXPAD: 0 = dense box and row-vector tile, 1 = conflict-free TMA box pitches (the
+    // tile copy stays 1:1), 2 = dense TMA box, conflict-free row-vector tile pitches
+    const int boxpad = env_int("SP_BOXPAD", 2);
+    int bx = (span[2] + 3 + 3) & ~3, by = span[1];
+    if (boxpad == 1) choose_box_pitch(span[2] + 3, span[1], B, 128 / (vec * 4), 4, bx, by);
+    int vx = bx, vy = by;
+    if (boxpad == 2) choose_box_pitch(bx, by, B, 128 / (vec * 4), 1, vx, vy);
+    const int bz = span[0];
     if (bx > 256 || by > 256 || bz > 256) return 0;
     const int boxv = bx * by * bz;
-    const int vec = p->tp_degree == 1 ? 2 : 4;
-    const size_t smem = 2 * (size_t)((boxv * 4 + 127) & ~127) + (size_t)boxv * vec * 4;
+    const size_t smem = 2 * (size_t)((boxv * 4 + 127) & ~127) + (size_t)vx * vy * bz * vec * 4;
     if (smem > 100 * 1024) return 0;
     CUtensorMap map;
     const cuuint64_t dims[3] = {(cuuint64_t)e2, (cuuint64_t)e1, (cuuint64_t)e0};
@@ -674,8 +721,8 @@ int try_bricks_tma(const sp_plan* p, const sp_grid_desc* g, const sp::EvalArgs<f
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return 0;
     const long long* bs = reinterpret_cast<const long long*>(bstart);
-    cudaError_t e = p->tp_degree == 1 ? launch_tma<1>(a, map, bs, nbricks, log2b, bx, by, bz, smem, p->num_sms, st)
-                                      : launch_tma<3>(a, map, bs, nbricks, log2b, bx, by, bz, smem, p->num_sms, st);
+    cudaError_t e = p->tp_degree == 1 ? launch_tma<1>(a, map, bs, nbricks, log2b, bx, by, bz, vx, vy, smem, p->num_sms, st)
+                                      : launch_tma<3>(a, map, bs, nbricks, log2b, bx, by, bz, vx, vy, smem, p->num_sms, st);
     if (e != cudaSuccess) return fail(SP_ERR_CUDA, "TMA brick kernel launch: %s", cudaGetErrorString(e));
     return 1;
 }
