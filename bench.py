@@ -354,6 +354,9 @@ def run_ours(args):
     host_pts = pts.to("cpu").pin_memory()
     host_out = torch.empty(n, dtype=grid.dtype).pin_memory()
 
+    if args.e2e_chunk:
+        interp.host_chunk = args.e2e_chunk
+
     def e2e_step():
         interp.eval_batch(grid, host_pts, out=host_out, check=False, order="morton")
 
@@ -489,6 +492,7 @@ def main():
     ap.add_argument("--workload", default=HEADLINE, choices=sorted(WORKLOADS))
     ap.add_argument("--points", type=int, default=None, help="points per GPU (default: the workload's)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunk", type=int, default=0, help="points per pipelined host chunk (0 = library default)")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

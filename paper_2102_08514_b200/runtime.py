@@ -309,6 +309,14 @@ class PlanInterpreter:
         if is_numpy:
             pts = torch.from_numpy(np.ascontiguousarray(np.asarray(pts, dtype=np.float64)))
         on_host = pts.device.type == "cpu"
+        if order not in ("given", "morton", "sort"):
+            raise RuntimeError_(f"unknown point order {order!r}")
+        if reorder:
+            order = "sort"
+        if (on_host and not is_numpy and pts.dtype == grid.dtype and pts.is_pinned() and pts.is_contiguous()
+                and pts.dim() == 2 and pts.shape[1] == self.plan.s and pts.shape[0] >= 2 * self.host_chunk
+                and (out is None or (out.device.type == "cpu" and out.is_pinned()))):
+            return self._eval_host_pipelined(grid, pts, out, check=check, order=order, stream=stream)
         if on_host:
             # host buffers: H2D copy of the points, D2H copy of the result (pinned -> async)
             src = pts.to(dtype=grid.dtype)
@@ -319,10 +327,6 @@ class PlanInterpreter:
             raise RuntimeError_(f"points must have shape (n, {self.plan.s})")
         n = p.shape[0]
         res = out if (out is not None and out.device == dev) else torch.empty(n, dtype=grid.dtype, device=dev)
-        if order not in ("given", "morton", "sort"):
-            raise RuntimeError_(f"unknown point order {order!r}")
-        if reorder:
-            order = "sort"
         if n:
             self._launch(grid, p, res, check=check, order=order, stream=stream)
         if is_numpy:
@@ -334,7 +338,57 @@ class PlanInterpreter:
             return res.to("cpu")
         return res
 
-    def _eval_bricks(self, grid, batch: "PointBatch", *, out=None, check=True, stream=None, unpermute=True):
+    # points per pipelined host chunk (pinned host buffers, see _eval_host_pipelined)
+    host_chunk = 1 << 22
+
+    def _eval_host_pipelined(self, grid, pts, out, *, check, order, stream):
+        """Pinned host points -> pinned host results, overlapping the PCIe transfers with
+        each other and with the evaluation: the batch is cut into chunks of `host_chunk`
+        points; all host->device copies are queued on one copy stream, each chunk's
+        evaluation waits for its copy on the compute stream, and each result chunk goes back
+        on a third stream as soon as it is evaluated.  Chunks are contiguous ranges, so a
+        Morton-ordered batch gives Morton-ordered chunks; values are identical to the
+        one-shot path (every point is evaluated by the same arithmetic)."""
+        dev = grid.device
+        n = pts.shape[0]
+        caller = stream if stream is not None else torch.cuda.current_stream(dev)
+        h2d = torch.cuda.Stream(dev)
+        d2h = torch.cuda.Stream(dev)
+        comp = torch.cuda.Stream(dev)
+        res_host = out if out is not None else torch.empty(n, dtype=grid.dtype, pin_memory=True)
+        with torch.cuda.stream(caller):
+            p_dev = torch.empty((n, pts.shape[1]), dtype=grid.dtype, device=dev)
+            r_dev = torch.empty(n, dtype=grid.dtype, device=dev)
+        for s_ in (h2d, d2h, comp):
+            s_.wait_stream(caller)
+        C = self.host_chunk
+        bounds = [(i, min(i + C, n)) for i in range(0, n, C)]
+        copied = []
+        with torch.cuda.stream(h2d):
+            for a, b in bounds:
+                p_dev[a:b].copy_(pts[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                copied.append(ev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev) if check else None
+        for (a, b), ev in zip(bounds, copied):
+            comp.wait_event(ev)
+            self._launch(grid, p_dev[a:b], r_dev[a:b], check=False, order=order, stream=comp, err=err)
+            done = torch.cuda.Event()
+            done.record(comp)
+            d2h.wait_event(done)
+            with torch.cuda.stream(d2h):
+                res_host[a:b].copy_(r_dev[a:b], non_blocking=True)
+        caller.wait_stream(d2h)
+        caller.wait_stream(comp)
+        if check:
+            caller.synchronize()
+            if int(err.item()):
+                raise RuntimeError_("sigma sentinel hit in batch evaluation")
+        return res_host
+
+    def _eval_bricks(self, grid, batch: "PointBatch", *, out=None, check=True, stream=None, unpermute=True,
+                     err=None):
         """Brick-mode evaluation (sp_eval_bricks).  Results are returned in the caller's
         original order (batch.perm scatter fused into the kernel) unless unpermute=False."""
         lib = _native.lib()
@@ -347,7 +401,8 @@ class PlanInterpreter:
         n = batch.n
         res = out if out is not None else torch.empty(n, dtype=grid.dtype, device=dev)
         st = stream if stream is not None else torch.cuda.current_stream(dev)
-        err = torch.zeros(1, dtype=torch.int32, device=dev) if check else None
+        if check:
+            err = torch.zeros(1, dtype=torch.int32, device=dev)
         idx = batch.perm if (unpermute and batch.perm is not None) else None
         if n:
             with torch.cuda.stream(st):
@@ -403,18 +458,22 @@ class PlanInterpreter:
             self._launch(grid, p, res, dbg=dbg, check=False)
         return dbg[:, :, 0].to(torch.int64), dbg[:, :, 1:].to(torch.int64)
 
-    def _launch(self, grid, p, res, *, dbg=None, check=True, order="given", stream=None):
+    def _launch(self, grid, p, res, *, dbg=None, check=True, order="given", stream=None, err=None):
+        """Evaluate device points p into res on `stream`.  `err` (optional int32 device flag)
+        accumulates sigma-sentinel hits without synchronising; with check=True a fresh flag
+        is used and tested."""
         lib = _native.lib()
         h = self._handle(grid.device)
         gdesc = grid.descriptor()
         dtype = _native.SP_F32 if grid.dtype == torch.float32 else _native.SP_F64
         st = stream if stream is not None else torch.cuda.current_stream(grid.device)
-        err = torch.zeros(1, dtype=torch.int32, device=grid.device) if check else None
+        if check:
+            err = torch.zeros(1, dtype=torch.int32, device=grid.device)
         n = p.shape[0]
         b = self.brick_log2(grid) if (order != "given" and dbg is None) else -1
         if b >= 0:
             batch = prepare_points(p, b, presorted=(order == "morton"), stream=st)
-            self._eval_bricks(grid, batch, out=res, check=check, stream=st)
+            self._eval_bricks(grid, batch, out=res, check=check, stream=st, err=err)
             return
         with torch.cuda.stream(st):
             if order == "sort":

@@ -200,12 +200,15 @@ def test_texture_variant_error_is_bounded(name, deg, cuda):
         PlanInterpreter(p2).eval_batch_texture(g2, pts)
 
 
-def test_arbitrary_brick_partitions_are_correct(cuda):
+@pytest.mark.parametrize("name,boundary", [("bcc_quintic_rd", "clamp"), ("cc_tricubic", "zero"),
+                                           ("cc_trilinear", "zero")])
+def test_arbitrary_brick_partitions_are_correct(name, boundary, cuda):
     """sp_eval_bricks is correct for ANY brick partition: unsorted points in one 'brick', or
-    random run boundaries, go through the global path where they leave the staged brick."""
+    random run boundaries, go through the global path where they leave the staged brick
+    (cc_tricubic / cc_trilinear + zero: the TMA brick kernel's global path)."""
     from paper_2102_08514_b200.runtime import PointBatch
 
-    g, plan, grid = _setup("bcc_quintic_rd", "clamp", torch.float32, cuda)
+    g, plan, grid = _setup(name, boundary, torch.float32, cuda)
     interp = PlanInterpreter(plan)
     pts = torch.from_numpy(g["pts"]).to(cuda)
     ref = interp.eval_batch(grid, pts)
@@ -248,3 +251,47 @@ def test_float64_ties_and_large_coordinates(name, cuda):
     for order in ("given", "sort"):
         got = interp.eval_batch(grid, t[torch.from_numpy(keep).to(cuda)], order=order).cpu().numpy()
         assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), order
+
+
+@pytest.mark.parametrize("order", ["morton", "given", "sort"])
+@pytest.mark.parametrize("name", ["cc_tricubic", "bcc_linear_rd"])
+def test_pipelined_host_path_matches_device_path(name, order, cuda):
+    """Pinned host buffers take the chunked, copy-overlapped path (_eval_host_pipelined);
+    results are bit-identical to evaluating the same points from device memory."""
+    g, plan, grid = _setup(name, "zero", torch.float32, cuda)
+    interp = PlanInterpreter(plan)
+    interp.host_chunk = 1000
+    pts = torch.from_numpy(g["pts"]).to(cuda, torch.float32)
+    if order == "morton":
+        pts = interp.prepare(grid, pts).pts
+    ref = interp.eval_batch(grid, pts, order=order)
+    host_pts = pts.cpu().pin_memory()
+    host_out = torch.full((pts.shape[0],), -7.0, dtype=torch.float32).pin_memory()
+    got = interp.eval_batch(grid, host_pts, out=host_out, order=order)
+    torch.cuda.synchronize()
+    assert got.data_ptr() == host_out.data_ptr()
+    torch.testing.assert_close(got, ref.cpu(), rtol=0, atol=0, equal_nan=True)
+    got2 = interp.eval_batch(grid, host_pts, order=order)  # result allocated (pinned) by the call
+    torch.cuda.synchronize()
+    torch.testing.assert_close(got2, ref.cpu(), rtol=0, atol=0, equal_nan=True)
+
+
+def test_pipelined_host_path_raises_on_sentinel(cuda):
+    """The sigma-sentinel error survives chunking: one device flag shared by all chunks,
+    the hit is in the LAST chunk."""
+    from oracle.plan_numpy import classify_batch
+
+    _, _, grid = _setup("bcc_linear_rd", "zero", torch.float64, cuda)
+    bad = deserialize_plan((corpus.PLAN_DIR / "bcc_linear_rd.plan.json").read_text())
+    x = np.array([[0.25, 0.125, 0.0625]])
+    hit = int(classify_batch(bad, x)[0][0, 0])
+    bad.sigma = tuple(-1 if v == hit else v for v in bad.sigma)
+    interp = PlanInterpreter(bad)
+    interp.host_chunk = 500
+    clean = np.tile([[100.9, 100.2, 100.6]], (1999, 1))  # outside the grid; a class sigma still maps
+    ok = classify_batch(bad, clean)[0] >= 0
+    assert ok.all()
+    pts = torch.from_numpy(np.concatenate([clean, x])).pin_memory()
+    with pytest.raises(RuntimeError_):
+        interp.eval_batch(grid, pts)
+    interp.eval_batch(grid, torch.from_numpy(clean).pin_memory())  # no hit: no error
