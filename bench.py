@@ -160,6 +160,31 @@ def algorithmic_bytes(n, grid, dtype_size):
     return n * (3 * dtype_size + dtype_size) + grid.nbytes()
 
 
+def onchip_roofline(plan, esize, pts_per_s, sm_mhz):
+    """Secondary (on-chip) roofline, SURVEY.md §8d 'secondary bounds': the tensor-product
+    kernels are bound by the shared-memory datapath (every point receives (DEG+1)^3 taps,
+    128 B per SM per clock), the box-spline kernels by the FP32 pipe (the plan's weight
+    programs, 128 FMA lanes per SM per clock).  Peaks at the clock sampled during the run."""
+    from paper_2102_08514_b200 import codegen
+
+    clk = (sm_mhz or 1965.0) * 1e6
+    deg = plan.tensor_bspline_degree()
+    if deg is not None:
+        taps = (deg + 1) ** 3
+        per_pt = taps * esize
+        peak = 148 * 128 * clk
+        return {"bound": "shared-memory datapath", "unit": "TB/s", "bytes_per_point": per_pt,
+                "achieved": pts_per_s * per_pt / 1e12, "peak": peak / 1e12, "frac": pts_per_s * per_pt / peak}
+    if not codegen.codegen_supported(plan):
+        return None
+    fl = codegen.weight_flops(plan)
+    per_pt = plan.M * sum(fl) / len(fl)  # specialised (one kernel per coset), mean over kernels
+    peak = 148 * 128 * clk * (1.0 if esize == 4 else 1.0 / 64)
+    return {"bound": "fp32 pipe (weight programs)" if esize == 4 else "fp64 pipe", "unit": "Top/s (FMA = 1 op)",
+            "flops_per_point": per_pt, "flops_per_coset_per_kernel": fl,
+            "achieved": pts_per_s * per_pt / 1e12, "peak": peak / 1e12, "frac": pts_per_s * per_pt / peak}
+
+
 def measure(fn, steps, warmup, stream, dist=None):
     import torch
 
@@ -435,6 +460,7 @@ def run_ours(args):
         "unsorted_e2e_device": {"value": world * n / (ms_b * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_b,
                                 "note": "protocol B: shuffled points; Morton keys + sort + gather + brick runs + eval "
                                         "+ scatter to caller order, all timed"},
+        "roofline_onchip": onchip_roofline(plan, esize, n / (ms * 1e-3), clk.summary().get("sm_mhz")),
         "texture_variant": texture,
         "gpu_launches": int(args.steps * launches_per_step),
         "clocks": clk.summary(),
@@ -468,6 +494,7 @@ def run_ours(args):
                 "value": world * nw / (msw * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": msw,
                 "points_per_gpu": nw, "kernel": interp_w.kernel_name(device),
                 "roofline_hbm_frac": bw / (msw * 1e-3) / 1e9 / peak, "bytes_per_point": bw / nw,
+                "roofline_onchip": onchip_roofline(plan_w, es, nw / (msw * 1e-3), None),
             }
             del plan_w, grid_w, pts_w, interp_w, out_w, batch_w
             torch.cuda.empty_cache()

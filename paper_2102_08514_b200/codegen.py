@@ -228,6 +228,12 @@ def _plane_expr(normal) -> str:
     return expr
 
 
+def weight_flops(plan: EvaluationPlan) -> list:
+    """Per kernel: floating-point ops of one coset's generated weight program (shared
+    monomials + FMA chains + group merges), as emitted by generate_plan_source."""
+    return [_kernel_function(plan, k, plan.diag[0])[1] for k in range(plan.K)]
+
+
 def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple:
     """(translation-unit source, stats) for one plan; `stem` names the catalog entry."""
     if not codegen_supported(plan):
