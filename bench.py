@@ -185,6 +185,32 @@ def onchip_roofline(plan, esize, pts_per_s, sm_mhz):
             "achieved": pts_per_s * per_pt / 1e12, "peak": peak / 1e12, "frac": pts_per_s * per_pt / peak}
 
 
+def bench_prefilter(args, device, rank, stream, dist, peak):
+    """the quasi-interpolation prefilter of the BCC quintic spline
+    (9 taps, corpus.py:71-82) over the C5 grid (BCC 2x406^3, fp32, 535 MB > L2).  Streaming
+    stencil: algorithmic HBM bytes = one read + one write of every coset sample."""
+    import torch
+
+    from paper_2102_08514_b200 import corpus
+    from paper_2102_08514_b200.prefilter import apply_prefilter
+    from paper_2102_08514_b200.runtime import CoefficientGrid
+
+    _, cos = corpus.lattice_of("bcc_quintic_rd")
+    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [811, 811, 811], device=device, dtype=torch.float32)
+    gen = torch.Generator(device=device).manual_seed(2102_08514 + 31 * rank)
+    for a in grid.arrays:
+        a.copy_(torch.rand(a.shape, generator=gen, device=device))
+    taps = corpus.prefilter_taps("bcc_quintic_rd")
+    out = apply_prefilter(grid, taps)
+    ms = measure(lambda: apply_prefilter(grid, taps, out=out), max(3, min(args.steps, 50)), args.warmup, stream, dist)
+    nbytes = 2 * grid.nbytes()
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"workload": "bcc_quintic_rd prefilter (9 taps) on BCC 2x406^3 fp32, zero policy",
+            "value": gbs, "unit": "GB/s", "ms_per_step": ms, "samples": grid.site_count(),
+            "algorithmic_bytes_per_step": nbytes, "roofline_hbm_frac": gbs / peak,
+            "l2": "input and output 535 MB each > 126 MB L2"}
+
+
 def measure(fn, steps, warmup, stream, dist=None):
     import torch
 
@@ -499,6 +525,7 @@ def run_ours(args):
             del plan_w, grid_w, pts_w, interp_w, out_w, batch_w
             torch.cuda.empty_cache()
         line["workloads"] = others
+        line["prefilter"] = bench_prefilter(args, device, rank, stream, dist, peak)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(name, args.cpu_seconds)

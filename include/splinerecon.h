@@ -176,6 +176,27 @@ int sp_texture_create(const sp_grid_desc* grid, sp_texture** out);
 void sp_texture_destroy(sp_texture* tex);
 int sp_eval_texture(const sp_plan* plan, const sp_texture* tex, const void* pts, int64_t n, void* out, void* stream);
 
+/*
+ * Quasi-interpolation prefilter on coset grids (taps from
+ * corpus.prefilter_taps, corpus.py:71-111): the lattice correlation
+ *     out[site] = sum_t w_t * in[site + o_t]
+ * resolved per output coset k into taps (source coset, coset-cell offset dz, weight):
+ * out_k[z] = sum_{t in [tap_start[k], tap_start[k+1])} weight[t] * in_{src[t]}[z + dz[t]],
+ * taps summed in the given order with separate multiply and add (no FMA contraction), the
+ * input read through the grid's boundary policy (runtime.py:109-123, as site_value does).
+ * `out[k]` are device arrays of the same dtype and extents as in->data[k] (must not alias).
+ * At most SP_MAX_STENCIL taps per output coset.  Stream-ordered.
+ */
+#define SP_MAX_STENCIL 64
+typedef struct sp_stencil_desc {
+    int32_t M;                                 /* output cosets (= grid M)                    */
+    int32_t tap_start[SP_MAX_COSETS + 1];      /* CSR over taps per output coset              */
+    const int32_t* src_coset;                  /* [T] host array                              */
+    const int32_t* dz;                         /* [T][3] host array                           */
+    const double* weight;                      /* [T] host array                              */
+} sp_stencil_desc;
+int sp_prefilter(const sp_grid_desc* in, const sp_stencil_desc* stencil, void* const* out, void* stream);
+
 /* Staging statistics for tuning (not thread-safe): copies the counters accumulated since the
  * last call into out[4] = {staged chunks, unstaged chunks, staged tile elements, 0} (when
  * out != NULL), then enables (1, counters reset) or disables (0) collection. */

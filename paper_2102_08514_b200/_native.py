@@ -80,6 +80,21 @@ class GridDesc(ctypes.Structure):
     ]
 
 
+SP_MAX_STENCIL = 64
+
+
+class StencilDesc(ctypes.Structure):
+    """sp_stencil_desc (include/splinerecon.h)."""
+
+    _fields_ = [
+        ("M", ctypes.c_int32),
+        ("tap_start", ctypes.c_int32 * (SP_MAX_COSETS + 1)),
+        ("src_coset", ctypes.POINTER(ctypes.c_int32)),
+        ("dz", ctypes.POINTER(ctypes.c_int32)),
+        ("weight", ctypes.POINTER(ctypes.c_double)),
+    ]
+
+
 EXPORTS = {
     "sp_plan_create": (ctypes.c_int, [ctypes.POINTER(PlanDesc), ctypes.POINTER(ctypes.c_void_p)]),
     "sp_plan_destroy": (None, [ctypes.c_void_p]),
@@ -120,6 +135,7 @@ EXPORTS = {
     "sp_eval_texture": (
         ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
     ),
+    "sp_prefilter": (ctypes.c_int, [ctypes.POINTER(GridDesc), ctypes.POINTER(StencilDesc), ctypes.c_void_p, ctypes.c_void_p]),
     "sp_last_error": (ctypes.c_char_p, []),
     "sp_version": (ctypes.c_char_p, []),
 }
