@@ -1,10 +1,30 @@
 // sp_launch.cuh — kernel launch helpers and the generated-kernel registry entry type.
 #pragma once
 
+#include <map>
+#include <mutex>
+
 #include "sp_common.cuh"
 #include "sp_evaluators.cuh"
 
 namespace sp {
+
+// Blocks per SM of `kern` at `smem` bytes, memoised per (kernel, smem): the occupancy query
+// costs tens of microseconds of host time, which short launches cannot hide.
+template <typename K>
+static int cached_occupancy(K kern, size_t smem) {
+    static std::mutex mu;
+    static std::map<size_t, int> memo;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = memo.find(smem);
+    if (it != memo.end()) return it->second;
+    int per_sm = 0;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    memo[smem] = per_sm;
+    return per_sm;
+}
 
 template <typename T>
 using LaunchFn = cudaError_t (*)(const EvalArgs<T>&, int, size_t, cudaStream_t);
@@ -39,20 +59,12 @@ static cudaError_t launch_bricks(const EvalArgs<T>& a, const long long* bstart, 
 
 template <typename T, class Ev>
 static int occupancy_bricks(size_t smem) {
-    int per_sm = 0;
-    cudaFuncSetAttribute(brick_kernel<T, Ev>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick_kernel<T, Ev>, kThreads, smem) != cudaSuccess)
-        per_sm = 1;
-    return per_sm < 1 ? 1 : per_sm;
+    return cached_occupancy(brick_kernel<T, Ev>, smem);
 }
 
 template <typename T, class Ev>
 static int occupancy_blocks(size_t smem) {
-    int per_sm = 0;
-    cudaFuncSetAttribute(eval_kernel<T, Ev>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, eval_kernel<T, Ev>, kThreads, smem) != cudaSuccess)
-        per_sm = 1;
-    return per_sm < 1 ? 1 : per_sm;
+    return cached_occupancy(eval_kernel<T, Ev>, smem);
 }
 
 struct GenEntry {

@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -634,11 +637,7 @@ cudaError_t launch_tma(const sp::EvalArgs<float>& a, const CUtensorMap& map, con
                        int log2b, int bx, int by, int bz, int vx, int vy, size_t smem, int num_sms, cudaStream_t st) {
     using Ev = sp::TensorBSplineEval<float, DEG>;
     auto kern = sp::brick_kernel_tma<float, Ev>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (e != cudaSuccess) return e;
-    int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, sp::kThreads, smem) != cudaSuccess || per_sm < 1)
-        per_sm = 1;
+    const int per_sm = sp::cached_occupancy(kern, smem);  // also sets the dynamic smem limit
     const int blocks = std::max(1, std::min(nbricks, num_sms * per_sm));
     kern<<<blocks, sp::kThreads, smem, st>>>(a, map, bstart, nbricks, log2b, bx, by, bz, vx, vy);
     return cudaGetLastError();
@@ -651,7 +650,25 @@ cudaError_t launch_tma(const sp::EvalArgs<float>& a, const CUtensorMap& map, con
 // belong to Morton-consecutive cells; score each candidate (bx, by) by the cell pairs at
 // Morton distance 1 and 2 inside a brick whose row offset is a multiple of the phase's slot
 // count, and take the cheapest (then smallest) box.
+void choose_box_pitch_uncached(int need_x, int need_y, int B, int slots, int xstep, int& bx, int& by);
+
+// memoised: the search is O(B^3 * candidates) host work, far too slow to repeat per launch
 void choose_box_pitch(int need_x, int need_y, int B, int slots, int xstep, int& bx, int& by) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int, int>, std::pair<int, int>> memo;
+    const auto key = std::make_tuple(need_x, need_y, B, slots, xstep);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = memo.find(key);
+    if (it == memo.end()) {
+        std::pair<int, int> v;
+        choose_box_pitch_uncached(need_x, need_y, B, slots, xstep, v.first, v.second);
+        it = memo.emplace(key, v).first;
+    }
+    bx = it->second.first;
+    by = it->second.second;
+}
+
+void choose_box_pitch_uncached(int need_x, int need_y, int B, int slots, int xstep, int& bx, int& by) {
     auto spread = [](int v) {
         int o = 0;
         for (int i = 0; i < 5; ++i) o |= ((v >> i) & 1) << (3 * i);

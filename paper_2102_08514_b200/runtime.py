@@ -150,6 +150,18 @@ class CoefficientGrid:
         return float(arr[tuple(idx)])
 
     def descriptor(self) -> _native.GridDesc:
+        """sp_grid_desc of this grid (memoised on the arrays' storage, shapes and policy:
+        building it costs ~10-30 us of Python, which short launches cannot hide)."""
+        key = (self.boundary, tuple((a.data_ptr(), tuple(a.shape), a.dtype) for a in self.arrays),
+               tuple(self.origins))
+        cached = self.__dict__.get("_desc")
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        g = self._build_descriptor()
+        self.__dict__["_desc"] = (key, g)
+        return g
+
+    def _build_descriptor(self) -> _native.GridDesc:
         if self.device.type != "cuda":
             raise RuntimeError_("the grid must live on a CUDA device for evaluation")
         s = self.cosets.parent.s
