@@ -336,7 +336,9 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        n = cpu_calibrated_sample(pool, cores, args.ref_step_seconds)
+        # bounded: the whole --steps K --warmup W run stays within ~ref_total_seconds
+        step_s = min(args.ref_step_seconds, args.ref_total_seconds / max(1, args.steps + args.warmup))
+        n = cpu_calibrated_sample(pool, cores, step_s)
         for _ in range(args.warmup):
             cpu_run(n, pool)
         times = [cpu_run(n, pool) for _ in range(args.steps)]
@@ -412,12 +414,20 @@ def run_ours(args):
         interp.eval_batch(grid, host_pts, out=host_out, check=False, order="morton")
 
     e2e_steps = max(2, min(args.steps, args.e2e_steps))
-    e2e_ms = measure(e2e_step, e2e_steps, 1, stream, dist)
+    e2e_ms = measure(e2e_step, e2e_steps, max(1, min(args.warmup, 3)), stream, dist)
+    e2e_each = []  # per-step spread (diagnostic; the value above is the K-step mean)
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_each.append(round(e0.elapsed_time(e1), 3))
     e2e = {
         "value": world * n / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
         "h2d_bytes_per_step": int(host_pts.numel() * host_pts.element_size()),
         "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
-        "ms_per_step": e2e_ms, "steps": e2e_steps,
+        "ms_per_step": e2e_ms, "steps": e2e_steps, "extra_step_ms": e2e_each,
         "path": "PlanInterpreter.eval_batch(grid, pinned CPU tensor, out=pinned CPU tensor, order='morton')",
     }
     del host_pts, host_out
@@ -551,6 +561,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
+    ap.add_argument("--ref-total-seconds", type=float, default=150.0,
+                    help="time budget of the whole --impl reference run (steps + warmup)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -141,6 +141,21 @@ int sp_eval_bricks(const sp_plan* plan, const sp_grid_desc* grid, const void* pt
  * or a negative value when brick mode is not applicable. */
 int sp_brick_log2(const sp_plan* plan, int32_t dtype);
 
+/* Sync-free brick mode.  sp_brick_runs finds the brick runs of Morton-ordered points from
+ * their sp_morton_keys (brick id = key >> 3*log2_brick): brick_start (device, capacity
+ * n + 1) and the brick count (device int32), without a host round trip.
+ * sp_eval_bricks_dev is sp_eval_bricks with the brick count read from device memory
+ * (n_bricks_cap bounds it and sizes the launch), so a host pipeline can queue chunk after
+ * chunk without synchronising (runtime.py:244-248 over pinned host batches). */
+int sp_brick_runs(const uint64_t* keys, int64_t n, int32_t log2_brick, int64_t* brick_start, int32_t* n_bricks,
+                  void* temp, int64_t temp_bytes, void* stream);
+/* device scratch bytes sp_brick_runs needs for n points (pass it as temp/temp_bytes to avoid
+ * a stream-ordered allocation per call; temp may be NULL). */
+int64_t sp_brick_runs_temp_bytes(int64_t n);
+int sp_eval_bricks_dev(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+                       const int64_t* brick_start, const int32_t* n_bricks_dev, int32_t n_bricks_cap,
+                       int32_t log2_brick, const int64_t* out_index, void* out, int32_t* err_flag, void* stream);
+
 /* Synchronous convenience: sp_eval + stream sync + sentinel check (SP_ERR_SENTINEL). */
 int sp_eval_sync(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
                  void* out, void* stream);

@@ -130,6 +130,18 @@ EXPORTS = {
          ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
     ),
     "sp_brick_log2": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
+    "sp_brick_runs": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_int64, ctypes.c_void_p],
+    ),
+    "sp_brick_runs_temp_bytes": (ctypes.c_int64, [ctypes.c_int64]),
+    "sp_eval_bricks_dev": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.POINTER(GridDesc), ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p],
+    ),
     "sp_texture_create": (ctypes.c_int, [ctypes.POINTER(GridDesc), ctypes.POINTER(ctypes.c_void_p)]),
     "sp_texture_destroy": (None, [ctypes.c_void_p]),
     "sp_eval_texture": (

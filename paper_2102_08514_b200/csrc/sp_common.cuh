@@ -64,6 +64,7 @@ struct EvalArgs {
     const long long* out_index; // nullable: value of point i goes to out[out_index[i]]
     int trec_bytes;             // per-(coset, class) tile records (generated kernels), in smem
     int vec_cap;                // row-vector tile capacity in elements (0: no row-vector tile)
+    const int* nbricks_dev;     // nullable: brick count in device memory (sync-free brick runs)
 };
 
 struct TileGeom {
@@ -617,6 +618,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     V* vtile = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(tile) +
                                     (((a.tile_cap + 4) * (int)sizeof(T) + 15) & ~15));
     const int B = 1 << log2b;
+    if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);
 
     for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
         const long long p0 = brick_start[b], p1 = brick_start[b + 1];

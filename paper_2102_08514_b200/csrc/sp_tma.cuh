@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         tma_load_3d(buf(slot), &tmap, &mbar[slot], z2, z1, z0);
     };
 
+    if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);
     if (tid == 0 && (int)blockIdx.x < nbricks) issue(blockIdx.x, 0);
     unsigned phase = 0u;  // bit s = mbarrier parity of buffer s
     int it = 0;

@@ -10,6 +10,9 @@
 //   * the generic table-driven kernel.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 #include <algorithm>
 #include <map>
 #include <mutex>
@@ -747,12 +750,13 @@ int try_bricks_tma(const sp_plan* p, const sp_grid_desc* g, const sp::EvalArgs<f
 template <typename T>
 int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, const int64_t* bstart,
                       int32_t nbricks, int32_t log2b, const int64_t* out_index, void* out, int32_t* err,
-                      cudaStream_t st) {
+                      cudaStream_t st, const int32_t* nbricks_dev = nullptr) {
     sp::EvalArgs<T> a;
     int vec = 0;
     int rc = build_args<T>(p, g, pts, n, out, nullptr, err, a, vec);
     if (rc != SP_OK) return rc;
     a.out_index = reinterpret_cast<const long long*>(out_index);
+    a.nbricks_dev = nbricks_dev;
     if constexpr (sizeof(T) == 4) {
         const int t = try_bricks_tma(p, g, a, bstart, nbricks, log2b, st);
         if (t != 0) return t > 0 ? SP_OK : t;
@@ -842,6 +846,27 @@ extern "C" int sp_eval_bricks(const sp_plan* plan, const sp_grid_desc* grid, con
     return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
 }
 
+extern "C" int sp_eval_bricks_dev(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n,
+                                  int32_t dtype, const int64_t* brick_start, const int32_t* n_bricks_dev,
+                                  int32_t n_bricks_cap, int32_t log2_brick, const int64_t* out_index, void* out,
+                                  int32_t* err_flag, void* stream) {
+    if (!plan) return fail(SP_ERR_INVALID, "null plan");
+    int rc = check_grid(plan, grid, dtype);
+    if (rc != SP_OK) return rc;
+    if (n < 0 || n_bricks_cap < 0) return fail(SP_ERR_INVALID, "negative size");
+    if (n == 0 || n_bricks_cap == 0) return SP_OK;
+    if (log2_brick < 0 || log2_brick > 20) return fail(SP_ERR_INVALID, "log2_brick out of range");
+    if (!pts || !out || !brick_start || !n_bricks_dev) return fail(SP_ERR_INVALID, "null points, output or brick runs");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32)
+        return eval_bricks_typed<float>(plan, grid, pts, n, brick_start, n_bricks_cap, log2_brick, out_index, out,
+                                        err_flag, st, n_bricks_dev);
+    if (dtype == SP_F64)
+        return eval_bricks_typed<double>(plan, grid, pts, n, brick_start, n_bricks_cap, log2_brick, out_index, out,
+                                         err_flag, st, n_bricks_dev);
+    return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
 extern "C" int sp_eval_sync(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
                             void* out, void* stream) {
     int32_t* d_err = nullptr;
@@ -928,6 +953,58 @@ int grid_for(int64_t n) {
 }
 
 }  // namespace
+
+// Brick runs of Morton-ordered points without a host round trip: brick_start[0..count) =
+// indices whose brick id (key >> 3*log2b) differs from the previous point's, then
+// brick_start[count] = n, count written to device memory (CUB stream compaction).
+struct BrickHead {
+    const uint64_t* keys;
+    int shift;
+    __host__ __device__ bool operator()(long long i) const {
+        return i == 0 || (keys[i] >> shift) != (keys[i - 1] >> shift);
+    }
+};
+
+__global__ void brick_runs_tail(long long n, const int32_t* count, int64_t* brick_start) { brick_start[*count] = n; }
+
+extern "C" int64_t sp_brick_runs_temp_bytes(int64_t n) {
+    if (n <= 0 || n >= (1ll << 31)) return 0;
+    size_t bytes = 0;
+    thrust::counting_iterator<long long> idx(0);
+    const BrickHead head{nullptr, 0};
+    if (cub::DeviceSelect::If(nullptr, bytes, idx, static_cast<int64_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                              (int)n, head) != cudaSuccess)
+        return -1;
+    return (int64_t)bytes;
+}
+
+extern "C" int sp_brick_runs(const uint64_t* keys, int64_t n, int32_t log2_brick, int64_t* brick_start,
+                             int32_t* n_bricks, void* temp, int64_t temp_bytes, void* stream) {
+    if (n < 0 || n >= (1ll << 31)) return fail(SP_ERR_INVALID, "brick runs: n out of range");
+    if (log2_brick < 0 || log2_brick > 20) return fail(SP_ERR_INVALID, "log2_brick out of range");
+    if ((n > 0 && !keys) || !brick_start || !n_bricks) return fail(SP_ERR_INVALID, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        SP_CUDA(cudaMemsetAsync(n_bricks, 0, sizeof(int32_t), st));
+        SP_CUDA(cudaMemsetAsync(brick_start, 0, sizeof(int64_t), st));
+        return SP_OK;
+    }
+    const BrickHead head{keys, 3 * log2_brick};
+    thrust::counting_iterator<long long> idx(0);
+    size_t bytes = 0;
+    SP_CUDA(cub::DeviceSelect::If(nullptr, bytes, idx, brick_start, n_bricks, (int)n, head, st));
+    void* tmp = temp;
+    if (!tmp || (size_t)temp_bytes < bytes) {  // no (or too small) caller scratch: stream-ordered allocation
+        tmp = nullptr;
+        SP_CUDA(cudaMallocAsync(&tmp, bytes, st));
+    }
+    const cudaError_t e = cub::DeviceSelect::If(tmp, bytes, idx, brick_start, n_bricks, (int)n, head, st);
+    if (tmp != temp) cudaFreeAsync(tmp, st);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "brick runs: %s", cudaGetErrorString(e));
+    brick_runs_tail<<<1, 1, 0, st>>>(n, n_bricks, brick_start);
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
+}
 
 extern "C" int sp_morton_keys(const void* pts, int64_t n, int32_t dtype, uint64_t* keys, void* stream) {
     if (n <= 0) return SP_OK;

@@ -353,44 +353,74 @@ class PlanInterpreter:
     # points per pipelined host chunk (pinned host buffers, see _eval_host_pipelined)
     host_chunk = 1 << 22
 
+    # device slots of the pinned-host pipeline (ring of chunk buffers)
+    host_slots = 3
+
+    def _pipeline_state(self, dev, dtype, s):
+        """Per (device, dtype) pipeline resources, created once: three streams (H2D copy,
+        compute, D2H copy) and a ring of `host_slots` chunk buffers with their events."""
+        key = (dev, dtype, s, self.host_chunk, self.host_slots)
+        st = self.__dict__.setdefault("_pipes", {}).get(key)
+        if st is None:
+            C = self.host_chunk
+            slots = []
+            for _ in range(self.host_slots):
+                slots.append({
+                    "p": torch.empty((C, s), dtype=dtype, device=dev),
+                    "r": torch.empty(C, dtype=dtype, device=dev),
+                    "scratch": torch.empty(max(1, int(_native.lib().sp_brick_runs_temp_bytes(C))), dtype=torch.uint8,
+                                           device=dev),
+                    "evaluated": None, "returned": None,
+                })
+            st = {"h2d": torch.cuda.Stream(dev), "comp": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
+                  "slots": slots}
+            self._pipes[key] = st
+        return st
+
     def _eval_host_pipelined(self, grid, pts, out, *, check, order, stream):
         """Pinned host points -> pinned host results, overlapping the PCIe transfers with
         each other and with the evaluation: the batch is cut into chunks of `host_chunk`
-        points; all host->device copies are queued on one copy stream, each chunk's
-        evaluation waits for its copy on the compute stream, and each result chunk goes back
-        on a third stream as soon as it is evaluated.  Chunks are contiguous ranges, so a
+        points that cycle through a ring of `host_slots` device buffers; chunk i is copied
+        in on the H2D stream (once its slot's previous chunk is evaluated), evaluated on the
+        compute stream (sync-free brick runs, no host round trip) and copied back on the D2H
+        stream, so result copies overlap point copies.  Chunks are contiguous ranges, so a
         Morton-ordered batch gives Morton-ordered chunks; values are identical to the
         one-shot path (every point is evaluated by the same arithmetic)."""
         dev = grid.device
-        n = pts.shape[0]
+        n, s = pts.shape
         caller = stream if stream is not None else torch.cuda.current_stream(dev)
-        h2d = torch.cuda.Stream(dev)
-        d2h = torch.cuda.Stream(dev)
-        comp = torch.cuda.Stream(dev)
+        state = self._pipeline_state(dev, grid.dtype, s)
+        h2d, comp, d2h = state["h2d"], state["comp"], state["d2h"]
         res_host = out if out is not None else torch.empty(n, dtype=grid.dtype, pin_memory=True)
-        with torch.cuda.stream(caller):
-            p_dev = torch.empty((n, pts.shape[1]), dtype=grid.dtype, device=dev)
-            r_dev = torch.empty(n, dtype=grid.dtype, device=dev)
         for s_ in (h2d, d2h, comp):
             s_.wait_stream(caller)
-        C = self.host_chunk
-        bounds = [(i, min(i + C, n)) for i in range(0, n, C)]
-        copied = []
-        with torch.cuda.stream(h2d):
-            for a, b in bounds:
-                p_dev[a:b].copy_(pts[a:b], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(h2d)
-                copied.append(ev)
         err = torch.zeros(1, dtype=torch.int32, device=dev) if check else None
-        for (a, b), ev in zip(bounds, copied):
-            comp.wait_event(ev)
-            self._launch(grid, p_dev[a:b], r_dev[a:b], check=False, order=order, stream=comp, err=err)
-            done = torch.cuda.Event()
-            done.record(comp)
-            d2h.wait_event(done)
+        C = self.host_chunk
+        slots = state["slots"]
+        for i, a in enumerate(range(0, n, C)):
+            b = min(a + C, n)
+            m = b - a
+            sl = slots[i % len(slots)]
+            if sl["evaluated"] is not None:
+                h2d.wait_event(sl["evaluated"])  # input slot free
+            with torch.cuda.stream(h2d):
+                sl["p"][:m].copy_(pts[a:b], non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(h2d)
+            comp.wait_event(copied)
+            if sl["returned"] is not None:
+                comp.wait_event(sl["returned"])  # output slot free
+            self._launch(grid, sl["p"][:m], sl["r"][:m], check=False, order=order, stream=comp, err=err,
+                         sync_free=True, scratch=sl["scratch"])
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            sl["evaluated"] = ev
+            d2h.wait_event(ev)
             with torch.cuda.stream(d2h):
-                res_host[a:b].copy_(r_dev[a:b], non_blocking=True)
+                res_host[a:b].copy_(sl["r"][:m], non_blocking=True)
+            ret = torch.cuda.Event()
+            ret.record(d2h)
+            sl["returned"] = ret
         caller.wait_stream(d2h)
         caller.wait_stream(comp)
         if check:
@@ -416,7 +446,14 @@ class PlanInterpreter:
         if check:
             err = torch.zeros(1, dtype=torch.int32, device=dev)
         idx = batch.perm if (unpermute and batch.perm is not None) else None
-        if n:
+        if n and batch.n_bricks_dev is not None:
+            with torch.cuda.stream(st):
+                _native.check(lib.sp_eval_bricks_dev(h, ctypes.byref(gdesc), batch.pts.data_ptr(), n, dtype,
+                                                     batch.brick_start.data_ptr(), batch.n_bricks_dev.data_ptr(),
+                                                     batch.n_bricks_cap, batch.log2_brick,
+                                                     None if idx is None else idx.data_ptr(), res.data_ptr(),
+                                                     None if err is None else err.data_ptr(), st.cuda_stream))
+        elif n:
             with torch.cuda.stream(st):
                 _native.check(lib.sp_eval_bricks(h, ctypes.byref(gdesc), batch.pts.data_ptr(), n, dtype,
                                                  batch.brick_start.data_ptr(), batch.n_bricks, batch.log2_brick,
@@ -470,7 +507,8 @@ class PlanInterpreter:
             self._launch(grid, p, res, dbg=dbg, check=False)
         return dbg[:, :, 0].to(torch.int64), dbg[:, :, 1:].to(torch.int64)
 
-    def _launch(self, grid, p, res, *, dbg=None, check=True, order="given", stream=None, err=None):
+    def _launch(self, grid, p, res, *, dbg=None, check=True, order="given", stream=None, err=None, sync_free=False,
+                scratch=None):
         """Evaluate device points p into res on `stream`.  `err` (optional int32 device flag)
         accumulates sigma-sentinel hits without synchronising; with check=True a fresh flag
         is used and tested."""
@@ -484,7 +522,10 @@ class PlanInterpreter:
         n = p.shape[0]
         b = self.brick_log2(grid) if (order != "given" and dbg is None) else -1
         if b >= 0:
-            batch = prepare_points(p, b, presorted=(order == "morton"), stream=st)
+            if sync_free:
+                batch = prepare_points_async(p, b, presorted=(order == "morton"), stream=st, scratch=scratch)
+            else:
+                batch = prepare_points(p, b, presorted=(order == "morton"), stream=st)
             self._eval_bricks(grid, batch, out=res, check=check, stream=st, err=err)
             return
         with torch.cuda.stream(st):
@@ -520,11 +561,15 @@ class PointBatch:
     `prepare_points`; evaluate with `PlanInterpreter.eval_batch(grid, batch)`.
     """
 
-    def __init__(self, pts: torch.Tensor, brick_start: torch.Tensor, log2_brick: int, perm: torch.Tensor | None):
+    def __init__(self, pts: torch.Tensor, brick_start: torch.Tensor, log2_brick: int, perm: torch.Tensor | None,
+                 n_bricks_dev: torch.Tensor | None = None):
         self.pts = pts
         self.brick_start = brick_start
         self.log2_brick = int(log2_brick)
         self.perm = perm
+        # sync-free runs: the count lives on the device (int32 [1]); brick_start has
+        # capacity n + 1 and only its first count + 1 entries are meaningful
+        self.n_bricks_dev = n_bricks_dev
 
     @property
     def n(self) -> int:
@@ -532,7 +577,42 @@ class PointBatch:
 
     @property
     def n_bricks(self) -> int:
+        if self.n_bricks_dev is not None:
+            return int(self.n_bricks_dev.item())  # synchronises
         return self.brick_start.shape[0] - 1
+
+    @property
+    def n_bricks_cap(self) -> int:
+        return self.brick_start.shape[0] - 1
+
+
+def prepare_points_async(pts: torch.Tensor, log2_brick: int, *, presorted: bool = False,
+                         stream: torch.cuda.Stream | None = None, scratch: torch.Tensor | None = None) -> PointBatch:
+    """prepare_points without any host synchronisation (64-bit Morton keys, GPU sort when
+    not presorted, brick runs by sp_brick_runs with the count kept on the device), so a host
+    pipeline can queue many batches back to back."""
+    lib = _native.lib()
+    st = stream if stream is not None else torch.cuda.current_stream(pts.device)
+    pts = pts.contiguous()
+    n = pts.shape[0]
+    dtype = _native.SP_F32 if pts.dtype == torch.float32 else _native.SP_F64
+    with torch.cuda.stream(st):
+        keys = torch.empty(n, dtype=torch.int64, device=pts.device)
+        _native.check(lib.sp_morton_keys(pts.data_ptr(), n, dtype, keys.data_ptr(), st.cuda_stream))
+        perm = None
+        if not presorted and n:
+            keys, perm = torch.sort(keys)
+            sp = torch.empty_like(pts)
+            _native.check(lib.sp_gather_points(pts.data_ptr(), perm.data_ptr(), n, dtype, sp.data_ptr(), st.cuda_stream))
+            pts = sp
+        start = torch.empty(n + 1, dtype=torch.int64, device=pts.device)
+        count = torch.empty(1, dtype=torch.int32, device=pts.device)
+        need = int(lib.sp_brick_runs_temp_bytes(n))
+        if scratch is None or scratch.numel() < need:
+            scratch = torch.empty(max(need, 1), dtype=torch.uint8, device=pts.device)
+        _native.check(lib.sp_brick_runs(keys.data_ptr(), n, int(log2_brick), start.data_ptr(), count.data_ptr(),
+                                        scratch.data_ptr(), scratch.numel(), st.cuda_stream))
+    return PointBatch(pts, start, log2_brick, perm, n_bricks_dev=count)
 
 
 def prepare_points(pts: torch.Tensor, log2_brick: int, *, presorted: bool = False,

@@ -295,3 +295,33 @@ def test_pipelined_host_path_raises_on_sentinel(cuda):
     with pytest.raises(RuntimeError_):
         interp.eval_batch(grid, pts)
     interp.eval_batch(grid, torch.from_numpy(clean).pin_memory())  # no hit: no error
+
+
+@pytest.mark.parametrize("name,presorted", [("cc_tricubic", True), ("cc_tricubic", False), ("fcc_cubic", True),
+                                            ("bcc_quintic_rd", False)])
+def test_sync_free_brick_runs_match(name, presorted, cuda):
+    """sp_brick_runs (device-side run detection, count in device memory) gives the same brick
+    runs as the host path, and sp_eval_bricks_dev the same values."""
+    from paper_2102_08514_b200.runtime import prepare_points, prepare_points_async
+
+    g, plan, grid = _setup(name, "zero", torch.float32, cuda)
+    interp = PlanInterpreter(plan)
+    pts = torch.from_numpy(g["pts"]).to(cuda)
+    if presorted:
+        pts = interp.prepare(grid, pts).pts
+    b = interp.brick_log2(grid)
+    ref = prepare_points(pts, b, presorted=presorted)
+    asy = prepare_points_async(pts, b, presorted=presorted)
+    nb = asy.n_bricks
+    assert asy.n_bricks_cap == pts.shape[0]
+    if presorted:  # same order in, same runs out
+        assert nb == ref.n_bricks
+        torch.testing.assert_close(asy.brick_start[: nb + 1], ref.brick_start, rtol=0, atol=0)
+        torch.testing.assert_close(asy.pts, ref.pts, rtol=0, atol=0)
+    else:  # the host path may sort by bbox-relative 32-bit keys: a different (equally valid) order
+        st = asy.brick_start[: nb + 1]
+        assert int(st[0]) == 0 and int(st[-1]) == pts.shape[0] and bool((st[1:] > st[:-1]).all())
+    torch.testing.assert_close(interp.eval_batch(grid, asy), interp.eval_batch(grid, ref), rtol=0, atol=0,
+                               equal_nan=True)
+    empty = prepare_points_async(pts[:0], b, presorted=True)
+    assert empty.n_bricks == 0 and interp.eval_batch(grid, empty).numel() == 0
