@@ -3,6 +3,7 @@
 
 #include <map>
 #include <mutex>
+#include <utility>
 
 #include "sp_common.cuh"
 #include "sp_evaluators.cuh"
@@ -13,16 +14,18 @@ namespace sp {
 // costs tens of microseconds of host time, which short launches cannot hide.
 template <typename K>
 static int cached_occupancy(K kern, size_t smem) {
+    // keyed by the kernel too: every kernel of one signature shares this instantiation
     static std::mutex mu;
-    static std::map<size_t, int> memo;
+    static std::map<std::pair<const void*, size_t>, int> memo;
     std::lock_guard<std::mutex> lock(mu);
-    auto it = memo.find(smem);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), smem);
+    auto it = memo.find(key);
     if (it != memo.end()) return it->second;
     int per_sm = 0;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-    memo[smem] = per_sm;
+    memo[key] = per_sm;
     return per_sm;
 }
 

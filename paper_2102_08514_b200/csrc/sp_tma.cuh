@@ -46,6 +46,28 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// Row-vector copy of a staged box: vtile[(z*vy + y)*vx + x] = tile[(z*by + y)*bx + x .. +kVec)
+// (the (vx, vy) pitches may be padded for conflict-free row loads).
+template <typename T, int kVec>
+__device__ __forceinline__ void build_vtile(const T* tile, typename VecT<T, kVec>::type* vtile, int boxv, bool padded,
+                                            int bx, int by, int vx, int vy, unsigned mx, unsigned sx, unsigned my,
+                                            unsigned sy, int tid) {
+    using V = typename VecT<T, kVec>::type;
+    for (int e = tid; e < boxv; e += kThreads) {
+        V v;
+        T* pv = reinterpret_cast<T*>(&v);
+#pragma unroll
+        for (int q = 0; q < kVec; ++q) pv[q] = e + q < boxv ? tile[e + q] : T(0);
+        int d = e;
+        if (padded) {
+            const int r = (int)fastdiv((unsigned)e, mx, sx);  // z*by + y
+            const int z = (int)fastdiv((unsigned)r, my, sy);
+            d = (r + z * (vy - by)) * vx + (e - r * bx);
+        }
+        vtile[d] = v;
+    }
+}
+
 // Single-coset (M = 1) brick kernel, T = float, evaluators with a row-vector tile.
 // box = (bz, by, bx) coset cells; bx is a multiple of 4 (16-byte TMA rows) and 3 wider than
 // needed, because the box's innermost start coordinate must be 16-byte aligned; the host may
@@ -115,20 +137,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         const int c0 = corner[cur][0], c1 = corner[cur][1], c2 = corner[cur][2];
         const int lo0 = c0 + a.fr.reach_lo[0], lo1 = c1 + a.fr.reach_lo[1];
         const int lo2 = ((c2 + a.fr.reach_lo[2] - a.grid.org[0][2]) & ~3) + a.grid.org[0][2];
-        // row-vector copy of the box: vtile[(z*vy + y)*vx + x] = tile[(z*by + y)*bx + x .. +kVec)
-        for (int e = tid; e < boxv; e += kThreads) {
-            V v;
-            T* pv = reinterpret_cast<T*>(&v);
-#pragma unroll
-            for (int q = 0; q < kVec; ++q) pv[q] = e + q < boxv ? tile[e + q] : T(0);
-            int d = e;
-            if (padded) {
-                const int r = (int)fastdiv((unsigned)e, mx, sx);  // z*by + y
-                const int z = (int)fastdiv((unsigned)r, my, sy);
-                d = (r + z * (vy - by)) * vx + (e - r * bx);
-            }
-            vtile[d] = v;
-        }
+        build_vtile<T, kVec>(tile, vtile, boxv, padded, bx, by, vx, vy, mx, sx, my, sy, tid);
         if (tid == 0) {
             geom.staged = 1;
             geom.total = boxv;
