@@ -28,6 +28,8 @@ from __future__ import annotations
 
 import os
 import re
+
+import numpy as np
 from fractions import Fraction
 from typing import List
 
@@ -160,6 +162,38 @@ def _poly_expr(poly, have, lines, ops_box, tag) -> str:
     return tag
 
 
+def _group_body(g, d: int, gname: str, tnames: list, body_lines: list, ops: list) -> list:
+    """One fetch group's block: weight lines, then the (software-merged) fetch and accumulate."""
+    body = ["    {"] + [f"        {ln}" for ln in body_lines]
+    sd = [tuple(v // d for v in site) for site in g.sites]
+    ns = len(g.span_axes)
+    if ns == 0:
+        body.append(f"        acc = fma({gname}, f.get({sd[0][0]}, {sd[0][1]}, {sd[0][2]}), acc);")
+        ops[0] += 1
+    elif ns == 1:
+        body.append(f"        const T c0 = f.get({sd[0][0]}, {sd[0][1]}, {sd[0][2]});")
+        body.append(f"        const T c1 = f.get({sd[1][0]}, {sd[1][1]}, {sd[1][2]});")
+        body.append(f"        acc = fma({gname}, c0, acc);")
+        body.append(f"        acc = fma({tnames[0]}, c1 - c0, acc);")
+        ops[0] += 3
+    else:
+        body.append(f"        const T gz = {gname};")
+        body.append("        const T rg = gz == T(0) ? T(0) : T(1) / gz;")
+        for j in range(ns):
+            body.append(f"        const T t{j} = gz == T(0) ? T(0.5) : {tnames[j]} * rg;")
+        for c in range(1 << ns):
+            body.append(f"        T v{c} = f.get({sd[c][0]}, {sd[c][1]}, {sd[c][2]});")
+        for j in range(ns):
+            step = 1 << j
+            for c in range(0, 1 << ns, 2 * step):
+                body.append(f"        v{c} = fma(t{j}, v{c + step} - v{c}, v{c});")
+                ops[0] += 2
+        body.append("        acc = fma(gz, v0, acc);")
+        ops[0] += 1 + ns
+    body.append("    }")
+    return body
+
+
 def _kernel_function(plan: EvaluationPlan, kidx: int, d: int) -> tuple:
     kern = plan.kernels[kidx]
     polys = [g.g for g in kern.groups] + [t for g in kern.groups for t in g.t_nums]
@@ -176,34 +210,7 @@ def _kernel_function(plan: EvaluationPlan, kidx: int, d: int) -> tuple:
         body_lines = []
         gname = _poly_expr(g.g, have, body_lines, ops, f"g{gi}")
         tnames = [_poly_expr(t, have, body_lines, ops, f"tn{gi}_{j}") for j, t in enumerate(g.t_nums)]
-        body = ["    {"] + [f"        {ln}" for ln in body_lines]
-        sd = [tuple(v // d for v in site) for site in g.sites]
-        ns = len(g.span_axes)
-        if ns == 0:
-            body.append(f"        acc = fma({gname}, f.get({sd[0][0]}, {sd[0][1]}, {sd[0][2]}), acc);")
-            ops[0] += 1
-        elif ns == 1:
-            body.append(f"        const T c0 = f.get({sd[0][0]}, {sd[0][1]}, {sd[0][2]});")
-            body.append(f"        const T c1 = f.get({sd[1][0]}, {sd[1][1]}, {sd[1][2]});")
-            body.append(f"        acc = fma({gname}, c0, acc);")
-            body.append(f"        acc = fma({tnames[0]}, c1 - c0, acc);")
-            ops[0] += 3
-        else:
-            body.append(f"        const T gz = {gname};")
-            body.append("        const T rg = gz == T(0) ? T(0) : T(1) / gz;")
-            for j in range(ns):
-                body.append(f"        const T t{j} = gz == T(0) ? T(0.5) : {tnames[j]} * rg;")
-            for c in range(1 << ns):
-                body.append(f"        T v{c} = f.get({sd[c][0]}, {sd[c][1]}, {sd[c][2]});")
-            for j in range(ns):
-                step = 1 << j
-                for c in range(0, 1 << ns, 2 * step):
-                    body.append(f"        v{c} = fma(t{j}, v{c + step} - v{c}, v{c});")
-                    ops[0] += 2
-            body.append("        acc = fma(gz, v0, acc);")
-            ops[0] += 1 + ns
-        body.append("    }")
-        out.extend(body)
+        out.extend(_group_body(g, d, gname, tnames, body_lines, ops))
     out.append("    return acc;")
     out.append("}")
     return out, ops[0]
@@ -234,6 +241,232 @@ def weight_flops(plan: EvaluationPlan) -> list:
     return [_kernel_function(plan, k, plan.diag[0])[1] for k in range(plan.K)]
 
 
+def affine_tables(plan: EvaluationPlan):
+    """Weight programs folded into the coset frame, for plans whose weight polynomials are
+    all affine (degree <= 1), K = 1 and r <= 64 (bcc_linear_rd).
+
+    Per plane code q in [0, r) with class c = sigma[q] (class 0 for the sentinel, which is
+    flagged, runtime.py:380-381), every polynomial p(y) of the kernel with y = T_c xp - t_c
+    (runtime.py:385) is the affine form A . xp + C.  T_c is a signed permutation and t_c
+    integral, so A and C are small dyadic rationals, exact in float32, and evaluating
+    A . xp + C by an FMA chain rounds exactly where y_i = +-xp_j - t_i did.  The per-class
+    transform (perm / sign decode + selects) disappears from the per-point program.
+    Returns (polys per q: [[(A0, A1, A2, C), ...] * r], sentinel mask) or None."""
+    if plan.K != 1 or plan.r > 64 or plan.M > 8:
+        return None
+    polys = []
+    for g in plan.kernels[0].groups:
+        polys.append(g.g)
+        polys.extend(g.t_nums)
+    if len(polys) > 8 or any(q.degree() > 1 for q in polys):
+        return None
+    rows, mask = [], 0
+    for q in range(plan.r):
+        c = plan.sigma[q]
+        if c < 0:
+            mask |= 1 << q
+            c = 0
+        ct = plan.classes[c]
+        T = [[Fraction(v) for v in row] for row in ct.T]
+        t = [Fraction(v) for v in ct.t]
+        row = []
+        for poly in polys:
+            A = [Fraction(0)] * 3
+            C = Fraction(poly.terms.get((0, 0, 0), 0))
+            for e, coef in poly.terms.items():
+                if sum(e) == 0:
+                    continue
+                i = e.index(1)
+                for j in range(3):
+                    A[j] += Fraction(coef) * T[i][j]
+                C -= Fraction(coef) * t[i]
+            vals = A + [C]
+            # exact in binary16: the table is stored as half2 pairs (one LDS.128 per two polys)
+            if any(float(np.float16(float(v))) != v for v in vals):
+                return None
+            row.append(tuple(vals))
+        rows.append(row)
+    return rows, mask
+
+
+def _affine_kernel_function(plan: EvaluationPlan, d: int) -> tuple:
+    kern = plan.kernels[0]
+    out = [
+        "__device__ __forceinline__ float2 half2_bits(unsigned w) {",
+        "    __half2 v;",
+        "    memcpy(&v, &w, 4);",
+        "    return __half22float2(v);",
+        "}",
+        "",
+        "template <typename T, class F>",
+        "__device__ __forceinline__ T kernel_aff(const T xq0, const T xq1, const T xq2, const uint4* co, const F& f) {",
+        "    T acc = T(0);",
+    ]
+    ops = [0]
+    p = 0
+
+    def aff(tag):
+        nonlocal p
+        lines = []
+        if p % 2 == 0:
+            lines.append(f"const uint4 h{p // 2} = co[{p // 2}];")
+        w = ("x", "y") if p % 2 == 0 else ("z", "w")
+        lines.append(f"const float2 a{p} = half2_bits(h{p // 2}.{w[0]}), b{p} = half2_bits(h{p // 2}.{w[1]});")
+        lines.append(f"const T {tag} = fma(T(b{p}.x), xq2, fma(T(a{p}.y), xq1, fma(T(a{p}.x), xq0, T(b{p}.y))));")
+        p += 1
+        ops[0] += 3
+        return lines
+
+    for gi, g in enumerate(kern.groups):
+        body_lines = aff(f"g{gi}")
+        tnames = []
+        for j in range(len(g.t_nums)):
+            body_lines += aff(f"tn{gi}_{j}")
+            tnames.append(f"tn{gi}_{j}")
+        out.extend(_group_body(g, d, f"g{gi}", tnames, body_lines, ops))
+    out.append("    return acc;")
+    out.append("}")
+    return out, ops[0], p
+
+
+def _affine_eval_source(plan: EvaluationPlan, rows, mask, min_blocks: int) -> str:
+    """Eval<T> of an affine plan: q -> per-(coset, q) tile record + per-q coefficients."""
+    npoly = len(rows[0])
+    nvec = (npoly + 1) // 2
+
+    def h(v):
+        return int(np.array([float(v)], dtype=np.float16).view(np.uint16)[0])
+
+    vecs = []
+    for row in rows:
+        words = []
+        for a0, a1, a2, c in list(row) + [(0, 0, 0, 0)] * (2 * nvec - npoly):
+            words += [h(a0) | h(a1) << 16, h(a2) | h(c) << 16]
+        vecs += ["{" + ", ".join(f"0x{w:08x}u" for w in words[4 * i:4 * i + 4]) + "}" for i in range(nvec)]
+    flat = ",\n    ".join(vecs)
+    return f"""constexpr int kNP = {npoly};
+constexpr int kNV = {nvec};  // uint4 per q: two polynomials as half2 (A0, A1), (A2, C) each
+constexpr unsigned long long kSentinel = {mask}ull;  // bit q: sigma[q] < 0
+// per q: the kernel's polynomials as (A0, A1, A2, C) in the coset frame xp (class sigma[q]),
+// binary16 (every value is a small dyadic rational, exact)
+__device__ const uint4 kAff[kR * kNV] = {{
+    {flat}
+}};
+
+// coset frame only (no class transform): xp exactly as runtime.py:371-373
+template <typename T>
+__device__ __forceinline__ void frame_f64(const T x[3], int k, int cell[3], double xp[3]) {{
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {{
+        const double xl = (double)x[i] - kShift[k][i];
+        const double q = floor(xl * kInvD);  // power-of-two d: exact
+        xp[i] = xl - q * kD;
+        cell[i] = clamp_cell(q);
+    }}
+}}
+__device__ __forceinline__ void frame_fast(const float frac[3], const int X[3], int k, int cell[3], float xp[3]) {{
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {{
+        const int xm = X[i] - kShiftI[k][i];
+        cell[i] = xm >> kLog2D;
+        const int p = xm & (kDI - 1);
+        xp[i] = kDI == 1 ? frac[i] : (kDI == 2 ? (p ? frac[i] + 1.0f : frac[i]) : frac[i] + (float)p);
+    }}
+}}
+
+template <typename T>
+struct Eval {{
+    static constexpr int kMinBlocks = {min_blocks};
+    static constexpr int kTrecBytes = kM * kR * 16 + kR * kNV * 16;
+    template <typename U>
+    static constexpr int vec_width() {{
+        return 0;
+    }}
+    // per-(coset, q) tile address records {{coef of site/d component 0, 1, 2; pib/d offset}} of
+    // class max(sigma[q], 0), then the per-q coefficient table (computed per tile)
+    __device__ static void tile_records(const EvalArgs<T>& a, const TileGeom& g, const unsigned char* tables,
+                                        int4* trec, int tid) {{
+        const int* sigma = reinterpret_cast<const int*>(tables);
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
+        for (int idx = tid; idx < kM * kR; idx += kThreads) {{
+            const int k = idx / kR, q = idx - k * kR;
+            const uint4 rec = cls_tab[max(sigma[q], 0)];
+            const int st[3] = {{g.ex[k][1] * g.ex[k][2], g.ex[k][2], 1}};
+            int cf[3] = {{0, 0, 0}}, z = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {{
+                const int rho = (int)((rec.x >> (13 + 2 * i)) & 3u);
+                const int tau = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
+                const int pb = (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
+                cf[rho] = tau * st[i];
+                z += pb * st[i];
+            }}
+            trec[idx] = make_int4(cf[0], cf[1], cf[2], z);
+        }}
+        uint4* co = reinterpret_cast<uint4*>(trec + kM * kR);
+        for (int idx = tid; idx < kR * kNV; idx += kThreads) co[idx] = kAff[idx];
+    }}
+    template <class F, class Ctx>
+    __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
+        const EvalArgs<T>& a = *ctx.a;
+        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
+        bool fast = false;
+        float frac[3] = {{0.f, 0.f, 0.f}};
+        if constexpr (sizeof(T) == 4) {{
+            const float m = fminf(fminf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
+            const float M = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
+            fast = m >= kFastLo && M < kFastHi;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) frac[i] = (float)x[i] - floorf((float)x[i]);
+        }}
+        T total = T(0);
+#pragma unroll
+        for (int k = 0; k < kM; ++k) {{
+            int cell[3], q;
+            T xq[3];
+            if (fast) {{
+                float xp[3];
+                frame_fast(frac, ctx.X, k, cell, xp);
+                q = plane_code<float>(xp[0], xp[1], xp[2]) % kR;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) xq[i] = (T)xp[i];
+            }} else {{
+                double xp[3];
+                frame_f64<T>(x, k, cell, xp);
+                q = plane_code<double>(xp[0], xp[1], xp[2]) % kR;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) xq[i] = (T)xp[i];
+            }}
+            ctx.err |= (int)((kSentinel >> q) & 1ull);  // sentinel (runtime.py:380-381): evaluated as class 0
+            if (a.dbg) write_dbg(a.dbg, ctx.index, kM, k, sigma[q], cell);  // raw class, -1 for the sentinel
+            const uint4* co;
+            if constexpr (F::kIsTile) {{
+                const int4 tr = ctx.trec[k * kR + q];
+                f.a0 = ctx.cbase[k] + cell[0] * ctx.st0[k] + cell[1] * ctx.st1[k] + cell[2] + tr.w;
+                f.c0 = tr.x;
+                f.c1 = tr.y;
+                f.c2 = tr.z;
+                co = reinterpret_cast<const uint4*>(ctx.trec + kM * kR) + q * kNV;
+            }} else {{
+                const uint4 rec = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes)[max(sigma[q], 0)];
+                int rho[3], tau[3], base[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {{
+                    rho[i] = (int)((rec.x >> (13 + 2 * i)) & 3u);
+                    tau[i] = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
+                    base[i] = cell[i] + (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
+                }}
+                bind(f, a, *ctx.geom, k, base, rho, tau);
+                co = kAff + q * kNV;
+            }}
+            total += kernel_aff<T>(xq[0], xq[1], xq[2], co, f);
+        }}
+        return total;
+    }}
+}};
+"""
+
+
 def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple:
     """(translation-unit source, stats) for one plan; `stem` names the catalog entry."""
     if not codegen_supported(plan):
@@ -244,11 +477,18 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
     words = canonical_words(pack_plan(plan))
     kfuncs = []
     kflops = []
-    for kidx in range(plan.K):
-        lines, fl = _kernel_function(plan, kidx, d)
+    aff = affine_tables(plan) if os.environ.get("SP_CODEGEN_AFFINE", "1") != "0" else None
+    if aff is not None:
+        lines, fl, _ = _affine_kernel_function(plan, d)
         kfuncs.extend(lines)
         kfuncs.append("")
         kflops.append(fl)
+    else:
+        for kidx in range(plan.K):
+            lines, fl = _kernel_function(plan, kidx, d)
+            kfuncs.extend(lines)
+            kfuncs.append("")
+            kflops.append(fl)
     sig_bytes = ((plan.r * 4) + 15) & ~15
     # occupancy hint for ptxas: light weight programs keep 4 CTAs (<= 64 regs) per SM
     min_blocks = 4 if max(kflops) <= 64 else (2 if max(kflops) <= 700 else 1)
@@ -269,9 +509,94 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
             f"                case {k}: acc = kernel{k}<T>(y0, y1, y2, f); break;" for k in range(plan.K)
         )
         dispatch = f"            T acc = T(0);\n            switch (kern) {{\n{cases}\n            }}"
+    if aff is not None:
+        eval_src = _affine_eval_source(plan, aff[0], aff[1], min_blocks)
+    else:
+        eval_src = f"""template <typename T>
+struct Eval {{
+    static constexpr int kMinBlocks = {min_blocks};
+    static constexpr int kTrecBytes = kM * kN * 16;
+    template <typename U>
+    static constexpr int vec_width() {{
+        return 0;
+    }}
+    // per-(coset, class) shared-memory address records for the staged tile:
+    // {{coef of site/d component 0, 1, 2; constant offset of pib/d}} (computed per tile)
+    __device__ static void tile_records(const EvalArgs<T>& a, const TileGeom& g, const unsigned char* tables,
+                                        int4* trec, int tid) {{
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
+        for (int idx = tid; idx < kM * kN; idx += kThreads) {{
+            const int k = idx / kN, c = idx - k * kN;
+            const uint4 rec = cls_tab[c];
+            const int st[3] = {{g.ex[k][1] * g.ex[k][2], g.ex[k][2], 1}};
+            int cf[3] = {{0, 0, 0}}, z = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {{
+                const int rho = (int)((rec.x >> (13 + 2 * i)) & 3u);
+                const int tau = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
+                const int pb = (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
+                cf[rho] = tau * st[i];
+                z += pb * st[i];
+            }}
+            trec[idx] = make_int4(cf[0], cf[1], cf[2], z);
+        }}
+    }}
+    template <class F, class Ctx>
+    __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
+        const EvalArgs<T>& a = *ctx.a;
+        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
+        bool fast = false;
+        float frac[3] = {{0.f, 0.f, 0.f}};
+        if constexpr (sizeof(T) == 4) {{
+            const float m = fminf(fminf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
+            const float M = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
+            fast = m >= kFastLo && M < kFastHi;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) frac[i] = (float)x[i] - floorf((float)x[i]);
+        }}
+        T total = T(0);
+#pragma unroll
+        for (int k = 0; k < kM; ++k) {{
+            int cell[3];
+            T yy[3];
+            uint4 rec;
+            const int raw = fast ? classify_fast<T>(frac, ctx.X, k, sigma, cls_tab, ctx.err, cell, yy, rec)
+                                 : classify_f64<T>(x, k, sigma, cls_tab, ctx.err, cell, yy, rec);
+            write_dbg(a.dbg, ctx.index, kM, k, raw, cell);  // raw class: -1 for the sentinel
+            const int c = max(raw, 0);
+            const int kern = (int)(rec.x & 15u);
+            (void)kern;
+            const T y0 = yy[0], y1 = yy[1], y2 = yy[2];
+            if constexpr (F::kIsTile) {{
+                const int4 tr = ctx.trec[k * kN + c];
+                f.a0 = ctx.cbase[k] + cell[0] * ctx.st0[k] + cell[1] * ctx.st1[k] + cell[2] + tr.w;
+                f.c0 = tr.x;
+                f.c1 = tr.y;
+                f.c2 = tr.z;
+            }} else {{
+                int rho[3], tau[3], base[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {{
+                    rho[i] = (int)((rec.x >> (13 + 2 * i)) & 3u);
+                    tau[i] = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
+                    base[i] = cell[i] + (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
+                }}
+                bind(f, a, *ctx.geom, k, base, rho, tau);
+            }}
+{dispatch}
+            total += acc;
+        }}
+        return total;
+    }}
+}};
+
+"""
     src = f"""// GENERATED by paper_2102_08514_b200/codegen.py from plans/{stem}.plan.json — do not edit.
 // Plan: {plan.name} on {plan.lattice_name}: s=3 M={plan.M} N={plan.N} Q={plan.Q} r={plan.r} K={plan.K}
 // Weight-program flops per coset per kernel (shared monomials + FMA chains + merge): {kflops}
+#include <cuda_fp16.h>
+
 #include "../sp_launch.cuh"
 
 namespace sp {{
@@ -355,85 +680,7 @@ __device__ __forceinline__ int classify_fast(const float frac[3], const int X[3]
     return class_and_y<float, T>(xp, sigma, cls_tab, err, y, rec);
 }}
 
-template <typename T>
-struct Eval {{
-    static constexpr int kMinBlocks = {min_blocks};
-    template <typename U>
-    static constexpr int vec_width() {{
-        return 0;
-    }}
-    // per-(coset, class) shared-memory address records for the staged tile:
-    // {{coef of site/d component 0, 1, 2; constant offset of pib/d}} (computed per tile)
-    __device__ static void tile_records(const EvalArgs<T>& a, const TileGeom& g, const unsigned char* tables,
-                                        int4* trec, int tid) {{
-        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
-        for (int idx = tid; idx < kM * kN; idx += kThreads) {{
-            const int k = idx / kN, c = idx - k * kN;
-            const uint4 rec = cls_tab[c];
-            const int st[3] = {{g.ex[k][1] * g.ex[k][2], g.ex[k][2], 1}};
-            int cf[3] = {{0, 0, 0}}, z = 0;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {{
-                const int rho = (int)((rec.x >> (13 + 2 * i)) & 3u);
-                const int tau = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
-                const int pb = (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
-                cf[rho] = tau * st[i];
-                z += pb * st[i];
-            }}
-            trec[idx] = make_int4(cf[0], cf[1], cf[2], z);
-        }}
-    }}
-    template <class F, class Ctx>
-    __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
-        const EvalArgs<T>& a = *ctx.a;
-        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
-        const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
-        bool fast = false;
-        float frac[3] = {{0.f, 0.f, 0.f}};
-        if constexpr (sizeof(T) == 4) {{
-            const float m = fminf(fminf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
-            const float M = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
-            fast = m >= kFastLo && M < kFastHi;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) frac[i] = (float)x[i] - floorf((float)x[i]);
-        }}
-        T total = T(0);
-#pragma unroll
-        for (int k = 0; k < kM; ++k) {{
-            int cell[3];
-            T yy[3];
-            uint4 rec;
-            const int raw = fast ? classify_fast<T>(frac, ctx.X, k, sigma, cls_tab, ctx.err, cell, yy, rec)
-                                 : classify_f64<T>(x, k, sigma, cls_tab, ctx.err, cell, yy, rec);
-            write_dbg(a.dbg, ctx.index, kM, k, raw, cell);  // raw class: -1 for the sentinel
-            const int c = max(raw, 0);
-            const int kern = (int)(rec.x & 15u);
-            (void)kern;
-            const T y0 = yy[0], y1 = yy[1], y2 = yy[2];
-            if constexpr (F::kIsTile) {{
-                const int4 tr = ctx.trec[k * kN + c];
-                f.a0 = ctx.cbase[k] + cell[0] * ctx.st0[k] + cell[1] * ctx.st1[k] + cell[2] + tr.w;
-                f.c0 = tr.x;
-                f.c1 = tr.y;
-                f.c2 = tr.z;
-            }} else {{
-                int rho[3], tau[3], base[3];
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {{
-                    rho[i] = (int)((rec.x >> (13 + 2 * i)) & 3u);
-                    tau[i] = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
-                    base[i] = cell[i] + (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
-                }}
-                bind(f, a, *ctx.geom, k, base, rho, tau);
-            }}
-{dispatch}
-            total += acc;
-        }}
-        return total;
-    }}
-}};
-
-static const uint64_t kBlob[{len(words)}] = {{
+{eval_src}static const uint64_t kBlob[{len(words)}] = {{
 {_format_words(words)}
 }};
 
@@ -452,9 +699,10 @@ extern const sp::GenEntry kGen_{ident} = {{
     &sp::launch_bricks<double, sp::gen_{ident}::Eval<double>>,
     &sp::occupancy_bricks<float, sp::gen_{ident}::Eval<float>>,
     &sp::occupancy_bricks<double, sp::gen_{ident}::Eval<double>>,
+    sp::gen_{ident}::Eval<float>::kTrecBytes,
 }};
 """
-    return src, {"ident": ident, "flops_per_coset": kflops, "words": len(words)}
+    return src, {"ident": ident, "flops_per_coset": kflops, "words": len(words), "affine": aff is not None}
 
 
 def _format_words(words: list) -> str:

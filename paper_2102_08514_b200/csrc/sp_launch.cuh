@@ -82,6 +82,7 @@ struct GenEntry {
     BrickLaunchFn<double> brick_f64;
     int (*bocc_f32)(size_t);
     int (*bocc_f64)(size_t);
+    int trec_bytes;  // per-tile address records (+ tables) in smem
 };
 
 }  // namespace sp

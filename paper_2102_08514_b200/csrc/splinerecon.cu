@@ -496,7 +496,7 @@ int build_args(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     a.err = err;
     a.tables = p->d_tables;
     a.table_bytes = p->table_bytes;
-    a.trec_bytes = p->kind == SP_KIND_GENERATED ? p->M * p->N * 16 : 0;
+    a.trec_bytes = p->kind == SP_KIND_GENERATED ? p->gen->trec_bytes : 0;
     // row-vector tile (fp32 tensor-product kernels): +vec*sizeof(T) bytes per tile element
     vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
     if (vec) {
