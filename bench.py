@@ -211,6 +211,30 @@ def bench_prefilter(args, device, rank, stream, dist, peak):
             "l2": "input and output 535 MB each > 126 MB L2"}
 
 
+def bench_render(args, device):
+    """the ray-marcher consuming reconstruction (render.py,
+    SPEC.md render_volume).  Marschner-Lobb on CC 128^3 sampled for the tricubic spline,
+    512x512 orthographic view, 384 steps of 1/128: 100.7 M reconstructions per frame plus
+    compositing.  Best of a few frames after a warm-up frame (CUDA events)."""
+    import torch
+
+    from paper_2102_08514_b200 import corpus
+    from paper_2102_08514_b200.render import Camera, RenderJob, ml_volume, render_volume
+    from paper_2102_08514_b200.runtime import PlanInterpreter
+
+    plan = corpus.build_plan("cc_tricubic")
+    grid, sc, off = ml_volume(plan, 128, device=device)
+    job = RenderJob(plan=plan, volume=grid, width=512, height=512, n_steps=384, step=1.0 / 128, lattice_scale=sc,
+                    lattice_offset=off, slab=64, camera=Camera(position=(0.0, 0.0, -1.5), fov=2.2))
+    interp = PlanInterpreter(plan)
+    render_volume(job, interp)
+    ms = min(render_volume(job, interp).ms for _ in range(3))
+    samples = job.width * job.height * job.n_steps
+    return {"workload": "Marschner-Lobb (f_M=6, alpha=0.25) on CC 128^3, cc_tricubic, 512x512, 384 steps, fp32",
+            "ms_per_frame": ms, "value": samples / (ms * 1e-3) / 1e9, "unit": "Gsamples/s (reconstruct + composite)",
+            "samples_per_frame": samples}
+
+
 def measure(fn, steps, warmup, stream, dist=None):
     import torch
 
@@ -536,6 +560,7 @@ def run_ours(args):
             torch.cuda.empty_cache()
         line["workloads"] = others
         line["prefilter"] = bench_prefilter(args, device, rank, stream, dist, peak)
+        line["render"] = bench_render(args, device)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(name, args.cpu_seconds)
