@@ -84,12 +84,9 @@ def sample_grid(cosets, target: Target, h: float, box: float, margin: int, *, de
 def spline_center(plan) -> tuple:
     """Centroid of the (non-centred) box spline = half the sum of its
     direction vectors: sum_m c_m phi(y - m) with c_m = f(h m) approximates f(h (y - centre))."""
-    from .corpus import DIRECTION_SETS
+    from .corpus import direction_set
 
-    name = plan.name.replace("_ungrouped", "")
-    if name not in DIRECTION_SETS:
-        raise KeyError(f"no direction set for {plan.name}")
-    cols = DIRECTION_SETS[name][0]
+    cols = direction_set(plan.name.replace("_ungrouped", ""))[0]
     return tuple(sum(c[i] for c in cols) / 2.0 for i in range(len(cols[0])))
 
 

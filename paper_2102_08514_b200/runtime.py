@@ -239,7 +239,8 @@ class PlanInterpreter:
                     f"GPU evaluation is implemented for s == 3 plans (plan {self.plan.name!r} has s={self.plan.s})"
                 )
             lib = _native.lib()
-            tp = -2 if self._kernel == "generic" else (-1 if self._tp is None else self._tp)
+            # separable kernels exist for degrees 1-3; other tensor degrees take the generic kernel
+            tp = -2 if self._kernel == "generic" else (self._tp if self._tp in (1, 2, 3) else -1)
             desc, keep = _native.make_plan_desc(pack_plan(self.plan), tp)
             out = ctypes.c_void_p()
             with torch.cuda.device(key):
