@@ -22,6 +22,7 @@ relative; fp32 grids to ~1e-7 of max|f|.
 from __future__ import annotations
 
 import ctypes
+import itertools
 import math
 from typing import Callable, Sequence
 
@@ -148,6 +149,30 @@ class CoefficientGrid:
             else:
                 idx.append(_mirror_index(v, n))
         return float(arr[tuple(idx)])
+
+    def fetch_nearest(self, coset: int, z: Sequence[float]) -> float:
+        """runtime.py:125-128: the slot nearest to coset-grid coordinate z (Python's
+        round, half to even), policy-aware."""
+        origin = self.origins[coset]
+        return self._read_scalar(coset, tuple(int(round(v)) - o for v, o in zip(z, origin)))
+
+    def fetch_linear(self, coset: int, u: Sequence[float], offset_half: bool = False) -> float:
+        """runtime.py:130-147: multilinear interpolation of the 2^s slots around u (the
+        software form of a hardware linear fetch; -0.5 first when offset_half)."""
+        if offset_half:
+            u = [v - 0.5 for v in u]
+        origin = self.origins[coset]
+        base = [math.floor(v) for v in u]
+        frac = [v - b for v, b in zip(u, base)]
+        total = 0.0
+        for corner in itertools.product((0, 1), repeat=len(u)):
+            w = 1.0
+            for f, c in zip(frac, corner):
+                w *= f if c else (1.0 - f)
+            if w == 0.0:
+                continue
+            total += w * self._read_scalar(coset, tuple(b + c - o for b, c, o in zip(base, corner, origin)))
+        return total
 
     def descriptor(self) -> _native.GridDesc:
         """sp_grid_desc of this grid (memoised on the arrays' storage, shapes and policy:

@@ -150,3 +150,34 @@ def test_grid_extents_match_reference_rule():
     c = decompose_cartesian(named_lattice("FCC"))
     origins, shapes = grid_extents(c, [0, 0, 0], [321, 321, 321])
     assert sum(int(np.prod(s)) for s in shapes) == 16_693_124
+
+
+@pytest.mark.parametrize("boundary", ["zero", "clamp", "mirror"])
+def test_scalar_fetches_match_oracle(boundary):
+    """CoefficientGrid.fetch_nearest / fetch_linear (runtime.py:125-147) against the oracle's
+    batch fetches (runtime.py:170-188) on a BCC grid, in and outside storage."""
+    import numpy as np
+    import torch
+
+    from oracle.plan_numpy import NumpyGrid
+    from paper_2102_08514_b200.lattice import decompose_cartesian, named_lattice
+    from paper_2102_08514_b200.runtime import CoefficientGrid
+
+    cos = decompose_cartesian(named_lattice("BCC"))
+    grid = CoefficientGrid.zeros(cos, [-3, -2, -1], [6, 5, 7], boundary=boundary, device="cpu",
+                                 dtype=torch.float64)
+    rng = np.random.default_rng(4)
+    for a in grid.arrays:
+        a.copy_(torch.from_numpy(rng.random(tuple(a.shape))))
+    ng = NumpyGrid(cos.diag, cos.shifts, [a.numpy() for a in grid.arrays], grid.origins, boundary)
+    z = rng.uniform(-6, 9, size=(200, 3))
+    z[:20] = np.round(z[:20]) + 0.5  # half-way ties: round half to even
+    for k in range(cos.M):
+        want_n = ng.fetch_nearest_batch(k, z)
+        want_l = ng.fetch_linear_batch(k, z)
+        got_n = [grid.fetch_nearest(k, tuple(p)) for p in z]
+        got_l = [grid.fetch_linear(k, tuple(p)) for p in z]
+        np.testing.assert_array_equal(got_n, want_n)
+        np.testing.assert_allclose(got_l, want_l, rtol=1e-14, atol=1e-15)
+        half = [grid.fetch_linear(k, tuple(p + 0.5), offset_half=True) for p in z]
+        np.testing.assert_allclose(half, want_l, rtol=1e-13, atol=1e-14)
