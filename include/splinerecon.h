@@ -212,6 +212,33 @@ typedef struct sp_stencil_desc {
 } sp_stencil_desc;
 int sp_prefilter(const sp_grid_desc* in, const sp_stencil_desc* stencil, void* const* out, void* stream);
 
+/*
+ * Ray-marcher around the reconstruction (SPEC.md render_volume, which
+ * the reference describes but does not ship).  A frame = per slab of steps:
+ *   sp_ray_points -> sp_eval (the slab's points) -> sp_composite.
+ * sp_ray_points writes the lattice coordinates of steps [k0, k1) of every pixel's ray,
+ * pixel-major (row-major pixels, steps of one ray contiguous), float32 [(w*h*(k1-k0))][3]:
+ * orthographic rays from position + v*span_y*up + u*fov*right along forward, sample t =
+ * (k + 0.5)*step, lattice = world*lattice_scale + lattice_offset, computed in float64.
+ * sp_composite folds one slab of values [npix][nsteps] (float32 or float64 device array) into
+ * the per-pixel state [npix][4] = (r, g, b, transmittance) in float64 (initialise to
+ * (0, 0, 0, 1)): front to back, colour += T * alpha * rgb, T *= 1 - alpha, with (rgb, alpha)
+ * piecewise linear in the value over the transfer function's control points (clamped).
+ */
+#define SP_MAX_TRANSFER 16
+typedef struct sp_camera {
+    double position[3], right[3], up[3], forward[3];
+    double fov, step, lattice_scale, lattice_offset[3];
+} sp_camera;
+typedef struct sp_transfer {
+    int32_t n;                              /* control points, 2..SP_MAX_TRANSFER, increasing value */
+    double points[5 * SP_MAX_TRANSFER];     /* (value, r, g, b, alpha) per control point           */
+} sp_transfer;
+int sp_ray_points(const sp_camera* cam, int32_t width, int32_t height, int32_t k0, int32_t k1, float* out,
+                  void* stream);
+int sp_composite(const void* values, int32_t dtype, int64_t npix, int32_t nsteps, const sp_transfer* tf, double* state,
+                 void* stream);
+
 /* Staging statistics for tuning (not thread-safe): copies the counters accumulated since the
  * last call into out[4] = {staged chunks, unstaged chunks, staged tile elements, 0} (when
  * out != NULL), then enables (1, counters reset) or disables (0) collection. */

@@ -95,6 +95,21 @@ class StencilDesc(ctypes.Structure):
     ]
 
 
+SP_MAX_TRANSFER = 16
+
+
+class Camera(ctypes.Structure):
+    """sp_camera (splinerecon.h)."""
+    _fields_ = [("position", ctypes.c_double * 3), ("right", ctypes.c_double * 3), ("up", ctypes.c_double * 3),
+                ("forward", ctypes.c_double * 3), ("fov", ctypes.c_double), ("step", ctypes.c_double),
+                ("lattice_scale", ctypes.c_double), ("lattice_offset", ctypes.c_double * 3)]
+
+
+class Transfer(ctypes.Structure):
+    """sp_transfer (splinerecon.h)."""
+    _fields_ = [("n", ctypes.c_int32), ("points", ctypes.c_double * (5 * SP_MAX_TRANSFER))]
+
+
 EXPORTS = {
     "sp_plan_create": (ctypes.c_int, [ctypes.POINTER(PlanDesc), ctypes.POINTER(ctypes.c_void_p)]),
     "sp_plan_destroy": (None, [ctypes.c_void_p]),
@@ -148,6 +163,14 @@ EXPORTS = {
         ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
     ),
     "sp_prefilter": (ctypes.c_int, [ctypes.POINTER(GridDesc), ctypes.POINTER(StencilDesc), ctypes.c_void_p, ctypes.c_void_p]),
+    "sp_ray_points": (
+        ctypes.c_int, [ctypes.POINTER(Camera), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                       ctypes.c_void_p, ctypes.c_void_p]
+    ),
+    "sp_composite": (
+        ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(Transfer),
+                       ctypes.c_void_p, ctypes.c_void_p]
+    ),
     "sp_last_error": (ctypes.c_char_p, []),
     "sp_version": (ctypes.c_char_p, []),
 }

@@ -62,7 +62,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     gen_tus = write_generated(_catalog_plans(), GEN)
     tus = [os.path.join(CSRC, "splinerecon.cu"), os.path.join(CSRC, "sp_texture.cu"),
-           os.path.join(CSRC, "sp_prefilter.cu")] + gen_tus
+           os.path.join(CSRC, "sp_prefilter.cu"), os.path.join(CSRC, "sp_render.cu")] + gen_tus
     deps = tus + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(GEN, "registry.inc"),
                                                            os.path.join(ROOT, "include", "splinerecon.h")]
     digest = _digest(deps)

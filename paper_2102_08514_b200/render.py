@@ -9,16 +9,18 @@ site and reconstructed by the spline under test.
 
 Every sample of every ray is reconstructed by the same GPU kernels as the benchmark
 (`PlanInterpreter.eval_batch`), one slab of `slab` steps for all pixels at a time: the
-slab's points are laid out pixel-major with the steps of one ray contiguous, so each CTA's
-chunk of consecutive points covers a few short parallel ray segments — a compact staged
-box (the coherent access pattern of ray marching the paper's kernels target).
-Compositing is a per-slab exclusive cumulative product of transmittance on the GPU; the
-same `composite` code runs on CPU tensors, which is how the tests check a GPU render
-against one composited from the oracle's values.
+slab's points are generated on the GPU (`sp_ray_points`, csrc/sp_render.cu) pixel-major
+with the steps of one ray contiguous, so each CTA's chunk of consecutive points covers a
+few short parallel ray segments — a compact staged box (the coherent access pattern of ray
+marching the paper's kernels target) — and composited front to back on the
+GPU (`sp_composite`, float64 per-pixel state).  `ray_points` is the host definition of the
+sample points (the device kernel reproduces it bit for bit); the tests composite the
+oracle's reconstruction of the same points with oracle/render_numpy.py and compare.
 """
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 from typing import Sequence
@@ -26,6 +28,7 @@ from typing import Sequence
 import numpy as np
 import torch
 
+from . import _native
 from .convergence import sample_grid, spline_center
 from .runtime import CoefficientGrid, PlanInterpreter
 
@@ -65,17 +68,6 @@ class TransferFunction:
         vals = [p[0] for p in self.points]
         if len(self.points) < 2 or any(b <= a for a, b in zip(vals, vals[1:])):
             raise ValueError("transfer function needs >= 2 control points with increasing values")
-
-    def apply(self, v: torch.Tensor) -> tuple:
-        """(rgb (..., 3), alpha (...)) for values v."""
-        tab = torch.tensor(self.points, dtype=v.dtype, device=v.device)
-        xs = tab[:, 0].contiguous()
-        vc = v.clamp(float(xs[0]), float(xs[-1]))
-        i = torch.searchsorted(xs, vc.contiguous(), right=True).clamp(1, len(self.points) - 1)
-        x0, x1 = xs[i - 1], xs[i]
-        w = ((vc - x0) / (x1 - x0)).unsqueeze(-1)
-        out = tab[i - 1, 1:] + w * (tab[i, 1:] - tab[i - 1, 1:])
-        return out[..., :3], out[..., 3]
 
 
 @dataclass
@@ -144,24 +136,6 @@ def ray_points(job: RenderJob, k0: int, k1: int, device, dtype) -> torch.Tensor:
     return (p * job.lattice_scale + off).reshape(-1, 3).to(dtype)
 
 
-def composite(values: torch.Tensor, transfer: TransferFunction, state=None):
-    """Front-to-back compositing of one slab: values (pixels, steps).  state = (colour
-    (pixels, 3), transmittance (pixels,)); returns the updated state.  Deterministic: an
-    exclusive cumulative product along each ray, no atomics."""
-    rgb, a = transfer.apply(values.to(torch.float64))
-    npx = values.shape[0]
-    if state is None:
-        state = (torch.zeros((npx, 3), dtype=torch.float64, device=values.device),
-                 torch.ones(npx, dtype=torch.float64, device=values.device))
-    col, trans = state
-    keep = 1.0 - a
-    excl = torch.cumprod(torch.cat([torch.ones_like(keep[:, :1]), keep[:, :-1]], 1), 1)  # prod_{j<i}
-    wgt = trans[:, None] * excl * a
-    col = col + (wgt[:, :, None] * rgb).sum(1)
-    trans = trans * torch.prod(keep, 1)
-    return col, trans
-
-
 def finish(state, background: Sequence[float], height: int, width: int) -> tuple:
     col, trans = state
     bg = torch.tensor(background, dtype=torch.float64, device=col.device)
@@ -170,23 +144,64 @@ def finish(state, background: Sequence[float], height: int, width: int) -> tuple
     return rad, img.cpu().numpy()
 
 
+def _camera_desc(job: RenderJob) -> _native.Camera:
+    cam = _native.Camera()
+    R = job.camera.orientation
+    for a in range(3):
+        cam.position[a] = float(job.camera.position[a])
+        cam.right[a] = float(R[0][a])
+        cam.up[a] = float(R[1][a])
+        cam.forward[a] = float(R[2][a])
+        cam.lattice_offset[a] = float(job.lattice_offset[a])
+    cam.fov = float(job.camera.fov)
+    cam.step = float(job.step)
+    cam.lattice_scale = float(job.lattice_scale)
+    return cam
+
+
+def _transfer_desc(tf: TransferFunction) -> _native.Transfer:
+    if len(tf.points) > _native.SP_MAX_TRANSFER:
+        raise ValueError(f"at most {_native.SP_MAX_TRANSFER} transfer-function control points")
+    d = _native.Transfer()
+    d.n = len(tf.points)
+    for i, pt in enumerate(tf.points):
+        for j in range(5):
+            d.points[5 * i + j] = float(pt[j])
+    return d
+
+
 def render_volume(job: RenderJob, interp: PlanInterpreter | None = None) -> RenderResult:
-    """SPEC.md render_volume: every ray sample reconstructed on the GPU, composited front to
-    back.  Raises RuntimeError_ when the volume does not match the plan's lattice."""
+    """SPEC.md render_volume: per slab of steps, the rays' sample points (sp_ray_points),
+    their reconstruction (eval_batch, chunk kernel) and front-to-back compositing
+    (sp_composite), all on the GPU and stream-ordered; one host sync at the end."""
     interp = interp or PlanInterpreter(job.plan)
     grid = job.volume
     dev = grid.device
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    state = None
+    if dev.type != "cuda":
+        raise RuntimeError("render_volume needs the volume on a CUDA device")
+    lib = _native.lib()
+    cam, tfd = _camera_desc(job), _transfer_desc(job.transfer)
     npx = job.width * job.height
-    for k0 in range(0, job.n_steps, job.slab):
-        k1 = min(job.n_steps, k0 + job.slab)
-        pts = ray_points(job, k0, k1, dev, grid.dtype)
-        vals = interp.eval_batch(grid, pts, check=False).reshape(npx, k1 - k0)
-        state = composite(vals, job.transfer, state)
-    rad, img = finish(state, job.background, job.height, job.width)
-    e1.record()
+    slab = min(job.slab, job.n_steps)
+    pts = torch.empty((npx * slab, 3), dtype=torch.float32, device=dev)
+    vals = torch.empty(npx * slab, dtype=grid.dtype, device=dev)
+    state = torch.zeros((npx, 4), dtype=torch.float64, device=dev)
+    state[:, 3] = 1.0
+    dt = _native.SP_F32 if grid.dtype == torch.float32 else _native.SP_F64
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k0 in range(0, job.n_steps, slab):
+        k1 = min(job.n_steps, k0 + slab)
+        m = npx * (k1 - k0)
+        _native.check(lib.sp_ray_points(ctypes.byref(cam), job.width, job.height, k0, k1, pts.data_ptr(),
+                                        ctypes.c_void_p(stream.cuda_stream)))
+        p = pts[:m] if grid.dtype == torch.float32 else pts[:m].to(grid.dtype)
+        interp.eval_batch(grid, p, out=vals[:m], check=False, stream=stream)
+        _native.check(lib.sp_composite(vals.data_ptr(), dt, npx, k1 - k0, ctypes.byref(tfd), state.data_ptr(),
+                                       ctypes.c_void_p(stream.cuda_stream)))
+    rad, img = finish((state[:, :3], state[:, 3]), job.background, job.height, job.width)
+    e1.record(stream)
     torch.cuda.synchronize(dev)
     return RenderResult(image=img, radiance=rad, samples=npx * job.n_steps, ms=e0.elapsed_time(e1))
 

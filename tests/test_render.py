@@ -9,35 +9,28 @@ import pytest
 import torch
 
 from paper_2102_08514_b200 import corpus
-from paper_2102_08514_b200.render import (Camera, RenderJob, TransferFunction, composite, finish, marschner_lobb,
-                                          ml_volume, ray_points, read_ppm, render_volume, write_ppm)
+from oracle.render_numpy import composite, finish, transfer
+from paper_2102_08514_b200.render import (Camera, RenderJob, TransferFunction, marschner_lobb, ml_volume, ray_points,
+                                          read_ppm, render_volume, write_ppm)
 
 
 def test_transfer_function_is_piecewise_linear_and_clamped():
     tf = TransferFunction(((0.0, 0, 0, 0, 0.0), (1.0, 1, 0.5, 0, 1.0)))
-    rgb, a = tf.apply(torch.tensor([-1.0, 0.0, 0.25, 1.0, 3.0], dtype=torch.float64))
+    rgb, a = transfer(tf.points, np.array([-1.0, 0.0, 0.25, 1.0, 3.0]))
     assert a.tolist() == [0.0, 0.0, 0.25, 1.0, 1.0]
     assert rgb[2].tolist() == [0.25, 0.125, 0.0]
     with pytest.raises(ValueError):
         TransferFunction(((0.0, 0, 0, 0, 0), (0.0, 1, 1, 1, 1)))
 
 
-def test_composite_matches_sequential_front_to_back():
+def test_composite_slabs_compose():
     rng = np.random.default_rng(1)
-    vals = torch.from_numpy(rng.random((7, 23)))
+    vals = rng.random((7, 23))
     tf = TransferFunction()
-    # two slabs vs one pass vs the textbook loop
-    s = composite(vals[:, 10:], tf, composite(vals[:, :10], tf))
-    whole = composite(vals, tf)
-    rgb, a = tf.apply(vals)
-    col = torch.zeros((7, 3), dtype=torch.float64)
-    trans = torch.ones(7, dtype=torch.float64)
-    for i in range(vals.shape[1]):
-        col += (trans * a[:, i])[:, None] * rgb[:, i]
-        trans = trans * (1 - a[:, i])
-    for got in (s, whole):
-        torch.testing.assert_close(got[0], col, rtol=1e-12, atol=1e-14)
-        torch.testing.assert_close(got[1], trans, rtol=1e-12, atol=1e-14)
+    s = composite(vals[:, 10:], tf.points, composite(vals[:, :10], tf.points))
+    whole = composite(vals, tf.points)
+    np.testing.assert_allclose(s[0], whole[0], rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(s[1], whole[1], rtol=1e-13, atol=1e-15)
 
 
 def test_ray_points_geometry():
@@ -112,9 +105,29 @@ def test_render_matches_oracle_composite(name, cuda):
     for k0 in range(0, job.n_steps, job.slab):
         k1 = min(job.n_steps, k0 + job.slab)
         pts = ray_points(job, k0, k1, "cpu", torch.float32).double().numpy()
-        vals = torch.from_numpy(oracle_eval(plan, ngrid, pts, tables)).reshape(npx, k1 - k0)
-        state = composite(vals, job.transfer, state)
+        vals = oracle_eval(plan, ngrid, pts, tables).reshape(npx, k1 - k0)
+        state = composite(vals, job.transfer.points, state)
     rad, img = finish(state, job.background, job.height, job.width)
     assert float(rad.max()) > 0.05  # the transfer function picks up the ML structure
-    torch.testing.assert_close(res.radiance.cpu(), rad, rtol=0, atol=2e-4)
+    np.testing.assert_allclose(res.radiance.cpu().numpy(), rad, rtol=0, atol=2e-4)
     assert int(np.abs(res.image.astype(int) - img.astype(int)).max()) <= 1
+
+
+@pytest.mark.gpu
+def test_device_ray_points_equal_host_definition(cuda):
+    import ctypes
+
+    from paper_2102_08514_b200 import _native
+    from paper_2102_08514_b200.render import _camera_desc
+
+    plan = corpus.build_plan("bcc_linear_rd")
+    job = RenderJob(plan=plan, volume=None, width=37, height=23, n_steps=50, step=0.037, lattice_scale=13.7,
+                    lattice_offset=(1.0, 1.0, 1.0),
+                    camera=Camera(position=(0.3, -0.2, -1.7), fov=2.3,
+                                  orientation=((0.8, 0.6, 0.0), (-0.36, 0.48, 0.8), (0.48, -0.64, 0.6))))
+    want = ray_points(job, 11, 50, "cpu", torch.float32)
+    got = torch.empty_like(want, device=cuda)
+    _native.check(_native.lib().sp_ray_points(ctypes.byref(_camera_desc(job)), job.width, job.height, 11, 50,
+                                              got.data_ptr(), None))
+    torch.cuda.synchronize()
+    assert torch.equal(got.cpu(), want)
