@@ -156,6 +156,24 @@ int sp_eval_bricks_dev(const sp_plan* plan, const sp_grid_desc* grid, const void
                        const int64_t* brick_start, const int32_t* n_bricks_dev, int32_t n_bricks_cap,
                        int32_t log2_brick, const int64_t* out_index, void* out, int32_t* err_flag, void* stream);
 
+/* Input-order protocol B (arbitrary point order) without a host round trip.
+ * sp_sort_points: 30-bit Morton keys of the points' unit cells relative to (lo0, lo1, lo2)
+ * with `bits` (<= 10) per axis — cells outside [lo, lo + 2^bits) are clamped, which only
+ * affects the order (any brick partition is evaluated correctly) — a radix sort of (key,
+ * index) pairs, the points gathered into key order (sorted_pts, same dtype/shape as pts),
+ * the int32 permutation (perm[i] = caller index of sorted point i) and the brick runs
+ * (brick_start [n+1], brick count in device memory), all stream-ordered; n < 2^31.
+ * temp: device scratch of sp_sort_points_temp_bytes(n) bytes (NULL: stream-ordered alloc).
+ * sp_eval_bricks_perm32: sp_eval_bricks_dev writing point i's value to out[perm[i]] — the
+ * results come back in the caller's order. */
+int64_t sp_sort_points_temp_bytes(int64_t n);
+int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t lo0, int32_t lo1, int32_t lo2, int32_t bits,
+                   int32_t log2_brick, void* sorted_pts, int32_t* perm, int64_t* brick_start, int32_t* n_bricks,
+                   void* temp, int64_t temp_bytes, void* stream);
+int sp_eval_bricks_perm32(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+                          const int64_t* brick_start, const int32_t* n_bricks_dev, int32_t n_bricks_cap,
+                          int32_t log2_brick, const int32_t* perm, void* out, int32_t* err_flag, void* stream);
+
 /* Synchronous convenience: sp_eval + stream sync + sentinel check (SP_ERR_SENTINEL). */
 int sp_eval_sync(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
                  void* out, void* stream);

@@ -171,6 +171,19 @@ EXPORTS = {
         ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(Transfer),
                        ctypes.c_void_p, ctypes.c_void_p]
     ),
+    "sp_sort_points_temp_bytes": (ctypes.c_int64, [ctypes.c_int64]),
+    "sp_sort_points": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+         ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
+    ),
+    "sp_eval_bricks_perm32": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.POINTER(GridDesc), ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p],
+    ),
     "sp_last_error": (ctypes.c_char_p, []),
     "sp_version": (ctypes.c_char_p, []),
 }

@@ -62,6 +62,7 @@ struct EvalArgs {
     int margin;         // extra halo cells (1 for float64 points on shifted cosets, else 0)
     unsigned long long* stats;  // nullable: [0] staged chunks, [1] unstaged chunks, [2] staged elements
     const long long* out_index; // nullable: value of point i goes to out[out_index[i]]
+    const int* out_index32;     // nullable: same with int32 indices (sp_sort_points' permutation)
     int trec_bytes;             // per-(coset, class) tile records (generated kernels), in smem
     int vec_cap;                // row-vector tile capacity in elements (0: no row-vector tile)
     const int* nbricks_dev;     // nullable: brick count in device memory (sync-free brick runs)
@@ -568,6 +569,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
 template <typename T>
 __device__ __forceinline__ void store_out(const EvalArgs<T>& a, long long j, T v) {
     if (a.out_index) a.out[a.out_index[j]] = v;
+    else if (a.out_index32) a.out[a.out_index32[j]] = v;
     else a.out[j] = v;
 }
 
@@ -688,8 +690,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
                 GlobalFetch<T> f;
                 v = Ev::template eval<GlobalFetch<T>>(x, f, ctx);
             }
-            if (a.out_index) a.out[a.out_index[j]] = v;
-            else a.out[j] = v;
+            store_out(a, j, v);
         }
         if (ctx.err && a.err) atomicOr(a.err, 1);
         __syncthreads();

@@ -10,6 +10,7 @@
 //   * the generic table-driven kernel.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -750,12 +751,13 @@ int try_bricks_tma(const sp_plan* p, const sp_grid_desc* g, const sp::EvalArgs<f
 template <typename T>
 int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, const int64_t* bstart,
                       int32_t nbricks, int32_t log2b, const int64_t* out_index, void* out, int32_t* err,
-                      cudaStream_t st, const int32_t* nbricks_dev = nullptr) {
+                      cudaStream_t st, const int32_t* nbricks_dev = nullptr, const int32_t* out_index32 = nullptr) {
     sp::EvalArgs<T> a;
     int vec = 0;
     int rc = build_args<T>(p, g, pts, n, out, nullptr, err, a, vec);
     if (rc != SP_OK) return rc;
     a.out_index = reinterpret_cast<const long long*>(out_index);
+    a.out_index32 = out_index32;
     a.nbricks_dev = nbricks_dev;
     if constexpr (sizeof(T) == 4) {
         const int t = try_bricks_tma(p, g, a, bstart, nbricks, log2b, st);
@@ -947,6 +949,22 @@ __global__ void gather_points_kernel(const T* __restrict__ pts, const int64_t* _
     }
 }
 
+__global__ void iota32_kernel(int* __restrict__ v, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        v[i] = (int)i;
+}
+
+template <typename T>
+__global__ void gather_points32_kernel(const T* __restrict__ pts, const int* __restrict__ perm, long long n,
+                                       T* __restrict__ dst) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long j = perm[i];
+        dst[3 * i] = pts[3 * j];
+        dst[3 * i + 1] = pts[3 * j + 1];
+        dst[3 * i + 2] = pts[3 * j + 2];
+    }
+}
+
 int grid_for(int64_t n) {
     long long b = (n + 255) / 256;
     return (int)std::max<long long>(1, std::min<long long>(b, 148ll * 16));
@@ -1004,6 +1022,117 @@ extern "C" int sp_brick_runs(const uint64_t* keys, int64_t n, int32_t log2_brick
     brick_runs_tail<<<1, 1, 0, st>>>(n, n_bricks, brick_start);
     SP_CUDA(cudaGetLastError());
     return SP_OK;
+}
+
+// 32-bit brick heads for sp_sort_points
+struct BrickHead32 {
+    const int32_t* keys;
+    int shift;
+    __host__ __device__ bool operator()(long long i) const {
+        return i == 0 || (keys[i] >> shift) != (keys[i - 1] >> shift);
+    }
+};
+
+namespace {
+// sp_sort_points scratch layout: keys_in | keys_out | iota | CUB scratch (sort or select)
+size_t sort_points_cub_bytes(int64_t n, int end_bit) {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                    static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr), (int)n, 0,
+                                    end_bit);
+    thrust::counting_iterator<long long> idx(0);
+    const BrickHead32 head{nullptr, 0};
+    cub::DeviceSelect::If(nullptr, b, idx, static_cast<int64_t*>(nullptr), static_cast<int32_t*>(nullptr), (int)n, head);
+    return std::max(a, b);
+}
+size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+}  // namespace
+
+extern "C" int64_t sp_sort_points_temp_bytes(int64_t n) {
+    if (n <= 0 || n >= (1ll << 31)) return 0;
+    return (int64_t)(3 * align256((size_t)n * 4) + sort_points_cub_bytes(n, 30));
+}
+
+// Protocol B in one sync-free call: 30-bit Morton keys of the points' unit cells relative to
+// (lo0, lo1, lo2), `bits` per axis (cells clamped into [0, 2^bits) — clamping only reorders,
+// any brick partition is correct), CUB radix sort of (key, index) pairs over the 3*bits key
+// bits, gather of the points into key order, and the brick runs of the sorted keys
+// (brick_start [n+1], count in device memory) — no host round trip.
+extern "C" int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t lo0, int32_t lo1, int32_t lo2,
+                              int32_t bits, int32_t log2_brick, void* sorted_pts, int32_t* perm, int64_t* brick_start,
+                              int32_t* n_bricks, void* temp, int64_t temp_bytes, void* stream) {
+    if (n < 0 || n >= (1ll << 31)) return fail(SP_ERR_INVALID, "sort points: n out of range");
+    if (bits < 0 || bits > 10) return fail(SP_ERR_INVALID, "bits must be in [0, 10]");
+    if (log2_brick < 0 || log2_brick > bits) return fail(SP_ERR_INVALID, "log2_brick out of range");
+    if (dtype != SP_F32 && dtype != SP_F64) return fail(SP_ERR_INVALID, "unknown dtype");
+    if (!brick_start || !n_bricks || (n > 0 && (!pts || !sorted_pts || !perm)))
+        return fail(SP_ERR_INVALID, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        SP_CUDA(cudaMemsetAsync(n_bricks, 0, sizeof(int32_t), st));
+        SP_CUDA(cudaMemsetAsync(brick_start, 0, sizeof(int64_t), st));
+        return SP_OK;
+    }
+    const int end_bit = 3 * bits;
+    const size_t seg = align256((size_t)n * 4);
+    const size_t cub_bytes = sort_points_cub_bytes(n, end_bit);
+    const size_t need = 3 * seg + cub_bytes;
+    void* tmp = temp;
+    if (!tmp || (size_t)temp_bytes < need) {
+        tmp = nullptr;
+        SP_CUDA(cudaMallocAsync(&tmp, need, st));
+    }
+    unsigned char* base = static_cast<unsigned char*>(tmp);
+    int32_t* k_in = reinterpret_cast<int32_t*>(base);
+    int32_t* k_out = reinterpret_cast<int32_t*>(base + seg);
+    int32_t* iota = reinterpret_cast<int32_t*>(base + 2 * seg);
+    void* cub_tmp = base + 3 * seg;
+    cudaError_t e = cudaSuccess;
+    if (dtype == SP_F32)
+        morton32_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, n, lo0, lo1, lo2, bits, k_in);
+    else
+        morton32_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, n, lo0, lo1, lo2, bits, k_in);
+    iota32_kernel<<<grid_for(n), 256, 0, st>>>(iota, n);
+    size_t cb = cub_bytes;
+    if (e == cudaSuccess) e = cub::DeviceRadixSort::SortPairs(cub_tmp, cb, k_in, k_out, iota, perm, (int)n, 0, end_bit, st);
+    if (e == cudaSuccess) {
+        if (dtype == SP_F32)
+            gather_points32_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, perm, n, (float*)sorted_pts);
+        else
+            gather_points32_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, perm, n, (double*)sorted_pts);
+        thrust::counting_iterator<long long> idx(0);
+        const BrickHead32 head{k_out, 3 * log2_brick};
+        cb = cub_bytes;
+        e = cub::DeviceSelect::If(cub_tmp, cb, idx, brick_start, n_bricks, (int)n, head, st);
+    }
+    if (e == cudaSuccess) {
+        brick_runs_tail<<<1, 1, 0, st>>>(n, n_bricks, brick_start);
+        e = cudaGetLastError();
+    }
+    if (tmp != temp) cudaFreeAsync(tmp, st);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "sort points: %s", cudaGetErrorString(e));
+    return SP_OK;
+}
+
+extern "C" int sp_eval_bricks_perm32(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n,
+                                     int32_t dtype, const int64_t* brick_start, const int32_t* n_bricks_dev,
+                                     int32_t n_bricks_cap, int32_t log2_brick, const int32_t* perm, void* out,
+                                     int32_t* err_flag, void* stream) {
+    if (!plan) return fail(SP_ERR_INVALID, "null plan");
+    int rc = check_grid(plan, grid, dtype);
+    if (rc != SP_OK) return rc;
+    if (n < 0 || n_bricks_cap < 0) return fail(SP_ERR_INVALID, "negative size");
+    if (n == 0 || n_bricks_cap == 0) return SP_OK;
+    if (log2_brick < 0 || log2_brick > 20) return fail(SP_ERR_INVALID, "log2_brick out of range");
+    if (!pts || !out || !brick_start || !n_bricks_dev || !perm) return fail(SP_ERR_INVALID, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32)
+        return eval_bricks_typed<float>(plan, grid, pts, n, brick_start, n_bricks_cap, log2_brick, nullptr, out,
+                                        err_flag, st, n_bricks_dev, perm);
+    if (dtype == SP_F64)
+        return eval_bricks_typed<double>(plan, grid, pts, n, brick_start, n_bricks_cap, log2_brick, nullptr, out,
+                                         err_flag, st, n_bricks_dev, perm);
+    return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
 }
 
 extern "C" int sp_morton_keys(const void* pts, int64_t n, int32_t dtype, uint64_t* keys, void* stream) {

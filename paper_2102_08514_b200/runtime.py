@@ -489,6 +489,33 @@ class PlanInterpreter:
             raise RuntimeError_("sigma sentinel hit in batch evaluation")
         return res
 
+    def _eval_sorted32(self, grid, p, res, b, frame, st, err):
+        """Protocol B without host round trips: sp_sort_points (30-bit Morton keys in the
+        grid's frame, CUB pair sort, gather, brick runs) then sp_eval_bricks_perm32 (results
+        scattered back to the caller's order by the brick kernel)."""
+        lib = _native.lib()
+        dev = grid.device
+        n = p.shape[0]
+        dtype = _native.SP_F32 if grid.dtype == torch.float32 else _native.SP_F64
+        (lo0, lo1, lo2), bits = frame
+        key = (dev.index, n, grid.dtype)
+        ws = self._sort_ws.get(key) if hasattr(self, "_sort_ws") else None
+        if ws is None:
+            ws = (torch.empty_like(p), torch.empty(n, dtype=torch.int32, device=dev),
+                  torch.empty(n + 1, dtype=torch.int64, device=dev), torch.empty(1, dtype=torch.int32, device=dev),
+                  torch.empty(max(1, int(lib.sp_sort_points_temp_bytes(n))), dtype=torch.uint8, device=dev))
+            self._sort_ws = {key: ws}  # one cached workspace (the last batch shape)
+        sp_, perm, start, count, tmp = ws
+        h = self._handle(dev)
+        gdesc = grid.descriptor()
+        with torch.cuda.stream(st):
+            _native.check(lib.sp_sort_points(p.data_ptr(), n, dtype, lo0, lo1, lo2, bits, b, sp_.data_ptr(),
+                                             perm.data_ptr(), start.data_ptr(), count.data_ptr(), tmp.data_ptr(),
+                                             tmp.numel(), st.cuda_stream))
+            _native.check(lib.sp_eval_bricks_perm32(h, ctypes.byref(gdesc), sp_.data_ptr(), n, dtype, start.data_ptr(),
+                                                    count.data_ptr(), n, b, perm.data_ptr(), res.data_ptr(),
+                                                    None if err is None else err.data_ptr(), st.cuda_stream))
+
     def eval_batch_texture(self, grid: CoefficientGrid, pts: torch.Tensor, *, out: torch.Tensor | None = None,
                            stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         """Hardware-texture-filtered variant (sp_eval_texture): the paper's GPU fetch path with
@@ -547,6 +574,13 @@ class PlanInterpreter:
             err = torch.zeros(1, dtype=torch.int32, device=grid.device)
         n = p.shape[0]
         b = self.brick_log2(grid) if (order != "given" and dbg is None) else -1
+        if b >= 0 and order == "sort" and not sync_free:
+            frame = _sort_frame(grid, b)
+            if frame is not None and 0 < n < (1 << 31):
+                self._eval_sorted32(grid, p, res, b, frame, st, err)
+                if check and int(err.item()):
+                    raise RuntimeError_("sigma sentinel hit in batch evaluation")
+                return
         if b >= 0:
             if sync_free:
                 batch = prepare_points_async(p, b, presorted=(order == "morton"), stream=st, scratch=scratch)
@@ -570,6 +604,21 @@ class PlanInterpreter:
                                           None if err is None else err.data_ptr(), st.cuda_stream))
         if check and int(err.item()):
             raise RuntimeError_("sigma sentinel hit in batch evaluation")
+
+
+def _sort_frame(grid: CoefficientGrid, log2_brick: int):
+    """(lo (3 ints, brick-aligned), bits) of a 30-bit Morton frame covering the grid's unit
+    cells plus a margin of 8 cells, or None when the grid needs more than 2^10 cells per axis
+    (protocol B then sorts 64-bit keys).  Host-only (grid metadata): no device sync."""
+    diag, shifts = grid.cosets.diag, grid.cosets.shifts
+    lo, hi = [], []
+    for i in range(3):
+        a = min(diag[i] * grid.origins[k][i] + shifts[k][i] for k in range(len(shifts)))
+        z = max(diag[i] * (grid.origins[k][i] + grid.arrays[k].shape[i] - 1) + shifts[k][i] for k in range(len(shifts)))
+        lo.append(((a - 8) >> log2_brick) << log2_brick)
+        hi.append(z + 8)
+    bits = max(log2_brick, max(h - l for h, l in zip(hi, lo)).bit_length())
+    return (tuple(lo), bits) if bits <= 10 else None
 
 
 def eval_plan(interp: PlanInterpreter, grid: CoefficientGrid, x: Sequence) -> float:

@@ -325,3 +325,42 @@ def test_sync_free_brick_runs_match(name, presorted, cuda):
                                equal_nan=True)
     empty = prepare_points_async(pts[:0], b, presorted=True)
     assert empty.n_bricks == 0 and interp.eval_batch(grid, empty).numel() == 0
+
+
+@pytest.mark.parametrize("name,dtype", [("cc_tricubic", torch.float32), ("bcc_quintic_rd", torch.float32),
+                                        ("fcc_cubic", torch.float64), ("bcc_linear_rd", torch.float32)])
+def test_sorted32_protocol_b_matches_given_order(name, dtype, cuda):
+    """order='sort' (sp_sort_points: 30-bit keys in the grid frame, CUB pair sort, gather,
+    device brick runs; sp_eval_bricks_perm32 scatters back) is bit-identical to the chunk
+    kernel on shuffled points, including points outside the grid (clamped keys) and NaN;
+    a grid wider than 2^10 cells falls back to the 64-bit-key path."""
+    from paper_2102_08514_b200.runtime import _sort_frame
+
+    g, plan, grid = _setup(name, "mirror", dtype, cuda)
+    interp = PlanInterpreter(plan)
+    rng = np.random.default_rng(17)
+    hi = max(a.shape[0] for a in grid.arrays) * plan.diag[0]
+    pts = rng.uniform(-3, hi + 3, size=(200_000, 3))
+    pts[:50] = rng.uniform(-1e4, 1e4, size=(50, 3))
+    pts[50:60, 2] = np.nan
+    rng.shuffle(pts)
+    p = torch.from_numpy(pts).to(cuda, dtype)
+    assert _sort_frame(grid, interp.brick_log2(grid)) is not None
+    want = interp.eval_batch(grid, p)
+    got = interp.eval_batch(grid, p, order="sort")
+    torch.testing.assert_close(got, want, rtol=0, atol=0, equal_nan=True)
+    got2 = interp.eval_batch(grid, p[:1000], order="sort")  # workspace for another size
+    torch.testing.assert_close(got2, want[:1000], rtol=0, atol=0, equal_nan=True)
+
+
+def test_sort_frame_falls_back_for_wide_grids(cuda):
+    from paper_2102_08514_b200.runtime import _sort_frame
+
+    plan = corpus.build_plan("cc_trilinear")
+    _, cos = corpus.lattice_of("cc_trilinear")
+    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [1999, 3, 3], device=cuda)
+    grid.arrays[0].copy_(torch.rand(grid.arrays[0].shape, device=cuda))
+    assert _sort_frame(grid, 3) is None
+    interp = PlanInterpreter(plan)
+    p = torch.rand((5000, 3), device=cuda) * torch.tensor([2000.0, 4.0, 4.0], device=cuda)
+    torch.testing.assert_close(interp.eval_batch(grid, p, order="sort"), interp.eval_batch(grid, p), rtol=0, atol=0)
