@@ -364,3 +364,23 @@ def test_sort_frame_falls_back_for_wide_grids(cuda):
     interp = PlanInterpreter(plan)
     p = torch.rand((5000, 3), device=cuda) * torch.tensor([2000.0, 4.0, 4.0], device=cuda)
     torch.testing.assert_close(interp.eval_batch(grid, p, order="sort"), interp.eval_batch(grid, p), rtol=0, atol=0)
+
+
+def test_auto_order_routes_and_matches(cuda):
+    """Default eval_batch (order="auto") on large iid / Morton-sorted / coherent batches gives
+    the chunk kernel's values bit for bit, whichever path it picks."""
+    from paper_2102_08514_b200.runtime import choose_order
+
+    g, plan, grid = _setup("cc_tricubic", "zero", torch.float32, cuda)
+    interp = PlanInterpreter(plan)
+    hi = grid.arrays[0].shape[0]
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    iid = torch.rand((1 << 20, 3), generator=gen, device=cuda) * hi
+    srt = interp.prepare(grid, iid).pts
+    for pts, want in ((iid, "sort"), (srt, "morton")):
+        assert choose_order(pts) == want
+        torch.testing.assert_close(interp.eval_batch(grid, pts), interp.eval_batch(grid, pts, order="given"),
+                                   rtol=0, atol=0)
+    host = iid.cpu().pin_memory()  # pinned host batch: the pipelined path with the chosen order
+    torch.testing.assert_close(interp.eval_batch(grid, host).to(cuda), interp.eval_batch(grid, iid, order="given"),
+                               rtol=0, atol=0)

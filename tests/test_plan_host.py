@@ -181,3 +181,25 @@ def test_scalar_fetches_match_oracle(boundary):
         np.testing.assert_allclose(got_l, want_l, rtol=1e-14, atol=1e-15)
         half = [grid.fetch_linear(k, tuple(p + 0.5), offset_half=True) for p in z]
         np.testing.assert_allclose(half, want_l, rtol=1e-13, atol=1e-14)
+
+
+def test_choose_order_heuristic():
+    """eval_batch(order="auto") routing: iid points -> sort (protocol B), Morton-sorted ->
+    morton (protocol A), raster scans / ray slabs (coherent) -> given (chunk staging)."""
+    import torch
+
+    from paper_2102_08514_b200.runtime import _morton64, choose_order
+
+    rng = np.random.default_rng(0)
+    iid = torch.from_numpy(rng.uniform(0, 200, (300_000, 3)))
+    assert choose_order(iid) == "sort"
+    keys = _morton64(np.floor(iid.numpy()).astype(np.int64))
+    assert choose_order(iid[torch.from_numpy(np.argsort(keys, kind="stable"))]) == "morton"
+    g = torch.arange(64, dtype=torch.float64)
+    raster = torch.stack(torch.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3) + 0.5
+    assert choose_order(raster) in ("given", "morton")
+    rays = (torch.arange(1000, dtype=torch.float64)[:, None, None] * torch.tensor([0.0, 0.0, 0.0])
+            + torch.from_numpy(rng.uniform(0, 100, (1000, 1, 3)))
+            + torch.linspace(0, 50, 300, dtype=torch.float64)[None, :, None] * torch.tensor([0.3, 0.5, 0.8]))
+    assert choose_order(rays.reshape(-1, 3)) == "given"
+    assert choose_order(iid[:1]) == "given"
