@@ -253,6 +253,12 @@ class PlanInterpreter:
         self._handles: dict = {}
         self._tp = plan.tensor_bspline_degree()
         self._kernel = kernel
+        # s = 2 plans run as their s = 3 lift (lift.py): same operations, third axis inert
+        self._lift = None
+        if plan.s == 2 and mode == "float":
+            from .lift import lift_plan
+
+            self._lift = PlanInterpreter(lift_plan(plan), mode, kernel)
 
     # -- native plan handle (one per device) ----------------------------------
     def _handle(self, device: torch.device):
@@ -291,11 +297,19 @@ class PlanInterpreter:
 
     def brick_log2(self, grid: CoefficientGrid) -> int:
         """Recommended brick edge (log2 unit cells) for this plan and the grid's dtype."""
+        if self._lift is not None:
+            from .lift import lift_grid
+
+            return self._lift.brick_log2(lift_grid(grid))
         dtype = _native.SP_F32 if grid.dtype == torch.float32 else _native.SP_F64
         return int(_native.lib().sp_brick_log2(self._handle(grid.device), dtype))
 
     def prepare(self, grid: CoefficientGrid, pts: torch.Tensor, *, presorted: bool = False) -> "PointBatch":
         """Brick-order a point set for repeated evaluation on this plan/grid."""
+        if self._lift is not None:
+            from .lift import lift_grid, lift_points
+
+            return self._lift.prepare(lift_grid(grid), lift_points(torch.as_tensor(pts)), presorted=presorted)
         b = self.brick_log2(grid)
         if b < 0:
             raise RuntimeError_("brick mode is not applicable to this plan")
@@ -303,6 +317,8 @@ class PlanInterpreter:
         return prepare_points(p, b, presorted=presorted)
 
     def kernel_name(self, device=None) -> str:
+        if self._lift is not None:
+            return self._lift.kernel_name(device)
         device = torch.device(device) if device is not None else _default_device()
         return _native.lib().sp_plan_kernel_name(self._handle(device)).decode()
 
@@ -342,6 +358,19 @@ class PlanInterpreter:
         self._check_grid(grid)
         if self.mode != "float":
             raise RuntimeError_("batch evaluation is float-mode only")
+        if self._lift is not None:
+            from .lift import lift_grid, lift_points
+
+            if isinstance(pts, PointBatch):
+                if pts.pts.shape[1] == 2:  # a brick partition of 2-D points: same runs, lifted points
+                    pts = PointBatch(lift_points(pts.pts), pts.brick_start, pts.log2_brick, pts.perm,
+                                     n_bricks_dev=pts.n_bricks_dev)
+            else:
+                if (pts.shape[-1] if hasattr(pts, "shape") else len(pts[0])) != 2:
+                    raise RuntimeError_("points must have shape (n, 2)")
+                pts = lift_points(pts)
+            return self._lift.eval_batch(lift_grid(grid), pts, out=out, check=check, order=order, reorder=reorder,
+                                         stream=stream)
         if isinstance(pts, PointBatch):
             return self._eval_bricks(grid, pts, out=out, check=check, stream=stream)
         is_numpy = not isinstance(pts, torch.Tensor)
@@ -574,6 +603,11 @@ class PlanInterpreter:
         """Per point and coset: class id and coset cell kk/d (runtime.py:371-379), as
         computed by the evaluation kernel itself.  Returns (classes (n,M), cells (n,M,s))."""
         self._check_grid(grid)
+        if self._lift is not None:
+            from .lift import lift_grid, lift_points
+
+            cls, cells = self._lift.classify(lift_grid(grid), lift_points(torch.as_tensor(pts)))
+            return cls, cells[:, :, :2]
         p = torch.as_tensor(pts).to(device=grid.device, dtype=grid.dtype).contiguous()
         n = p.shape[0]
         M = self.plan.M

@@ -19,7 +19,9 @@ from paper_2102_08514_b200.runtime import CoefficientGrid, PlanInterpreter, Runt
 
 pytestmark = pytest.mark.gpu
 
-NAMES = [n for n in golden_names() if deserialize_plan((corpus.PLAN_DIR / f"{n}.plan.json").read_text()).s == 3]
+# every golden plan: the 3-D ones natively, the reference corpus' 2-D ones (tp2, zp, qc_tensor)
+# through their 3-D lift (lift.py)
+NAMES = [n for n in golden_names() if deserialize_plan((corpus.PLAN_DIR / f"{n}.plan.json").read_text()).s in (2, 3)]
 
 
 def _setup(name, boundary, dtype, device):
@@ -154,12 +156,37 @@ def test_errors(cuda):
         PlanInterpreter(bad).eval_batch(grid, pts)
 
 
-def test_two_dimensional_plans_not_implemented(cuda):
+def test_two_dimensional_plans_run_lifted_and_four_dimensional_raise(cuda):
+    """2-D plans evaluate through their 3-D lift (numpy in -> numpy out, scalar eval); a
+    plan of any other dimension raises NotImplementedError (no CPU fallback)."""
+    from fractions import Fraction
+
+    from paper_2102_08514_b200.exact import Poly
+    from paper_2102_08514_b200.plan import ClassTransform, EvaluationPlan, FetchGroup, PlanKernel, PlanOptions
+
     plan = corpus.build_plan("zp")
     cos = decompose_cartesian(named_lattice("CC2"))
     grid = CoefficientGrid.zeros(cos, [0, 0], [8, 8], device=cuda)
+    grid.arrays[0].fill_(1.0)
+    interp = PlanInterpreter(plan)
+    out = interp.eval_batch(grid, np.array([[3.25, 4.5], [4.0, 4.0]]))
+    assert isinstance(out, np.ndarray) and np.allclose(out, 1.0, atol=1e-12)  # partition of unity inside
+    assert abs(interp.eval(grid, (4.5, 3.75)) - 1.0) < 1e-12
+    with pytest.raises(RuntimeError_):
+        interp.eval_batch(grid, torch.zeros((2, 3), dtype=torch.float64, device=cuda))
+    one = Fraction(1)
+    ident = tuple(tuple(one if i == j else Fraction(0) for j in range(4)) for i in range(4))
+    p4 = EvaluationPlan(name="nearest4", lattice_name="CC4", s=4, diag=(1,) * 4, shifts=((0,) * 4,), scale=one,
+                        planes=(), r=1, sigma=(0,),
+                        classes=(ClassTransform(0, ident, (Fraction(0),) * 4,
+                                                tuple(tuple(int(i == j) for j in range(4)) for i in range(4)), (0,) * 4),),
+                        kernels=(PlanKernel(0, (FetchGroup(((0, 0, 0, 0),), (), Poly.const(4, 1), ()),)),),
+                        options=PlanOptions(), basis_nonnegative=True, pou_on_sublattice=True,
+                        reflective_axes=(True,) * 4)
+    cos4 = decompose_cartesian(named_lattice("CC", 4))
+    g4 = CoefficientGrid.zeros(cos4, [0] * 4, [3] * 4, device=cuda)
     with pytest.raises(NotImplementedError):
-        PlanInterpreter(plan).eval_batch(grid, torch.zeros((2, 2), dtype=torch.float64, device=cuda))
+        PlanInterpreter(p4).eval_batch(g4, torch.zeros((2, 4), dtype=torch.float64, device=cuda))
 
 
 @pytest.mark.parametrize("name", NAMES)
@@ -177,7 +204,7 @@ def test_brick_mode_matches_chunk_mode(name, dtype, boundary, cuda):
     assert batch.n_bricks >= 1 and int(batch.brick_start[-1]) == pts.shape[0]
     b = interp.eval_batch(grid, batch)  # back in the caller's order
     torch.testing.assert_close(a, b, rtol=0, atol=0)
-    sorted_pts = batch.pts
+    sorted_pts = batch.pts[:, : plan.s]  # (2-D plans: the batch holds the lifted points)
     presorted = interp.prepare(grid, sorted_pts, presorted=True)
     c = interp.eval_batch(grid, presorted)
     torch.testing.assert_close(interp.eval_batch(grid, sorted_pts), c, rtol=0, atol=0)
