@@ -32,11 +32,12 @@ Target = Callable[[torch.Tensor], torch.Tensor]  # (m, 3) float64 positions -> (
 
 
 def gaussian(center=(0.05, -0.03, 0.02), sigma: float = 0.25) -> Target:
-    """SPEC.md:514 target: exp(-|x - c|^2 / (2 sigma^2))."""
+    """SPEC.md:514 target: exp(-|x - c|^2 / (2 sigma^2)) (the centre truncated to the
+    points' dimension)."""
     c = torch.tensor(center, dtype=torch.float64)
 
     def f(x: torch.Tensor) -> torch.Tensor:
-        d = x - c.to(x.device)
+        d = x - c[: x.shape[1]].to(x.device)
         return torch.exp(-(d * d).sum(-1) / (2.0 * sigma * sigma))
 
     return f
@@ -71,11 +72,12 @@ def sample_grid(cosets, target: Target, h: float, box: float, margin: int, *, de
                 boundary: str = "zero") -> CoefficientGrid:
     """Coefficient grid of f(h * site) over all lattice sites within box/h + margin."""
     r = int(math.ceil(box / h)) + margin
-    grid = CoefficientGrid.zeros(cosets, [-r] * 3, [r] * 3, boundary=boundary, device=device, dtype=dtype)
+    s = len(cosets.diag)
+    grid = CoefficientGrid.zeros(cosets, [-r] * s, [r] * s, boundary=boundary, device=device, dtype=dtype)
     diag = torch.tensor(cosets.diag, dtype=torch.float64, device=device)
     for k, arr in enumerate(grid.arrays):
         axes = [torch.arange(n, device=device, dtype=torch.float64) + o for n, o in zip(arr.shape, grid.origins[k])]
-        z = torch.stack(torch.meshgrid(*axes, indexing="ij"), -1).reshape(-1, 3)
+        z = torch.stack(torch.meshgrid(*axes, indexing="ij"), -1).reshape(-1, s)
         site = z * diag + torch.tensor(cosets.shifts[k], dtype=torch.float64, device=device)
         arr.copy_(target(h * site).reshape(arr.shape).to(dtype))
     return grid
@@ -94,14 +96,14 @@ def run_convergence(plan, target: Target, *, prefilter: Mapping | None = None, h
                     halvings: int = 4, samples: int = 1_000_000, box: float = 0.5, seed: int = 0,
                     dtype: torch.dtype = torch.float64, device=None) -> ConvergenceReport:
     """SPEC.md:508-516.  Scales h0 / 2^i for i < halvings; Monte-Carlo points uniform in the
-    centred box [-box, box]^3; the grid covers the box plus the spline's support."""
+    centred box [-box, box]^s; the grid covers the box plus the spline's support."""
     from .lattice import decompose_cartesian, named_lattice
 
     device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     cos = decompose_cartesian(named_lattice(plan.lattice_name))
     interp = PlanInterpreter(plan)
     gen = torch.Generator(device=device).manual_seed(seed)
-    x = (torch.rand((samples, 3), generator=gen, device=device, dtype=torch.float64) * 2.0 - 1.0) * box
+    x = (torch.rand((samples, plan.s), generator=gen, device=device, dtype=torch.float64) * 2.0 - 1.0) * box
     fx = target(x)
     rep = ConvergenceReport(plan=plan.name, prefiltered=prefilter is not None)
     margin = 8 + max(cos.diag)  # covers every corpus spline's support (SURVEY.md §9 footprints)

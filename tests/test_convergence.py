@@ -52,3 +52,16 @@ def test_approximation_order(name, order, taps, cuda):
     assert abs(rep.fitted_order - order) < 0.35, (rep.fitted_order, rep.errors)
     if order == 4:
         assert corpus.REFERENCE_ORDERS.get(name, 4) == 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["tp2", "zp", "qc_tensor"])
+def test_two_dimensional_corpus_splines(name, cuda):
+    """SPEC.md convergence examples in 2-D: TP2 on CC with a Gaussian target converges at
+    order 2; constants are reproduced (the 2-D plans run through their 3-D lift)."""
+    plan = corpus.build_plan(name)
+    rep = run_convergence(plan, constant(0.3), halvings=2, samples=100_000, device=cuda)
+    assert max(rep.max_errors) < 1e-12
+    rep = run_convergence(plan, gaussian(sigma=0.125), h0=0.0625, halvings=4, samples=200_000, device=cuda)
+    assert np.all(np.diff(rep.errors) < 0), rep.errors
+    assert abs(rep.fitted_order - corpus.REFERENCE_ORDERS.get(name, 2)) < 0.35, (rep.fitted_order, rep.errors)
