@@ -353,31 +353,11 @@ __device__ const uint4 kAff[kR * kNV] = {{
     {flat}
 }};
 
-// coset frame only (no class transform): xp exactly as runtime.py:371-373
-template <typename T>
-__device__ __forceinline__ void frame_f64(const T x[3], int k, int cell[3], double xp[3]) {{
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {{
-        const double xl = (double)x[i] - kShift[k][i];
-        const double q = floor(xl * kInvD);  // power-of-two d: exact
-        xp[i] = xl - q * kD;
-        cell[i] = clamp_cell(q);
-    }}
-}}
-__device__ __forceinline__ void frame_fast(const float frac[3], const int X[3], int k, int cell[3], float xp[3]) {{
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {{
-        const int xm = X[i] - kShiftI[k][i];
-        cell[i] = xm >> kLog2D;
-        const int p = xm & (kDI - 1);
-        xp[i] = kDI == 1 ? frac[i] : (kDI == 2 ? (p ? frac[i] + 1.0f : frac[i]) : frac[i] + (float)p);
-    }}
-}}
-
 template <typename T>
 struct Eval {{
     static constexpr int kMinBlocks = {min_blocks};
     static constexpr int kTrecBytes = kM * kR * 16 + kR * kNV * 16;
+    static constexpr bool kSig = false;
     template <typename U>
     static constexpr int vec_width() {{
         return 0;
@@ -467,6 +447,52 @@ struct Eval {{
 """
 
 
+_WORD_CLASS = """    __device__ __forceinline__ static int word_class(unsigned word, int k) {
+        const unsigned b = (word >> (8 * k)) & 0xffu;
+        return b == 0xffu ? -1 : (int)b;
+    }
+"""
+
+
+def _signature_methods(plan: EvaluationPlan) -> str:
+    """Kernel-signature support for K > 1 plans (brick_kernel_sig, sp_common.cuh): the raw
+    classes of all cosets packed in one word, and the point's signature = its kernel id per
+    coset in base K; the driver groups a brick's points by signature so that warps run one
+    kernel per coset instead of every kernel that occurs among their lanes."""
+    return f"""    static constexpr bool kSig = true;
+    static constexpr int kSigCount = {plan.K ** plan.M};
+""" + _WORD_CLASS + """    template <class Ctx>
+    __device__ __forceinline__ static unsigned classify_word(const T x[3], const Ctx& ctx) {
+        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
+        float frac[3] = {0.f, 0.f, 0.f};
+        const bool fast = fast_frame(x, frac);
+        unsigned w = 0;
+#pragma unroll
+        for (int k = 0; k < kM; ++k) {
+            int cell[3], raw;
+            if (fast) {
+                float xp[3];
+                frame_fast(frac, ctx.X, k, cell, xp);
+                raw = class_of<float>(xp, sigma);
+            } else {
+                double xp[3];
+                frame_f64<T>(x, k, cell, xp);
+                raw = class_of<double>(xp, sigma);
+            }
+            w |= (unsigned)(raw & 0xff) << (8 * k);
+        }
+        return w;
+    }
+    __device__ __forceinline__ static int signature(unsigned word, const unsigned char* tables) {
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
+        int sig = 0;
+#pragma unroll
+        for (int k = 0; k < kM; ++k) sig = sig * """ + str(plan.K) + """ + (int)(cls_tab[max(word_class(word, k), 0)].x & 15u);
+        return sig;
+    }
+"""
+
+
 def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple:
     """(translation-unit source, stats) for one plan; `stem` names the catalog entry."""
     if not codegen_supported(plan):
@@ -490,8 +516,17 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
             kfuncs.append("")
             kflops.append(fl)
     sig_bytes = ((plan.r * 4) + 15) & ~15
-    # occupancy hint for ptxas: light weight programs keep 4 CTAs (<= 64 regs) per SM
-    min_blocks = 4 if max(kflops) <= 64 else (2 if max(kflops) <= 700 else 1)
+    # occupancy hint (measured on B200): light programs keep 4 CTAs (<= 64 regs); heavier ones 2
+    # (cc_zp3_ungrouped, 935 ops: 2 CTAs with 60 B of spills beat 1 CTA without by 14 %;
+    # bcc_quintic_rd at 3 CTAs spills 236 B and loses 9 %)
+    min_blocks = 4 if max(kflops) <= 64 else (2 if max(kflops) <= 1000 else 1)
+    if plan.K > 1 and max(kflops) <= 128:
+        min_blocks = 3  # signature driver: 80 registers, 3 CTAs/SM (measured +11 % over 2)
+    # build-time override for occupancy experiments: SP_CODEGEN_MINBLOCKS="stem:n,stem:n"
+    for item in filter(None, os.environ.get("SP_CODEGEN_MINBLOCKS", "").split(",")):
+        k, v = item.split(":")
+        if k == stem:
+            min_blocks = int(v)
     planes = []
     for j, (n, off) in enumerate(plan.planes):
         planes.append(f"    q |= ({_plane_expr(n)} >= R({float(off)!r})) ? {1 << j} : 0;")
@@ -509,6 +544,8 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
             f"                case {k}: acc = kernel{k}<T>(y0, y1, y2, f); break;" for k in range(plan.K)
         )
         dispatch = f"            T acc = T(0);\n            switch (kern) {{\n{cases}\n            }}"
+    sig_ok = plan.K > 1 and plan.M <= 4 and plan.N < 255 and plan.K ** plan.M <= 1024
+    sig_methods = _signature_methods(plan) if sig_ok else "    static constexpr bool kSig = false;\n" + _WORD_CLASS
     if aff is not None:
         eval_src = _affine_eval_source(plan, aff[0], aff[1], min_blocks)
     else:
@@ -541,13 +578,9 @@ struct Eval {{
             trec[idx] = make_int4(cf[0], cf[1], cf[2], z);
         }}
     }}
-    template <class F, class Ctx>
-    __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
-        const EvalArgs<T>& a = *ctx.a;
-        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
-        const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
+    // float32 points: exact float32 frame when |x_i| in [kFastLo, kFastHi) (see kFastLo)
+    __device__ __forceinline__ static bool fast_frame(const T x[3], float frac[3]) {{
         bool fast = false;
-        float frac[3] = {{0.f, 0.f, 0.f}};
         if constexpr (sizeof(T) == 4) {{
             const float m = fminf(fminf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
             const float M = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fabsf(x[2]));
@@ -555,14 +588,43 @@ struct Eval {{
 #pragma unroll
             for (int i = 0; i < 3; ++i) frac[i] = (float)x[i] - floorf((float)x[i]);
         }}
+        return fast;
+    }}
+{sig_methods}
+    template <class F, class Ctx>
+    __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
+        return eval_impl<false>(x, 0u, f, ctx);
+    }}
+    // classes given (8 bits per coset, 0xff = sentinel), e.g. by classify_word: no plane tests
+    template <class F, class Ctx>
+    __device__ __forceinline__ static T eval_word(const T x[3], unsigned word, F& f, const Ctx& ctx) {{
+        return eval_impl<true>(x, word, f, ctx);
+    }}
+    template <bool kWord, class F, class Ctx>
+    __device__ __forceinline__ static T eval_impl(const T x[3], unsigned word, F& f, const Ctx& ctx) {{
+        const EvalArgs<T>& a = *ctx.a;
+        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
+        float frac[3] = {{0.f, 0.f, 0.f}};
+        const bool fast = fast_frame(x, frac);
         T total = T(0);
 #pragma unroll
         for (int k = 0; k < kM; ++k) {{
             int cell[3];
             T yy[3];
             uint4 rec;
-            const int raw = fast ? classify_fast<T>(frac, ctx.X, k, sigma, cls_tab, ctx.err, cell, yy, rec)
-                                 : classify_f64<T>(x, k, sigma, cls_tab, ctx.err, cell, yy, rec);
+            int raw;
+            if (fast) {{
+                float xp[3];
+                frame_fast(frac, ctx.X, k, cell, xp);
+                raw = kWord ? word_class(word, k) : class_of<float>(xp, sigma);
+                y_of<float, T>(xp, raw, cls_tab, ctx.err, yy, rec);
+            }} else {{
+                double xp[3];
+                frame_f64<T>(x, k, cell, xp);
+                raw = kWord ? word_class(word, k) : class_of<double>(xp, sigma);
+                y_of<double, T>(xp, raw, cls_tab, ctx.err, yy, rec);
+            }}
             write_dbg(a.dbg, ctx.index, kM, k, raw, cell);  // raw class: -1 for the sentinel
             const int c = max(raw, 0);
             const int kern = (int)(rec.x & 15u);
@@ -630,10 +692,9 @@ __device__ __forceinline__ int plane_code(const R xp0, const R xp1, const R xp2)
 // coset frame (runtime.py:371-373), plane tests (:374-378), sigma (:379) and y = T xp - t
 // (:385) for coset k, evaluated in R (float on the fast path, else double).
 // class lookup + y = T xp - t from the packed class record
+// y = T xp - t (runtime.py:385) from the packed record of class max(raw, 0)
 template <typename R, typename T>
-__device__ __forceinline__ int class_and_y(const R xp[3], const int* sigma, const uint4* cls_tab, int& err,
-                                           T y[3], uint4& rec) {{
-    const int raw = sigma[plane_code<R>(xp[0], xp[1], xp[2]) % kR];
+__device__ __forceinline__ void y_of(const R xp[3], int raw, const uint4* cls_tab, int& err, T y[3], uint4& rec) {{
     err |= raw < 0;  // sigma sentinel (runtime.py:380-381): flagged, evaluated as class 0
     const int c = max(raw, 0);
     rec = cls_tab[c];
@@ -645,14 +706,25 @@ __device__ __forceinline__ int class_and_y(const R xp[3], const int* sigma, cons
         const R v = (perm & 2u) ? xp[2] : v01;
         y[i] = (T)((((rec.x >> (10 + i)) & 1u) ? -v : v) - (R)tt[i]);
     }}
+}}
+
+// plane tests (:374-378) and sigma (:379)
+template <typename R>
+__device__ __forceinline__ int class_of(const R xp[3], const int* sigma) {{
+    return sigma[plane_code<R>(xp[0], xp[1], xp[2]) % kR];
+}}
+
+template <typename R, typename T>
+__device__ __forceinline__ int class_and_y(const R xp[3], const int* sigma, const uint4* cls_tab, int& err,
+                                           T y[3], uint4& rec) {{
+    const int raw = class_of<R>(xp, sigma);
+    y_of<R, T>(xp, raw, cls_tab, err, y, rec);
     return raw;
 }}
 
 // float64 coset frame exactly as runtime.py:371-373 (any point)
 template <typename T>
-__device__ __forceinline__ int classify_f64(const T x[3], int k, const int* sigma, const uint4* cls_tab, int& err,
-                                            int cell[3], T y[3], uint4& rec) {{
-    double xp[3];
+__device__ __forceinline__ void frame_f64(const T x[3], int k, int cell[3], double xp[3]) {{
 #pragma unroll
     for (int i = 0; i < 3; ++i) {{
         const double xl = (double)x[i] - kShift[k][i];
@@ -660,16 +732,12 @@ __device__ __forceinline__ int classify_f64(const T x[3], int k, const int* sigm
         xp[i] = xl - q * kD;
         cell[i] = clamp_cell(q);
     }}
-    return class_and_y<double, T>(xp, sigma, cls_tab, err, y, rec);
 }}
 
 // float32 fast frame from X = floor(x) and frac = x - X (exact): for integer l and d = 2^j,
 // floor((x-l)/d) = (X-l) >> j and xp = frac + ((X-l) & (d-1)), exactly the float64 values
 // for |x| >= kFastLo (frac + p needs no rounding there).
-template <typename T>
-__device__ __forceinline__ int classify_fast(const float frac[3], const int X[3], int k, const int* sigma,
-                                             const uint4* cls_tab, int& err, int cell[3], T y[3], uint4& rec) {{
-    float xp[3];
+__device__ __forceinline__ void frame_fast(const float frac[3], const int X[3], int k, int cell[3], float xp[3]) {{
 #pragma unroll
     for (int i = 0; i < 3; ++i) {{
         const int xm = X[i] - kShiftI[k][i];
@@ -677,6 +745,21 @@ __device__ __forceinline__ int classify_fast(const float frac[3], const int X[3]
         const int p = xm & (kDI - 1);
         xp[i] = kDI == 1 ? frac[i] : (kDI == 2 ? (p ? frac[i] + 1.0f : frac[i]) : frac[i] + (float)p);
     }}
+}}
+
+template <typename T>
+__device__ __forceinline__ int classify_f64(const T x[3], int k, const int* sigma, const uint4* cls_tab, int& err,
+                                            int cell[3], T y[3], uint4& rec) {{
+    double xp[3];
+    frame_f64<T>(x, k, cell, xp);
+    return class_and_y<double, T>(xp, sigma, cls_tab, err, y, rec);
+}}
+
+template <typename T>
+__device__ __forceinline__ int classify_fast(const float frac[3], const int X[3], int k, const int* sigma,
+                                             const uint4* cls_tab, int& err, int cell[3], T y[3], uint4& rec) {{
+    float xp[3];
+    frame_fast(frac, X, k, cell, xp);
     return class_and_y<float, T>(xp, sigma, cls_tab, err, y, rec);
 }}
 

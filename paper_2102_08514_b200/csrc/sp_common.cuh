@@ -591,6 +591,118 @@ __device__ __forceinline__ T eval_one(const T x[3], bool staged, int c0, int c1,
     return Ev::template eval<GlobalFetch<T>>(x, f, ctx);
 }
 
+// Kernel-signature grouping for plans with K > 1 kernels (generated Evs with kSig): a warp
+// evaluating points whose cosets select different kernels runs every selected kernel for
+// every coset (SIMT divergence: fcc_cubic spends 55 % of its instructions there).  Per
+// segment of up to 1024 points of a brick: pass 1 classifies each point (plane tests and
+// sigma only) into a word of per-coset classes and a signature = its kernel id per coset;
+// a counting sort by signature (shared-memory histogram, warp scan, atomic scatter) orders
+// the segment; pass 2 evaluates in that order from the stored classes (Ev::eval_word: no
+// plane tests), so consecutive lanes share kernels.  Values are those of Ev::eval bit for
+// bit (same frames, same classes); only the evaluation order changes.  Points that are
+// non-finite or outside the staged brick form their own bucket and take the per-point path.
+template <typename T, class Ev, typename V>
+__device__ __forceinline__ void eval_brick_sig(const EvalArgs<T>& a, EvalCtx<T, Ev>& ctx, long long p0, long long p1,
+                                               bool staged, int c0, int c1, int c2, int B, const T* tile,
+                                               const V* vtile, const unsigned char* tables) {
+    constexpr int kSeg = 1024;
+    constexpr int kBuckets = Ev::kSigCount + 1;  // last bucket: per-point path
+    static_assert(kBuckets <= 65535, "signature count");
+    constexpr int kPer = kSeg / kThreads;
+    __shared__ unsigned s_word[kSeg];
+    __shared__ unsigned short s_order[kSeg];
+    __shared__ unsigned short s_key[kSeg];
+    __shared__ int s_hist[kBuckets];
+    __shared__ T s_pts[3 * kSeg];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (long long seg = p0; seg < p1; seg += kSeg) {
+        const int n = (int)min((long long)kSeg, p1 - seg);
+        for (int i = tid; i < kBuckets; i += kThreads) s_hist[i] = 0;
+        // the segment's points -> shared memory (coalesced, all loads in flight together)
+        {
+            T v[3 * kPer];
+            const T* src = a.pts + 3 * seg;
+#pragma unroll
+            for (int q = 0; q < 3 * kPer; ++q) {
+                const int e = tid + q * kThreads;
+                v[q] = e < 3 * n ? __ldg(src + e) : T(0);
+            }
+#pragma unroll
+            for (int q = 0; q < 3 * kPer; ++q) s_pts[tid + q * kThreads] = v[q];
+        }
+        __syncthreads();
+        for (int i = tid; i < n; i += kThreads) {  // pass 1: classes and signature
+            const T x[3] = {s_pts[3 * i], s_pts[3 * i + 1], s_pts[3 * i + 2]};
+            const bool fin = isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]);
+            ctx.X[0] = clamp_cell(x[0]);
+            ctx.X[1] = clamp_cell(x[1]);
+            ctx.X[2] = clamp_cell(x[2]);
+            const bool inside = (unsigned)(ctx.X[0] - c0) < (unsigned)B && (unsigned)(ctx.X[1] - c1) < (unsigned)B &&
+                                (unsigned)(ctx.X[2] - c2) < (unsigned)B;
+            int key = kBuckets - 1;
+            unsigned w = 0u;
+            if (fin && staged && inside) {
+                w = Ev::classify_word(x, ctx);
+                key = Ev::signature(w, tables);
+            }
+            s_word[i] = w;
+            s_key[i] = (unsigned short)key;
+            atomicAdd(&s_hist[key], 1);
+        }
+        __syncthreads();
+        if (tid < 32) {  // exclusive scan of the histogram: lane-contiguous chunks + warp scan
+            constexpr int kPer = (kBuckets + 31) / 32;
+            int local = 0;
+            for (int q = 0; q < kPer; ++q) {
+                const int b = lane * kPer + q;
+                if (b < kBuckets) local += s_hist[b];
+            }
+            int incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int run = incl - local;
+            for (int q = 0; q < kPer; ++q) {
+                const int b = lane * kPer + q;
+                if (b < kBuckets) {
+                    const int c = s_hist[b];
+                    s_hist[b] = run;
+                    run += c;
+                }
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < n; i += kThreads) s_order[atomicAdd(&s_hist[s_key[i]], 1)] = (unsigned short)i;
+        __syncthreads();
+#pragma unroll 1
+        for (int r = tid; r < n; r += kThreads) {  // pass 2: evaluation in signature order
+            const int i = s_order[r];
+            const long long j = seg + i;
+            const T x[3] = {s_pts[3 * i], s_pts[3 * i + 1], s_pts[3 * i + 2]};
+            ctx.index = j;
+            ctx.X[0] = clamp_cell(x[0]);
+            ctx.X[1] = clamp_cell(x[1]);
+            ctx.X[2] = clamp_cell(x[2]);
+            T v;
+            if (s_key[i] != kBuckets - 1) {
+                TileFetch<T, V> f;
+                f.tile = tile;
+                f.vtile = vtile;
+                v = Ev::template eval_word<TileFetch<T, V>>(x, s_word[i], f, ctx);
+            } else if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) {
+                v = T(NAN);
+            } else {
+                GlobalFetch<T> f;
+                v = Ev::template eval<GlobalFetch<T>>(x, f, ctx);
+            }
+            store_out(a, j, v);
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // Brick mode: points sorted by the Morton code of their unit cell are grouped into aligned
 // bricks of B^3 unit cells (B = 2^log2b); brick_start[b]..brick_start[b+1] are brick b's
@@ -661,6 +773,13 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
             xn0 = __ldg(px);
             xn1 = __ldg(px + 1);
             xn2 = __ldg(px + 2);
+        }
+        if constexpr (Ev::kSig) {
+            // K > 1 plans: points grouped by kernel signature before evaluation
+            eval_brick_sig<T, Ev, V>(a, ctx, p0, p1, staged, c0, c1, c2, B, tile, vtile, smem);
+            if (ctx.err && a.err) atomicOr(a.err, 1);
+            __syncthreads();
+            continue;
         }
 #pragma unroll 1
         for (long long j = p0 + tid; j < p1; j += kThreads) {

@@ -68,6 +68,7 @@ struct BWeights<3> {
 template <typename T, int DEG>
 struct TensorBSplineEval {
     static constexpr int kMinBlocks = sizeof(T) == 4 ? 4 : 3;  // <= 64 / 80 registers
+    static constexpr bool kSig = false;
     __device__ static void tile_records(const EvalArgs<T>&, const TileGeom&, const unsigned char*, int4*, int) {}
     // fp32: rows of DEG+1 taps are one LDS.64 / LDS.128 from the row-vector tile
     template <typename U>
@@ -180,6 +181,7 @@ __device__ __forceinline__ T generic_poly(const GenericTables& gt, int p, const 
 template <typename T>
 struct GenericEval {
     static constexpr int kMinBlocks = 1;
+    static constexpr bool kSig = false;
 
     __device__ static void tile_records(const EvalArgs<T>&, const TileGeom&, const unsigned char*, int4*, int) {}
     template <typename U>
