@@ -8,6 +8,7 @@
 // write of every output coset.
 // Separate multiply / add roundings in the given tap order, boundary policy on every read
 // (runtime.py:109-123), so float64 results equal the reference's per-site loop bit for bit.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -34,7 +35,7 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 // lanes along the contiguous axis, boundary policy resolved here — then every output is
 // sum_t w_t * box[t][...] with the tap's box offset precomputed on the host: one LDS, one
 // multiply, one add per tap, separate roundings, taps in the given order.
-constexpr int kTX = 128, kTY = 32, kThreadsPF = 256;
+constexpr int kTX = 128, kTY = 16, kThreadsPF = 256, kZChunk = 32;
 
 template <typename T>
 struct TileTaps {             // one output coset
@@ -43,9 +44,12 @@ struct TileTaps {             // one output coset
     int box_src[SP_MAX_COSETS];
     int box_lo[SP_MAX_COSETS][3];   // min tap offset per axis (box origin relative to the tile)
     int box_ex[SP_MAX_COSETS][3];   // box extents
-    int box_off[SP_MAX_COSETS];     // smem element offset of the box
+    int box_off[SP_MAX_COSETS];     // smem element offset of the box's plane ring
+    int ring[SP_MAX_COSETS];        // planes in the ring: power of two >= box_ex[0] + 1 (one prefetched ahead)
+    int slot_elems[SP_MAX_COSETS];  // ring slot stride (elements; 128-byte multiple)
     int tap_box[SP_MAX_STENCIL];
-    int tap_off[SP_MAX_STENCIL];    // box_off + linear offset of (dz - lo) in the box
+    int tap_dz0[SP_MAX_STENCIL];    // plane offset of the tap
+    int tap_off[SP_MAX_STENCIL];    // in-plane offset of (dz1 - lo1, dz2 - lo2)
     T w[SP_MAX_STENCIL];
 };
 
@@ -80,96 +84,210 @@ __device__ __forceinline__ long long policy_index(const sp::GridArgs<T>& g, int 
     return ((long long)a0 * e1 + a1) * e2 + a2;
 }
 
-template <typename T, int NT>
-__global__ void __launch_bounds__(kThreadsPF) prefilter_tiled(const sp::GridArgs<T> g, const TileParams<T> P) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* sm = reinterpret_cast<T*>(smem_raw);
-    const int k = blockIdx.z % g.M;
-    const int z0 = blockIdx.z / g.M;
-    const TileTaps<T>& tp = P.c[k];
-    const int e1 = g.ext[k][1], e2 = g.ext[k][2];
-    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
-    if (z0 >= g.ext[k][0] || y0 >= e1 || x0 >= e2) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // stage the source boxes: warp per box row, each lane issues all of its row's loads
-    // before storing any (up to kChunks in flight), boundary policy folded into the index.
-    // Only the part of each box the tile's VALID outputs read is staged (edge tiles are
-    // clipped to the array), so interior-vs-policy is decided on what is actually read.
-    const int wv = min(kTX, e2 - x0), hv = min(kTY, e1 - y0);
-    for (int b = 0; b < tp.nbox; ++b) {
-        const int s = tp.box_src[b];
-        const int ex1 = tp.box_ex[b][1], ex2 = tp.box_ex[b][2];
-        const int ex1c = ex1 - (kTY - hv), ex2c = ex2 - (kTX - wv);  // clipped extents
-        const int ex0 = tp.box_ex[b][0];
-        const int s0 = z0 + tp.box_lo[b][0], s1 = y0 + tp.box_lo[b][1], s2 = x0 + tp.box_lo[b][2];
-        const T* src = g.data[s];
-        T* dst = sm + tp.box_off[b];
-        const bool inside = s0 >= 0 && s1 >= 0 && s2 >= 0 && s0 + ex0 <= g.ext[s][0] && s1 + ex1c <= g.ext[s][1] &&
-                            s2 + ex2c <= g.ext[s][2];
-        for (int i0 = 0; i0 < ex0; ++i0) {
-            for (int i1 = warp; i1 < ex1c; i1 += kThreadsPF / 32) {
-                T* drow = dst + (i0 * ex1 + i1) * ex2;
-                T v[kChunks];
-                if (inside) {
-                    const T* rp = src + ((long long)(s0 + i0) * g.ext[s][1] + (s1 + i1)) * g.ext[s][2] + s2;
-#pragma unroll
-                    for (int c = 0; c < kChunks; ++c) v[c] = lane + 32 * c < ex2c ? __ldg(rp + lane + 32 * c) : T(0);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < kChunks; ++c) {
-                        bool ok = lane + 32 * c < ex2c;
-                        const long long idx = policy_index(g, s, s0 + i0, s1 + i1, s2 + lane + 32 * c, ok);
-                        v[c] = ok ? __ldg(src + idx) : T(0);
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < kChunks; ++c)
-                    if (lane + 32 * c < ex2c) drow[lane + 32 * c] = v[c];
+// Copy plane `p` (coset-cell index along axis 0) of box b's rows [y0 + lo1, ...) x
+// [x0 + lo2, ...) into ring slot `slot` with cp.async (4 / 8-byte elements, zero-filled for the
+// 'zero' policy outside the array, clamp / mirror indices otherwise): warp per row.
+template <typename T>
+__device__ __forceinline__ void stage_plane(const sp::GridArgs<T>& g, const TileTaps<T>& tp, int b, int p, int slot,
+                                            int y0, int x0, int hv, int wv, T* sm, int lane, int warp) {
+    const int s = tp.box_src[b];
+    const int ex1 = tp.box_ex[b][1], ex2 = tp.box_ex[b][2];
+    const int ex1c = ex1 - (kTY - hv), ex2c = ex2 - (kTX - wv);  // rows / columns the valid outputs read
+    const int s1 = y0 + tp.box_lo[b][1], s2 = x0 + tp.box_lo[b][2];
+    const T* src = g.data[s];
+    T* dst = sm + tp.box_off[b] + slot * tp.slot_elems[b];
+    const int e0 = g.ext[s][0], e1 = g.ext[s][1], e2 = g.ext[s][2];
+    const bool inside = p >= 0 && p < e0 && s1 >= 0 && s2 >= 0 && s1 + ex1c <= e1 && s2 + ex2c <= e2;
+    for (int i1 = warp; i1 < ex1c; i1 += kThreadsPF / 32) {
+        T* drow = dst + i1 * ex2;
+        if (inside) {
+            const T* rp = src + ((long long)p * e1 + (s1 + i1)) * e2 + s2;
+            for (int c = lane; c < ex2c; c += 32) sp::cp_async_elem<sizeof(T)>(drow + c, rp + c, (int)sizeof(T));
+        } else {
+            for (int c = lane; c < ex2c; c += 32) {
+                bool ok = true;
+                const long long idx = policy_index(g, s, p, s1 + i1, s2 + c, ok);
+                sp::cp_async_elem<sizeof(T)>(drow + c, src + (ok ? idx : 0), ok ? (int)sizeof(T) : 0);
             }
         }
     }
-    __syncthreads();
-    const int tx = tid % kTX;
-    const int z2 = x0 + tx;
-    if (z2 >= e2) return;
-    const int ty = tid / kTX;
-    constexpr int kRowsPerThread = kTY / (kThreadsPF / kTX);
-    T* out = P.out[k] + ((long long)z0 * e1 + y0) * e2 + z2;
-    if constexpr (NT > 0) {
-        int base[NT], pitch[NT];
-        T w[NT];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-            pitch[t] = tp.box_ex[tp.tap_box[t]][2];
-            base[t] = tp.tap_off[t] + ty * pitch[t] + tx;
-            w[t] = tp.w[t];
+}
+
+// z-marching kernel.  One block = an output tile of kTX (z2) x kTY (z1) samples of output
+// coset k, marching over kZChunk planes z0: each source box keeps a ring of box_ex[0] + 1
+// staged planes, so every input plane is copied into shared memory once per tile column
+// (cp.async, one plane ahead of the computation) instead of once per output plane.  Each
+// output is sum_t w_t * box[t][...] — one LDS, one multiply, one add per tap, separate
+// roundings, taps in the given order (bit-identical to a per-site loop over site_value).
+// Tensor maps of the TMA variant: one per (output coset, source box), box = one plane of the
+// source box (rows x 16-byte aligned columns); out-of-range texels are zero-filled by the TMA
+// unit, which is the 'zero' policy.
+constexpr int kMaxMaps = 16;
+struct PfMaps {
+    CUtensorMap m[kMaxMaps];
+    int nbox_max;
+    unsigned set_bytes[SP_MAX_COSETS];  // bytes of one plane of every box, per output coset
+};
+
+__device__ __forceinline__ void pf_mbar_init(unsigned long long* bar) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void pf_mbar_expect(unsigned long long* bar, unsigned bytes) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pf_mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void pf_tma_plane(void* dst, const CUtensorMap* map, unsigned long long* bar, int c0, int c1,
+                                             int c2) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(d), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(b)
+        : "memory");
+}
+
+template <typename T, int NT, bool kTma>
+__global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArgs<T> g, const TileParams<T> P,
+                                                               const __grid_constant__ PfMaps maps) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* sm = reinterpret_cast<T*>(smem_raw);
+    __shared__ __align__(8) unsigned long long mbar[2];
+    const int k = blockIdx.z % g.M;
+    const int zc = blockIdx.z / g.M;
+    const TileTaps<T>& tp = P.c[k];
+    const int e0 = g.ext[k][0], e1 = g.ext[k][1], e2 = g.ext[k][2];
+    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+    const int za = zc * kZChunk, zb = min(za + kZChunk, e0);
+    if (za >= e0 || y0 >= e1 || x0 >= e2) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wv = min(kTX, e2 - x0), hv = min(kTY, e1 - y0);
+    auto slot_of = [&](int b, int p) { return p & (tp.ring[b] - 1); };  // ring sizes are powers of two
+    // TMA: one elected thread copies whole box planes (mbarrier complete_tx), set i of planes on
+    // mbar[i & 1]; cp.async: every thread copies its share, one commit group per set
+    auto issue_tma = [&](int b, int p, unsigned long long* bar) {
+        pf_tma_plane(sm + tp.box_off[b] + slot_of(b, p) * tp.slot_elems[b], &maps.m[k * maps.nbox_max + b], bar,
+                     x0 + tp.box_lo[b][2], y0 + tp.box_lo[b][1], p);
+    };
+    if constexpr (kTma) {
+        if (tid == 0) {
+            pf_mbar_init(&mbar[0]);
+            pf_mbar_init(&mbar[1]);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-#pragma unroll
-        for (int j = 0; j < kRowsPerThread; ++j) {
-            const int r = ty + j * (kThreadsPF / kTX);
-            if (y0 + r >= e1) break;
-            T acc = T(0);
-#pragma unroll
-            for (int t = 0; t < NT; ++t) acc = add_rn(acc, mul_rn(w[t], sm[base[t] + j * (kThreadsPF / kTX) * pitch[t]]));
-            out[(long long)r * e2] = acc;
+        __syncthreads();
+    }
+    // prologue: planes za + lo0 .. za + hi0 of every box
+    if constexpr (kTma) {
+        if (tid == 0) {
+            unsigned bytes = 0;
+            for (int b = 0; b < tp.nbox; ++b) bytes += (unsigned)tp.box_ex[b][0] * (unsigned)(tp.box_ex[b][1] * tp.box_ex[b][2] * (int)sizeof(T));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            pf_mbar_expect(&mbar[0], bytes);
+            for (int b = 0; b < tp.nbox; ++b)
+                for (int i0 = 0; i0 < tp.box_ex[b][0]; ++i0) issue_tma(b, za + tp.box_lo[b][0] + i0, &mbar[0]);
         }
     } else {
-        for (int j = 0; j < kRowsPerThread; ++j) {
-            const int r = ty + j * (kThreadsPF / kTX);
-            if (y0 + r >= e1) break;
-            T acc = T(0);
-            for (int t = 0; t < tp.n; ++t) {
-                const int b = tp.tap_box[t];
-                acc = add_rn(acc, mul_rn(tp.w[t], sm[tp.tap_off[t] + r * tp.box_ex[b][2] + tx]));
+        for (int b = 0; b < tp.nbox; ++b)
+            for (int i0 = 0; i0 < tp.box_ex[b][0]; ++i0) {
+                const int p = za + tp.box_lo[b][0] + i0;
+                stage_plane(g, tp, b, p, slot_of(b, p), y0, x0, hv, wv, sm, lane, warp);
             }
-            out[(long long)r * e2] = acc;
-        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
+    const int tx = tid % kTX, ty = tid / kTX;
+    constexpr int kRowsPerThread = kTY / (kThreadsPF / kTX);
+    const bool col_ok = x0 + tx < e2;
+    for (int z0 = za; z0 < zb; ++z0) {
+        const int it = z0 - za;
+        if constexpr (kTma) {
+            if (tid == 0 && z0 + 1 < zb) {  // prefetch the one new plane per box the next output plane needs
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                pf_mbar_expect(&mbar[(it + 1) & 1], maps.set_bytes[k]);
+                for (int b = 0; b < tp.nbox; ++b)
+                    issue_tma(b, z0 + 1 + tp.box_lo[b][0] + tp.box_ex[b][0] - 1, &mbar[(it + 1) & 1]);
+            }
+            pf_mbar_wait(&mbar[it & 1], (unsigned)(it >> 1) & 1u);
+        } else {
+            if (z0 + 1 < zb)  // prefetch the one new plane per box the next output plane needs
+                for (int b = 0; b < tp.nbox; ++b) {
+                    const int p = z0 + 1 + tp.box_lo[b][0] + tp.box_ex[b][0] - 1;
+                    stage_plane(g, tp, b, p, slot_of(b, p), y0, x0, hv, wv, sm, lane, warp);
+                }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            __syncthreads();
+        }
+        if (col_ok) {
+            T* out = P.out[k] + ((long long)z0 * e1 + y0) * e2 + x0 + tx;
+            if constexpr (NT > 0) {
+                int base[NT], pitch[NT];
+                T w[NT];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    const int b = tp.tap_box[t];
+                    pitch[t] = tp.box_ex[b][2];
+                    base[t] = tp.box_off[b] + slot_of(b, z0 + tp.tap_dz0[t]) * tp.slot_elems[b] + tp.tap_off[t] +
+                              ty * pitch[t] + tx;
+                    w[t] = tp.w[t];
+                }
+#pragma unroll
+                for (int j = 0; j < kRowsPerThread; ++j) {
+                    const int r = ty + j * (kThreadsPF / kTX);
+                    if (y0 + r >= e1) break;
+                    T acc = T(0);
+#pragma unroll
+                    for (int t = 0; t < NT; ++t)
+                        acc = add_rn(acc, mul_rn(w[t], sm[base[t] + j * (kThreadsPF / kTX) * pitch[t]]));
+                    out[(long long)r * e2] = acc;
+                }
+            } else {
+                for (int j = 0; j < kRowsPerThread; ++j) {
+                    const int r = ty + j * (kThreadsPF / kTX);
+                    if (y0 + r >= e1) break;
+                    T acc = T(0);
+                    for (int t = 0; t < tp.n; ++t) {
+                        const int b = tp.tap_box[t];
+                        const int pl = tp.box_off[b] + slot_of(b, z0 + tp.tap_dz0[t]) * tp.slot_elems[b];
+                        acc = add_rn(acc, mul_rn(tp.w[t], sm[pl + tp.tap_off[t] + r * tp.box_ex[b][2] + tx]));
+                    }
+                    out[(long long)r * e2] = acc;
+                }
+            }
+        }
+        __syncthreads();  // the slot read now is refilled by the next step's prefetch
+    }
+    if constexpr (!kTma) asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 int pfail(int code, const std::string& msg) {
     sp::set_error(msg);
     return code;
+}
+
+typedef CUresult (*PfEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PfEncodeFn pf_encoder() {
+    static PfEncodeFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PfEncodeFn>(f);
+    }
+    return fn;
 }
 
 template <typename T>
@@ -189,85 +307,160 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
             max_e[i] = std::max(max_e[i], (long long)in->extent[k][i]);
         }
     }
-    if ((max_e[1] + kTY - 1) / kTY > 65535 || max_e[0] * in->M > 65535)
+    if ((max_e[1] + kTY - 1) / kTY > 65535 || (max_e[0] + kZChunk - 1) / kZChunk * in->M > 65535)
         return pfail(SP_ERR_UNSUPPORTED, "prefilter: coset extents too large for the launch grid");
+    // 1. per output coset: one source box per source coset = tile + the taps' offset range
     TileParams<T> P{};
-    int smem_max = 0;
+    int lo[SP_MAX_COSETS][SP_MAX_COSETS][3], box_of[SP_MAX_COSETS][SP_MAX_COSETS];
+    int nbox_max = 0;
     for (int k = 0; k < in->M; ++k) {
         TileTaps<T>& tp = P.c[k];
         const int t0 = st->tap_start[k], t1 = st->tap_start[k + 1];
         tp.n = t1 - t0;
         if (tp.n < 0 || tp.n > SP_MAX_STENCIL) return pfail(SP_ERR_INVALID, "tap count out of range");
-        int lo[SP_MAX_COSETS][3], hi[SP_MAX_COSETS][3], box_of[SP_MAX_COSETS];
-        for (int s = 0; s < SP_MAX_COSETS; ++s) box_of[s] = -1;
+        int hi[SP_MAX_COSETS][3];
+        for (int s2 = 0; s2 < SP_MAX_COSETS; ++s2) box_of[k][s2] = -1;
         for (int t = 0; t < tp.n; ++t) {
-            const int s = st->src_coset[t0 + t];
-            if (s < 0 || s >= in->M) return pfail(SP_ERR_INVALID, "tap source coset out of range");
+            const int s2 = st->src_coset[t0 + t];
+            if (s2 < 0 || s2 >= in->M) return pfail(SP_ERR_INVALID, "tap source coset out of range");
             const int* dz = st->dz + 3 * (t0 + t);
             for (int i = 0; i < 3; ++i)
                 if (dz[i] < -(1 << 20) || dz[i] > (1 << 20)) return pfail(SP_ERR_INVALID, "tap offset out of range");
-            if (box_of[s] < 0) {
-                box_of[s] = tp.nbox++;
-                for (int i = 0; i < 3; ++i) lo[s][i] = hi[s][i] = dz[i];
+            if (box_of[k][s2] < 0) {
+                box_of[k][s2] = tp.nbox++;
+                for (int i = 0; i < 3; ++i) lo[k][s2][i] = hi[s2][i] = dz[i];
             }
             for (int i = 0; i < 3; ++i) {
-                lo[s][i] = std::min(lo[s][i], dz[i]);
-                hi[s][i] = std::max(hi[s][i], dz[i]);
+                lo[k][s2][i] = std::min(lo[k][s2][i], dz[i]);
+                hi[s2][i] = std::max(hi[s2][i], dz[i]);
             }
         }
-        long long off = 0;
-        for (int s = 0; s < in->M; ++s) {
-            const int b = box_of[s];
+        for (int s2 = 0; s2 < in->M; ++s2) {
+            const int b = box_of[k][s2];
             if (b < 0) continue;
-            tp.box_src[b] = s;
+            tp.box_src[b] = s2;
             const int tile[3] = {1, kTY, kTX};
             for (int i = 0; i < 3; ++i) {
-                tp.box_lo[b][i] = lo[s][i];
-                tp.box_ex[b][i] = tile[i] + hi[s][i] - lo[s][i];
+                tp.box_lo[b][i] = lo[k][s2][i];
+                tp.box_ex[b][i] = tile[i] + hi[s2][i] - lo[k][s2][i];
             }
-            if (tp.box_ex[b][2] > 32 * kChunks)
-                return pfail(SP_ERR_UNSUPPORTED, "prefilter: tap offsets span more than 32 cells along axis 2");
-            tp.box_off[b] = (int)off;
-            off += (long long)tp.box_ex[b][0] * tp.box_ex[b][1] * tp.box_ex[b][2];
-            off = (off + 3) & ~3ll;
-            if (off * (long long)sizeof(T) > 160 * 1024)
-                return pfail(SP_ERR_UNSUPPORTED, "prefilter: tap offsets span too large a box");
+            if (tp.box_ex[b][2] > kTX + 32) return pfail(SP_ERR_UNSUPPORTED, "prefilter: tap offsets span more than 32 cells along axis 2");
         }
-        smem_max = std::max(smem_max, (int)(off * sizeof(T)));
-        for (int t = 0; t < tp.n; ++t) {
-            const int s = st->src_coset[t0 + t];
-            const int b = box_of[s];
-            const int* dz = st->dz + 3 * (t0 + t);
-            tp.tap_box[t] = b;
-            tp.tap_off[t] = tp.box_off[b] + ((dz[0] - lo[s][0]) * tp.box_ex[b][1] + (dz[1] - lo[s][1])) * tp.box_ex[b][2] +
-                            (dz[2] - lo[s][2]);
-            tp.w[t] = (T)st->weight[t0 + t];
-        }
+        nbox_max = std::max(nbox_max, tp.nbox);
         P.out[k] = reinterpret_cast<T*>(out[k]);
     }
-    if (smem_max == 0) {  // no taps anywhere: zero output
+    if (nbox_max == 0) {  // no taps anywhere: zero output
         for (int k = 0; k < in->M; ++k)
             cudaMemsetAsync(out[k], 0, (size_t)(in->extent[k][0] * in->extent[k][1] * in->extent[k][2]) * sizeof(T),
                             stream);
         return SP_OK;
     }
+    // 2. TMA planes when the policy is 'zero' (the TMA unit zero-fills out of range) and every
+    //    coset row is a multiple of 16 bytes (tensor-map strides); else cp.async staging
+    constexpr int kVecE = 16 / (int)sizeof(T);
+    PfEncodeFn enc = pf_encoder();
+    bool use_tma = in->boundary == SP_ZERO && enc != nullptr && in->M * nbox_max <= kMaxMaps;
+    for (int k = 0; k < in->M && use_tma; ++k)
+        if ((in->extent[k][2] * (long long)sizeof(T)) % 16 != 0 || (reinterpret_cast<uintptr_t>(in->data[k]) & 15) != 0)
+            use_tma = false;
+    // 3. ring layout (and, for TMA, 16-byte aligned box columns); TMA boxes are wider (aligned
+    //    columns), so a layout that does not fit falls back to cp.async staging
+    const TileParams<T> P0 = P;
+    if (use_tma) {
+        long long need = 0;
+        for (int k = 0; k < in->M; ++k) {
+            long long off = 0;
+            for (int b = 0; b < P.c[k].nbox; ++b) {
+                const int l2 = P.c[k].box_lo[b][2];
+                const int al = l2 >= 0 ? l2 / kVecE * kVecE : -((-l2 + kVecE - 1) / kVecE) * kVecE;
+                const int ex2 = (P.c[k].box_ex[b][2] + (l2 - al) + kVecE - 1) / kVecE * kVecE;
+                int ring = 1;
+                while (ring < P.c[k].box_ex[b][0] + 1) ring *= 2;
+                off += (long long)ring * ((P.c[k].box_ex[b][1] * ex2 * (int)sizeof(T) + 127) / 128 * 128);
+                if (ex2 > 256 || P.c[k].box_ex[b][1] > 256) need = 1ll << 40;
+            }
+            need = std::max(need, off);
+        }
+        if (need > 160 * 1024) use_tma = false;
+    }
+    P = P0;
+    int smem_max = 0;
+    for (int k = 0; k < in->M; ++k) {
+        TileTaps<T>& tp = P.c[k];
+        long long off = 0;
+        for (int b = 0; b < tp.nbox; ++b) {
+            if (use_tma) {
+                const int l2 = tp.box_lo[b][2];
+                const int al = l2 >= 0 ? l2 / kVecE * kVecE : -((-l2 + kVecE - 1) / kVecE) * kVecE;
+                tp.box_ex[b][2] = (tp.box_ex[b][2] + (l2 - al) + kVecE - 1) / kVecE * kVecE;
+                tp.box_lo[b][2] = al;
+                if (tp.box_ex[b][2] > 256 || tp.box_ex[b][1] > 256) use_tma = false;
+            }
+            tp.ring[b] = 1;
+            while (tp.ring[b] < tp.box_ex[b][0] + 1) tp.ring[b] *= 2;  // >= one plane ahead; slot = plane & (ring-1)
+            const int plane = tp.box_ex[b][1] * tp.box_ex[b][2];
+            tp.slot_elems[b] = (plane * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
+            tp.box_off[b] = (int)off;
+            off += (long long)tp.ring[b] * tp.slot_elems[b];
+        }
+        if (off * (long long)sizeof(T) > 160 * 1024) return pfail(SP_ERR_UNSUPPORTED, "prefilter: tap offsets span too large a box");
+        smem_max = std::max(smem_max, (int)(off * sizeof(T)));
+        const int t0 = st->tap_start[k];
+        for (int t = 0; t < tp.n; ++t) {
+            const int s2 = st->src_coset[t0 + t];
+            const int b = box_of[k][s2];
+            const int* dz = st->dz + 3 * (t0 + t);
+            tp.tap_box[t] = b;
+            tp.tap_dz0[t] = dz[0];
+            tp.tap_off[t] = (dz[1] - tp.box_lo[b][1]) * tp.box_ex[b][2] + (dz[2] - tp.box_lo[b][2]);
+            tp.w[t] = (T)st->weight[t0 + t];
+        }
+    }
+    PfMaps maps{};
+    maps.nbox_max = nbox_max;
+    if (use_tma) {
+        for (int k = 0; k < in->M && use_tma; ++k) {
+            const TileTaps<T>& tp = P.c[k];
+            unsigned bytes = 0;
+            for (int b = 0; b < tp.nbox; ++b) {
+                const int src = tp.box_src[b];
+                const cuuint64_t dims[3] = {(cuuint64_t)in->extent[src][2], (cuuint64_t)in->extent[src][1],
+                                            (cuuint64_t)in->extent[src][0]};
+                const cuuint64_t strides[2] = {(cuuint64_t)(in->extent[src][2] * sizeof(T)),
+                                               (cuuint64_t)(in->extent[src][2] * in->extent[src][1] * sizeof(T))};
+                const cuuint32_t box[3] = {(cuuint32_t)tp.box_ex[b][2], (cuuint32_t)tp.box_ex[b][1], 1u};
+                const cuuint32_t estr[3] = {1, 1, 1};
+                if (enc(&maps.m[k * nbox_max + b], sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                        3, const_cast<void*>(in->data[src]), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                    use_tma = false;
+                bytes += (unsigned)(tp.box_ex[b][1] * tp.box_ex[b][2] * (int)sizeof(T));
+            }
+            maps.set_bytes[k] = bytes;
+        }
+    }
     int nt = P.c[0].n;
     for (int k = 1; k < in->M; ++k)
         if (P.c[k].n != nt) nt = 0;
     const dim3 grid((unsigned)((max_e[2] + kTX - 1) / kTX), (unsigned)((max_e[1] + kTY - 1) / kTY),
-                    (unsigned)(max_e[0] * in->M));
+                    (unsigned)((max_e[0] + kZChunk - 1) / kZChunk * in->M));
     cudaError_t e = cudaSuccess;
+    auto launch = [&](auto kern) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        if (e == cudaSuccess) kern<<<grid, kThreadsPF, smem_max, stream>>>(g, P, maps);
+    };
     switch (nt) {
-#define SP_PF_CASE(N)                                                                                      \
-    case N:                                                                                                \
-        e = cudaFuncSetAttribute(prefilter_tiled<T, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024); \
-        if (e == cudaSuccess) prefilter_tiled<T, N><<<grid, kThreadsPF, smem_max, stream>>>(g, P);        \
+#define SP_PF_CASE(N)                                                                  \
+    case N:                                                                            \
+        if (use_tma) launch(prefilter_zmarch<T, N, true>);                             \
+        else launch(prefilter_zmarch<T, N, false>);                                    \
         break;
         SP_PF_CASE(1) SP_PF_CASE(2) SP_PF_CASE(3) SP_PF_CASE(4) SP_PF_CASE(5) SP_PF_CASE(7) SP_PF_CASE(9)
         SP_PF_CASE(27)
         default:
-            e = cudaFuncSetAttribute(prefilter_tiled<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-            if (e == cudaSuccess) prefilter_tiled<T, 0><<<grid, kThreadsPF, smem_max, stream>>>(g, P);
+            if (use_tma) launch(prefilter_zmarch<T, 0, true>);
+            else launch(prefilter_zmarch<T, 0, false>);
             break;
 #undef SP_PF_CASE
     }
