@@ -185,7 +185,7 @@ def onchip_roofline(plan, esize, pts_per_s, sm_mhz):
             "achieved": pts_per_s * per_pt / 1e12, "peak": peak / 1e12, "frac": pts_per_s * per_pt / peak}
 
 
-def bench_prefilter(args, device, rank, stream, dist, peak):
+def bench_prefilter(args, device, rank, stream, dist, peak, hi=811):
     """the quasi-interpolation prefilter of the BCC quintic spline
     (9 taps, corpus.py:71-82) over the C5 grid (BCC 2x406^3, fp32, 535 MB > L2).  Streaming
     stencil: algorithmic HBM bytes = one read + one write of every coset sample."""
@@ -196,7 +196,7 @@ def bench_prefilter(args, device, rank, stream, dist, peak):
     from paper_2102_08514_b200.runtime import CoefficientGrid
 
     _, cos = corpus.lattice_of("bcc_quintic_rd")
-    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [811, 811, 811], device=device, dtype=torch.float32)
+    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [hi, hi, hi], device=device, dtype=torch.float32)
     gen = torch.Generator(device=device).manual_seed(2102_08514 + 31 * rank)
     for a in grid.arrays:
         a.copy_(torch.rand(a.shape, generator=gen, device=device))
@@ -205,7 +205,9 @@ def bench_prefilter(args, device, rank, stream, dist, peak):
     ms = measure(lambda: apply_prefilter(grid, taps, out=out), max(3, min(args.steps, 50)), args.warmup, stream, dist)
     nbytes = 2 * grid.nbytes()
     gbs = nbytes / (ms * 1e-3) / 1e9
-    return {"workload": "bcc_quintic_rd prefilter (9 taps) on BCC 2x406^3 fp32, zero policy",
+    n = (hi + 1) // 2
+    return {"workload": f"bcc_quintic_rd prefilter (9 taps) on BCC 2x{n}^3 fp32, zero policy",
+            "staging": "TMA planes (16-byte coset rows)" if (n * 4) % 16 == 0 else "cp.async (rows not 16-byte multiples)",
             "value": gbs, "unit": "GB/s", "ms_per_step": ms, "samples": grid.site_count(),
             "algorithmic_bytes_per_step": nbytes, "roofline_hbm_frac": gbs / peak,
             "l2": "input and output 535 MB each > 126 MB L2"}
@@ -560,6 +562,7 @@ def run_ours(args):
             torch.cuda.empty_cache()
         line["workloads"] = others
         line["prefilter"] = bench_prefilter(args, device, rank, stream, dist, peak)
+        line["prefilter_tma"] = bench_prefilter(args, device, rank, stream, dist, peak, hi=1023)
         line["render"] = bench_render(args, device)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -36,6 +36,7 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 // sum_t w_t * box[t][...] with the tap's box offset precomputed on the host: one LDS, one
 // multiply, one add per tap, separate roundings, taps in the given order.
 constexpr int kTX = 128, kTY = 16, kThreadsPF = 256, kZChunk = 32;
+constexpr int kAhead = 1;  // prefetch depth: planes staged ahead of the step being computed (2 measured no faster)
 
 template <typename T>
 struct TileTaps {             // one output coset
@@ -47,9 +48,11 @@ struct TileTaps {             // one output coset
     int box_off[SP_MAX_COSETS];     // smem element offset of the box's plane ring
     int ring[SP_MAX_COSETS];        // planes in the ring: power of two >= box_ex[0] + 1 (one prefetched ahead)
     int slot_elems[SP_MAX_COSETS];  // ring slot stride (elements; 128-byte multiple)
+    int pitch[SP_MAX_COSETS];       // staged row pitch (elements)
     int tap_box[SP_MAX_STENCIL];
     int tap_dz0[SP_MAX_STENCIL];    // plane offset of the tap
     int tap_off[SP_MAX_STENCIL];    // in-plane offset of (dz1 - lo1, dz2 - lo2)
+    int tap_row[SP_MAX_STENCIL];    // dz1 - lo1
     T w[SP_MAX_STENCIL];
 };
 
@@ -84,10 +87,34 @@ __device__ __forceinline__ long long policy_index(const sp::GridArgs<T>& g, int 
     return ((long long)a0 * e1 + a1) * e2 + a2;
 }
 
+// Staging modes of the z-marching kernel.
+//   kCpAsync: every thread copies its share of a plane element by element (cp.async, boundary
+//             policy folded into the source index) — any grid, any policy.
+//   kTmaPlane: one thread copies whole box planes with a 3-D tensor map (TMA zero-fills out
+//             of range = the 'zero' policy) — coset rows that are 16-byte multiples.
+//   kBulkRow: box planes fully inside the array are copied row by row with 1-D bulk copies
+//             (cp.async.bulk: the 16-byte aligned span around each row; the row's data then
+//             starts at a per-row phase), other planes element by element at the same phase —
+//             any row length whose phase is the same for rows two apart (fp32: even rows).
+enum PfMode { kCpAsync = 0, kTmaPlane = 1, kBulkRow = 2 };
+
+// element phase of the 16-byte aligned copy of the row starting at element e (array base
+// 16-byte aligned): 0 except in kBulkRow mode
+// (for the row of plane p, row y, starting at column x of an e1 x e2 coset array: only the
+// low bits of its linear element index matter, so 32-bit unsigned wrap-around is exact)
+template <typename T, int kMode>
+__device__ __forceinline__ int row_phase(int p, int y, int x, int e1, int e2) {
+    if constexpr (kMode == kBulkRow) {
+        constexpr unsigned V = 16 / sizeof(T);
+        return (int)((((unsigned)p * (unsigned)e1 + (unsigned)y) * (unsigned)e2 + (unsigned)x) & (V - 1));
+    }
+    return 0;
+}
+
 // Copy plane `p` (coset-cell index along axis 0) of box b's rows [y0 + lo1, ...) x
 // [x0 + lo2, ...) into ring slot `slot` with cp.async (4 / 8-byte elements, zero-filled for the
 // 'zero' policy outside the array, clamp / mirror indices otherwise): warp per row.
-template <typename T>
+template <typename T, int kMode>
 __device__ __forceinline__ void stage_plane(const sp::GridArgs<T>& g, const TileTaps<T>& tp, int b, int p, int slot,
                                             int y0, int x0, int hv, int wv, T* sm, int lane, int warp) {
     const int s = tp.box_src[b];
@@ -99,9 +126,10 @@ __device__ __forceinline__ void stage_plane(const sp::GridArgs<T>& g, const Tile
     const int e0 = g.ext[s][0], e1 = g.ext[s][1], e2 = g.ext[s][2];
     const bool inside = p >= 0 && p < e0 && s1 >= 0 && s2 >= 0 && s1 + ex1c <= e1 && s2 + ex2c <= e2;
     for (int i1 = warp; i1 < ex1c; i1 += kThreadsPF / 32) {
-        T* drow = dst + i1 * ex2;
+        const long long row = ((long long)p * e1 + (s1 + i1)) * e2 + s2;
+        T* drow = dst + i1 * tp.pitch[b] + row_phase<T, kMode>(p, s1 + i1, s2, e1, e2);
         if (inside) {
-            const T* rp = src + ((long long)p * e1 + (s1 + i1)) * e2 + s2;
+            const T* rp = src + row;
             for (int c = lane; c < ex2c; c += 32) sp::cp_async_elem<sizeof(T)>(drow + c, rp + c, (int)sizeof(T));
         } else {
             for (int c = lane; c < ex2c; c += 32) {
@@ -113,12 +141,30 @@ __device__ __forceinline__ void stage_plane(const sp::GridArgs<T>& g, const Tile
     }
 }
 
-// z-marching kernel.  One block = an output tile of kTX (z2) x kTY (z1) samples of output
-// coset k, marching over kZChunk planes z0: each source box keeps a ring of box_ex[0] + 1
-// staged planes, so every input plane is copied into shared memory once per tile column
-// (cp.async, one plane ahead of the computation) instead of once per output plane.  Each
-// output is sum_t w_t * box[t][...] — one LDS, one multiply, one add per tap, separate
-// roundings, taps in the given order (bit-identical to a per-site loop over site_value).
+// kBulkRow: can box b's plane p be bulk-copied (fully inside, not touching the array's last row)?
+template <typename T>
+__device__ __forceinline__ bool bulk_ok(const sp::GridArgs<T>& g, const TileTaps<T>& tp, int b, int p, int y0, int x0) {
+    const int s = tp.box_src[b];
+    const int e0 = g.ext[s][0], e1 = g.ext[s][1], e2 = g.ext[s][2];
+    const int s1 = y0 + tp.box_lo[b][1], s2 = x0 + tp.box_lo[b][2];
+    return p >= 0 && p < e0 && s1 >= 0 && s2 >= 0 && s1 + tp.box_ex[b][1] <= e1 && s2 + tp.box_ex[b][2] <= e2 &&
+           !(p == e0 - 1 && s1 + tp.box_ex[b][1] == e1);
+}
+
+template <typename T>
+__device__ __forceinline__ unsigned bulk_row_bytes(long long row, int ex2) {
+    const unsigned long long a = (unsigned long long)row * sizeof(T);
+    return (unsigned)(((a + (unsigned long long)ex2 * sizeof(T) + 15) & ~15ull) - (a & ~15ull));
+}
+
+__device__ __forceinline__ void pf_bulk_row(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+
 // Tensor maps of the TMA variant: one per (output coset, source box), box = one plane of the
 // source box (rows x 16-byte aligned columns); out-of-range texels are zero-filled by the TMA
 // unit, which is the 'zero' policy.
@@ -154,12 +200,20 @@ __device__ __forceinline__ void pf_tma_plane(void* dst, const CUtensorMap* map, 
         : "memory");
 }
 
-template <typename T, int NT, bool kTma>
+// z-marching kernel.  One block = an output tile of kTX (z2) x kTY (z1) samples of output
+// coset k, marching over kZChunk planes z0: each source box keeps a ring of box_ex[0] + 1 (or
+// more: a power of two) staged planes, so every input plane is copied into shared memory
+// once per tile column, one plane ahead of the computation, instead of once per output
+// plane.  Each output is sum_t w_t * box[t][...] — one LDS, one multiply, one add per tap,
+// separate roundings, taps in the given order (bit-identical to a per-site loop over
+// site_value).
+template <typename T, int NT, int kMode>
 __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArgs<T> g, const TileParams<T> P,
                                                                const __grid_constant__ PfMaps maps) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* sm = reinterpret_cast<T*>(smem_raw);
     __shared__ __align__(8) unsigned long long mbar[2];
+    constexpr bool kAsyncBar = kMode != kCpAsync;  // mbarrier-tracked copies
     const int k = blockIdx.z % g.M;
     const int zc = blockIdx.z / g.M;
     const TileTaps<T>& tp = P.c[k];
@@ -170,13 +224,7 @@ __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArg
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wv = min(kTX, e2 - x0), hv = min(kTY, e1 - y0);
     auto slot_of = [&](int b, int p) { return p & (tp.ring[b] - 1); };  // ring sizes are powers of two
-    // TMA: one elected thread copies whole box planes (mbarrier complete_tx), set i of planes on
-    // mbar[i & 1]; cp.async: every thread copies its share, one commit group per set
-    auto issue_tma = [&](int b, int p, unsigned long long* bar) {
-        pf_tma_plane(sm + tp.box_off[b] + slot_of(b, p) * tp.slot_elems[b], &maps.m[k * maps.nbox_max + b], bar,
-                     x0 + tp.box_lo[b][2], y0 + tp.box_lo[b][1], p);
-    };
-    if constexpr (kTma) {
+    if constexpr (kAsyncBar) {
         if (tid == 0) {
             pf_mbar_init(&mbar[0]);
             pf_mbar_init(&mbar[1]);
@@ -184,47 +232,98 @@ __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArg
         }
         __syncthreads();
     }
-    // prologue: planes za + lo0 .. za + hi0 of every box
-    if constexpr (kTma) {
-        if (tid == 0) {
-            unsigned bytes = 0;
-            for (int b = 0; b < tp.nbox; ++b) bytes += (unsigned)tp.box_ex[b][0] * (unsigned)(tp.box_ex[b][1] * tp.box_ex[b][2] * (int)sizeof(T));
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            pf_mbar_expect(&mbar[0], bytes);
+    // stage one set of planes: plane p(b) of every box b, tracked by `bar`
+    auto stage_set = [&](auto plane_of, int nplanes, unsigned long long* bar) {
+        if constexpr (kMode == kCpAsync) {
             for (int b = 0; b < tp.nbox; ++b)
-                for (int i0 = 0; i0 < tp.box_ex[b][0]; ++i0) issue_tma(b, za + tp.box_lo[b][0] + i0, &mbar[0]);
-        }
-    } else {
-        for (int b = 0; b < tp.nbox; ++b)
-            for (int i0 = 0; i0 < tp.box_ex[b][0]; ++i0) {
-                const int p = za + tp.box_lo[b][0] + i0;
-                stage_plane(g, tp, b, p, slot_of(b, p), y0, x0, hv, wv, sm, lane, warp);
+                for (int i = 0; i < nplanes; ++i) {
+                    const int p = plane_of(b, i);
+                    if (p != INT_MIN) stage_plane<T, kMode>(g, tp, b, p, slot_of(b, p), y0, x0, hv, wv, sm, lane, warp);
+                }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        } else if constexpr (kMode == kTmaPlane) {
+            if (tid == 0) {
+                unsigned bytes = 0;
+                for (int b = 0; b < tp.nbox; ++b)
+                    for (int i = 0; i < nplanes; ++i)
+                        if (plane_of(b, i) != INT_MIN) bytes += (unsigned)(tp.box_ex[b][1] * tp.box_ex[b][2] * (int)sizeof(T));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                pf_mbar_expect(bar, bytes);
+                for (int b = 0; b < tp.nbox; ++b)
+                    for (int i = 0; i < nplanes; ++i) {
+                        const int p = plane_of(b, i);
+                        if (p != INT_MIN)
+                            pf_tma_plane(sm + tp.box_off[b] + slot_of(b, p) * tp.slot_elems[b],
+                                         &maps.m[k * maps.nbox_max + b], bar, x0 + tp.box_lo[b][2], y0 + tp.box_lo[b][1], p);
+                    }
             }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        } else {  // kBulkRow: warp 0 bulk-copies the rows of inside planes, everyone else element-copies
+            if (warp == 0) {
+                unsigned bytes = 0;  // this lane's rows, then summed over the warp
+                for (int b = 0; b < tp.nbox; ++b)
+                    for (int i = 0; i < nplanes; ++i) {
+                        const int p = plane_of(b, i);
+                        if (p == INT_MIN || !bulk_ok(g, tp, b, p, y0, x0)) continue;
+                        const int s = tp.box_src[b];
+                        for (int r = lane; r < tp.box_ex[b][1]; r += 32) {
+                            const long long row =
+                                ((long long)p * g.ext[s][1] + (y0 + tp.box_lo[b][1] + r)) * g.ext[s][2] + x0 + tp.box_lo[b][2];
+                            bytes += bulk_row_bytes<T>(row, tp.box_ex[b][2]);
+                        }
+                    }
+                bytes = __reduce_add_sync(0xffffffffu, bytes);
+                if (lane == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    pf_mbar_expect(bar, bytes);
+                }
+                __syncwarp();
+                for (int b = 0; b < tp.nbox; ++b)
+                    for (int i = 0; i < nplanes; ++i) {
+                        const int p = plane_of(b, i);
+                        if (p == INT_MIN || !bulk_ok(g, tp, b, p, y0, x0)) continue;
+                        const int s = tp.box_src[b];
+                        T* dst = sm + tp.box_off[b] + slot_of(b, p) * tp.slot_elems[b];
+                        for (int r = lane; r < tp.box_ex[b][1]; r += 32) {
+                            const long long row =
+                                ((long long)p * g.ext[s][1] + (y0 + tp.box_lo[b][1] + r)) * g.ext[s][2] + x0 + tp.box_lo[b][2];
+                            const T* sp_ = g.data[s] + row;
+                            pf_bulk_row(dst + r * tp.pitch[b], reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(sp_) & ~(uintptr_t)15),
+                                        bulk_row_bytes<T>(row, tp.box_ex[b][2]), bar);
+                        }
+                    }
+            }
+            for (int b = 0; b < tp.nbox; ++b)
+                for (int i = 0; i < nplanes; ++i) {
+                    const int p = plane_of(b, i);
+                    if (p != INT_MIN && !bulk_ok(g, tp, b, p, y0, x0))
+                        stage_plane<T, kMode>(g, tp, b, p, slot_of(b, p), y0, x0, hv, wv, sm, lane, warp);
+                }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        }
+    };
+    // prologue: set 0 = planes za + lo0 .. za + hi0 of every box (mbar[0]); set a < kAhead = the
+    // plane step za + a adds; set i + kAhead is issued during step i (mbar[(i + kAhead) & 1])
+    int maxex0 = 0;
+    for (int b = 0; b < tp.nbox; ++b) maxex0 = max(maxex0, tp.box_ex[b][0]);
+    stage_set([&](int b, int i) { return i < tp.box_ex[b][0] ? za + tp.box_lo[b][0] + i : INT_MIN; }, maxex0, &mbar[0]);
+    for (int a = 1; a < kAhead; ++a) {
+        if (za + a < zb) stage_set([&](int b, int) { return za + a + tp.box_lo[b][0] + tp.box_ex[b][0] - 1; }, 1, &mbar[a & 1]);
+        else if constexpr (kMode != kTmaPlane) asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
     const int tx = tid % kTX, ty = tid / kTX;
     constexpr int kRowsPerThread = kTY / (kThreadsPF / kTX);
     const bool col_ok = x0 + tx < e2;
     for (int z0 = za; z0 < zb; ++z0) {
         const int it = z0 - za;
-        if constexpr (kTma) {
-            if (tid == 0 && z0 + 1 < zb) {  // prefetch the one new plane per box the next output plane needs
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                pf_mbar_expect(&mbar[(it + 1) & 1], maps.set_bytes[k]);
-                for (int b = 0; b < tp.nbox; ++b)
-                    issue_tma(b, z0 + 1 + tp.box_lo[b][0] + tp.box_ex[b][0] - 1, &mbar[(it + 1) & 1]);
-            }
-            pf_mbar_wait(&mbar[it & 1], (unsigned)(it >> 1) & 1u);
-        } else {
-            if (z0 + 1 < zb)  // prefetch the one new plane per box the next output plane needs
-                for (int b = 0; b < tp.nbox; ++b) {
-                    const int p = z0 + 1 + tp.box_lo[b][0] + tp.box_ex[b][0] - 1;
-                    stage_plane(g, tp, b, p, slot_of(b, p), y0, x0, hv, wv, sm, lane, warp);
-                }
+        if constexpr (kMode != kTmaPlane) asm volatile("cp.async.wait_group %0;\n" ::"n"(kAhead - 1) : "memory");
+        if constexpr (kAsyncBar) pf_mbar_wait(&mbar[it & 1], (unsigned)(it >> 1) & 1u);
+        __syncthreads();  // set it landed for every thread; every thread is past step it - 1
+        // prefetch set it + kAhead (the plane per box that step adds) into the slot step it - 1 read
+        if (z0 + kAhead < zb)
+            stage_set([&](int b, int) { return z0 + kAhead + tp.box_lo[b][0] + tp.box_ex[b][0] - 1; }, 1,
+                      &mbar[(it + kAhead) & 1]);
+        else if constexpr (kMode != kTmaPlane)
             asm volatile("cp.async.commit_group;\n" ::: "memory");
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-            __syncthreads();
-        }
         if (col_ok) {
             T* out = P.out[k] + ((long long)z0 * e1 + y0) * e2 + x0 + tx;
             if constexpr (NT > 0) {
@@ -233,9 +332,13 @@ __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArg
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
                     const int b = tp.tap_box[t];
-                    pitch[t] = tp.box_ex[b][2];
+                    const int s = tp.box_src[b];
+                    pitch[t] = tp.pitch[b];
+                    // rows ty, ty + 2, ... share the copy phase (kBulkRow requirement)
+                    const int ph = row_phase<T, kMode>(z0 + tp.tap_dz0[t], y0 + tp.box_lo[b][1] + ty + tp.tap_row[t],
+                                                       x0 + tp.box_lo[b][2], g.ext[s][1], g.ext[s][2]);
                     base[t] = tp.box_off[b] + slot_of(b, z0 + tp.tap_dz0[t]) * tp.slot_elems[b] + tp.tap_off[t] +
-                              ty * pitch[t] + tx;
+                              ty * pitch[t] + tx + ph;
                     w[t] = tp.w[t];
                 }
 #pragma unroll
@@ -255,16 +358,18 @@ __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArg
                     T acc = T(0);
                     for (int t = 0; t < tp.n; ++t) {
                         const int b = tp.tap_box[t];
+                        const int s = tp.box_src[b];
+                        const int ph = row_phase<T, kMode>(z0 + tp.tap_dz0[t], y0 + tp.box_lo[b][1] + r + tp.tap_row[t],
+                                                           x0 + tp.box_lo[b][2], g.ext[s][1], g.ext[s][2]);
                         const int pl = tp.box_off[b] + slot_of(b, z0 + tp.tap_dz0[t]) * tp.slot_elems[b];
-                        acc = add_rn(acc, mul_rn(tp.w[t], sm[pl + tp.tap_off[t] + r * tp.box_ex[b][2] + tx]));
+                        acc = add_rn(acc, mul_rn(tp.w[t], sm[pl + tp.tap_off[t] + r * tp.pitch[b] + tx + ph]));
                     }
                     out[(long long)r * e2] = acc;
                 }
             }
         }
-        __syncthreads();  // the slot read now is refilled by the next step's prefetch
     }
-    if constexpr (!kTma) asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if constexpr (kMode != kTmaPlane) asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 int pfail(int code, const std::string& msg) {
@@ -355,67 +460,71 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
                             stream);
         return SP_OK;
     }
-    // 2. TMA planes when the policy is 'zero' (the TMA unit zero-fills out of range) and every
-    //    coset row is a multiple of 16 bytes (tensor-map strides); else cp.async staging
+    // 2. staging mode: TMA planes when the policy is 'zero' (the TMA unit zero-fills out of
+    //    range) and every coset row is a multiple of 16 bytes (tensor-map strides); 1-D bulk row
+    //    copies when rows two apart share their 16-byte phase; else element-wise cp.async.
+    //    Each mode's ring layout must fit shared memory, else the next mode is tried.
     constexpr int kVecE = 16 / (int)sizeof(T);
     PfEncodeFn enc = pf_encoder();
-    bool use_tma = in->boundary == SP_ZERO && enc != nullptr && in->M * nbox_max <= kMaxMaps;
-    for (int k = 0; k < in->M && use_tma; ++k)
-        if ((in->extent[k][2] * (long long)sizeof(T)) % 16 != 0 || (reinterpret_cast<uintptr_t>(in->data[k]) & 15) != 0)
-            use_tma = false;
-    // 3. ring layout (and, for TMA, 16-byte aligned box columns); TMA boxes are wider (aligned
-    //    columns), so a layout that does not fit falls back to cp.async staging
+    bool aligned16 = true, phase2 = true;
+    for (int k = 0; k < in->M; ++k) {
+        aligned16 &= (in->extent[k][2] * (long long)sizeof(T)) % 16 == 0;
+        phase2 &= (2 * in->extent[k][2] * (long long)sizeof(T)) % 16 == 0;
+        if ((reinterpret_cast<uintptr_t>(in->data[k]) & 15) != 0) aligned16 = phase2 = false;
+    }
     const TileParams<T> P0 = P;
-    if (use_tma) {
+    // lay out mode `m` into P; returns the shared-memory bytes, or -1 if the mode does not apply
+    auto layout = [&](int m) -> long long {
+        P = P0;
         long long need = 0;
         for (int k = 0; k < in->M; ++k) {
+            TileTaps<T>& tp = P.c[k];
             long long off = 0;
-            for (int b = 0; b < P.c[k].nbox; ++b) {
-                const int l2 = P.c[k].box_lo[b][2];
-                const int al = l2 >= 0 ? l2 / kVecE * kVecE : -((-l2 + kVecE - 1) / kVecE) * kVecE;
-                const int ex2 = (P.c[k].box_ex[b][2] + (l2 - al) + kVecE - 1) / kVecE * kVecE;
-                int ring = 1;
-                while (ring < P.c[k].box_ex[b][0] + 1) ring *= 2;
-                off += (long long)ring * ((P.c[k].box_ex[b][1] * ex2 * (int)sizeof(T) + 127) / 128 * 128);
-                if (ex2 > 256 || P.c[k].box_ex[b][1] > 256) need = 1ll << 40;
+            for (int b = 0; b < tp.nbox; ++b) {
+                if (m == kTmaPlane) {  // 16-byte aligned box columns
+                    const int l2 = tp.box_lo[b][2];
+                    const int al = l2 >= 0 ? l2 / kVecE * kVecE : -((-l2 + kVecE - 1) / kVecE) * kVecE;
+                    tp.box_ex[b][2] = (tp.box_ex[b][2] + (l2 - al) + kVecE - 1) / kVecE * kVecE;
+                    tp.box_lo[b][2] = al;
+                    if (tp.box_ex[b][2] > 256 || tp.box_ex[b][1] > 256) return -1;
+                }
+                // bulk rows: the aligned span around a row is up to 2 vectors longer than the row
+                tp.pitch[b] = m == kBulkRow ? (tp.box_ex[b][2] + 2 * kVecE + kVecE - 1) / kVecE * kVecE : tp.box_ex[b][2];
+                tp.ring[b] = 1;
+                while (tp.ring[b] < tp.box_ex[b][0] + kAhead) tp.ring[b] *= 2;  // kAhead planes ahead; slot = plane & (ring-1)
+                const int plane = tp.box_ex[b][1] * tp.pitch[b];
+                tp.slot_elems[b] = (plane * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
+                tp.box_off[b] = (int)off;
+                off += (long long)tp.ring[b] * tp.slot_elems[b];
             }
-            need = std::max(need, off);
-        }
-        if (need > 160 * 1024) use_tma = false;
-    }
-    P = P0;
-    int smem_max = 0;
-    for (int k = 0; k < in->M; ++k) {
-        TileTaps<T>& tp = P.c[k];
-        long long off = 0;
-        for (int b = 0; b < tp.nbox; ++b) {
-            if (use_tma) {
-                const int l2 = tp.box_lo[b][2];
-                const int al = l2 >= 0 ? l2 / kVecE * kVecE : -((-l2 + kVecE - 1) / kVecE) * kVecE;
-                tp.box_ex[b][2] = (tp.box_ex[b][2] + (l2 - al) + kVecE - 1) / kVecE * kVecE;
-                tp.box_lo[b][2] = al;
-                if (tp.box_ex[b][2] > 256 || tp.box_ex[b][1] > 256) use_tma = false;
+            need = std::max(need, off * (long long)sizeof(T));
+            const int t0 = st->tap_start[k];
+            for (int t = 0; t < tp.n; ++t) {
+                const int s2 = st->src_coset[t0 + t];
+                const int bx = box_of[k][s2];
+                const int* dz = st->dz + 3 * (t0 + t);
+                tp.tap_box[t] = bx;
+                tp.tap_dz0[t] = dz[0];
+                tp.tap_off[t] = (dz[1] - tp.box_lo[bx][1]) * tp.pitch[bx] + (dz[2] - tp.box_lo[bx][2]);
+                tp.tap_row[t] = dz[1] - tp.box_lo[bx][1];
+                tp.w[t] = (T)st->weight[t0 + t];
             }
-            tp.ring[b] = 1;
-            while (tp.ring[b] < tp.box_ex[b][0] + 1) tp.ring[b] *= 2;  // >= one plane ahead; slot = plane & (ring-1)
-            const int plane = tp.box_ex[b][1] * tp.box_ex[b][2];
-            tp.slot_elems[b] = (plane * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
-            tp.box_off[b] = (int)off;
-            off += (long long)tp.ring[b] * tp.slot_elems[b];
         }
-        if (off * (long long)sizeof(T) > 160 * 1024) return pfail(SP_ERR_UNSUPPORTED, "prefilter: tap offsets span too large a box");
-        smem_max = std::max(smem_max, (int)(off * sizeof(T)));
-        const int t0 = st->tap_start[k];
-        for (int t = 0; t < tp.n; ++t) {
-            const int s2 = st->src_coset[t0 + t];
-            const int b = box_of[k][s2];
-            const int* dz = st->dz + 3 * (t0 + t);
-            tp.tap_box[t] = b;
-            tp.tap_dz0[t] = dz[0];
-            tp.tap_off[t] = (dz[1] - tp.box_lo[b][1]) * tp.box_ex[b][2] + (dz[2] - tp.box_lo[b][2]);
-            tp.w[t] = (T)st->weight[t0 + t];
-        }
-    }
+        return need <= 160 * 1024 ? need : -1;
+    };
+    int mode = -1;
+    long long smem_need = -1;
+    if (in->boundary == SP_ZERO && enc != nullptr && in->M * nbox_max <= kMaxMaps && aligned16 &&
+        (smem_need = layout(kTmaPlane)) >= 0)
+        mode = kTmaPlane;
+    // kBulkRow measured slower than element-wise cp.async on the C5 grid (BCC 2x406^3 fp32: 1.02
+    // vs 0.78 ms: 34 small row copies per plane set, edge tiles staged element-wise); opt-in
+    const char* bulk_env = getenv("SP_PF_BULK");
+    const bool bulk_ok_mode = phase2 && bulk_env && atoi(bulk_env) != 0;
+    if (mode < 0 && bulk_ok_mode && (smem_need = layout(kBulkRow)) >= 0) mode = kBulkRow;
+    if (mode < 0 && (smem_need = layout(kCpAsync)) >= 0) mode = kCpAsync;
+    if (mode < 0) return pfail(SP_ERR_UNSUPPORTED, "prefilter: tap offsets span too large a box");
+    bool use_tma = mode == kTmaPlane;
     PfMaps maps{};
     maps.nbox_max = nbox_max;
     if (use_tma) {
@@ -440,6 +549,13 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
             maps.set_bytes[k] = bytes;
         }
     }
+    if (mode == kTmaPlane && !use_tma) {  // tensor-map encoding refused: next mode
+        mode = -1;
+        if (bulk_ok_mode && (smem_need = layout(kBulkRow)) >= 0) mode = kBulkRow;
+        if (mode < 0 && (smem_need = layout(kCpAsync)) >= 0) mode = kCpAsync;
+        if (mode < 0) return pfail(SP_ERR_UNSUPPORTED, "prefilter: tap offsets span too large a box");
+    }
+    const int smem_bytes = (int)smem_need;
     int nt = P.c[0].n;
     for (int k = 1; k < in->M; ++k)
         if (P.c[k].n != nt) nt = 0;
@@ -448,19 +564,21 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
     cudaError_t e = cudaSuccess;
     auto launch = [&](auto kern) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        if (e == cudaSuccess) kern<<<grid, kThreadsPF, smem_max, stream>>>(g, P, maps);
+        if (e == cudaSuccess) kern<<<grid, kThreadsPF, smem_bytes, stream>>>(g, P, maps);
     };
     switch (nt) {
 #define SP_PF_CASE(N)                                                                  \
     case N:                                                                            \
-        if (use_tma) launch(prefilter_zmarch<T, N, true>);                             \
-        else launch(prefilter_zmarch<T, N, false>);                                    \
+        if (mode == kTmaPlane) launch(prefilter_zmarch<T, N, kTmaPlane>);              \
+        else if (mode == kBulkRow) launch(prefilter_zmarch<T, N, kBulkRow>);           \
+        else launch(prefilter_zmarch<T, N, kCpAsync>);                                 \
         break;
         SP_PF_CASE(1) SP_PF_CASE(2) SP_PF_CASE(3) SP_PF_CASE(4) SP_PF_CASE(5) SP_PF_CASE(7) SP_PF_CASE(9)
         SP_PF_CASE(27)
         default:
-            if (use_tma) launch(prefilter_zmarch<T, 0, true>);
-            else launch(prefilter_zmarch<T, 0, false>);
+            if (mode == kTmaPlane) launch(prefilter_zmarch<T, 0, kTmaPlane>);
+            else if (mode == kBulkRow) launch(prefilter_zmarch<T, 0, kBulkRow>);
+            else launch(prefilter_zmarch<T, 0, kCpAsync>);
             break;
 #undef SP_PF_CASE
     }

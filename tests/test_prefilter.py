@@ -118,9 +118,11 @@ def test_gpu_prefilter_properties_at_scale(cuda):
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("boundary", ["zero", "clamp"])
-def test_tma_and_cpasync_staging_agree_with_oracle(dtype, boundary, cuda):
+@pytest.mark.parametrize("hi2", [255, 251, 253])  # coset rows of 128 (TMA / bulk), 126 (bulk), 127 (cp.async fp32)
+def test_tma_and_cpasync_staging_agree_with_oracle(dtype, boundary, hi2, cuda):
     """Coset rows that are a multiple of 16 bytes with the 'zero' policy take the TMA plane
-    path (zero-filled out of range), everything else the cp.async path; both equal the
+    path (zero-filled out of range), rows whose 16-byte phase repeats every two rows the
+    bulk-row path, everything else element-wise cp.async; all equal the
     oracle's per-site correlation (float64: bit for bit) on a BCC grid with tiles spanning
     several z chunks and partial edge tiles."""
     import numpy as np
@@ -129,11 +131,10 @@ def test_tma_and_cpasync_staging_agree_with_oracle(dtype, boundary, cuda):
     from paper_2102_08514_b200.runtime import CoefficientGrid
 
     _, cos = corpus.lattice_of("bcc_quintic_rd")
-    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [141, 77, 255], boundary=boundary, device=cuda, dtype=dtype)
+    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [141, 77, hi2], boundary=boundary, device=cuda, dtype=dtype)
     rng = np.random.default_rng(12)
     for a in grid.arrays:
         a.copy_(torch.from_numpy(rng.random(tuple(a.shape))))
-    assert grid.arrays[0].shape[2] * grid.arrays[0].element_size() % 16 == 0
     taps = corpus.prefilter_taps("bcc_quintic_rd")
     got = [a.double().cpu().numpy() for a in apply_prefilter(grid, taps).arrays]
     ng = NumpyGrid(cos.diag, cos.shifts, [a.double().cpu().numpy() for a in grid.arrays], grid.origins, boundary)
