@@ -210,7 +210,7 @@ def bench_prefilter(args, device, rank, stream, dist, peak, hi=811):
             "staging": "TMA planes (16-byte coset rows)" if (n * 4) % 16 == 0 else "cp.async (rows not 16-byte multiples)",
             "value": gbs, "unit": "GB/s", "ms_per_step": ms, "samples": grid.site_count(),
             "algorithmic_bytes_per_step": nbytes, "roofline_hbm_frac": gbs / peak,
-            "l2": "input and output 535 MB each > 126 MB L2"}
+            "l2": f"input and output {grid.nbytes() / 1e6:.0f} MB each > 126 MB L2"}
 
 
 def bench_render(args, device):
