@@ -52,7 +52,6 @@ struct TileTaps {             // one output coset
     int tap_box[SP_MAX_STENCIL];
     int tap_dz0[SP_MAX_STENCIL];    // plane offset of the tap
     int tap_off[SP_MAX_STENCIL];    // in-plane offset of (dz1 - lo1, dz2 - lo2)
-    int tap_row[SP_MAX_STENCIL];    // dz1 - lo1
     T w[SP_MAX_STENCIL];
 };
 
@@ -92,29 +91,12 @@ __device__ __forceinline__ long long policy_index(const sp::GridArgs<T>& g, int 
 //             policy folded into the source index) — any grid, any policy.
 //   kTmaPlane: one thread copies whole box planes with a 3-D tensor map (TMA zero-fills out
 //             of range = the 'zero' policy) — coset rows that are 16-byte multiples.
-//   kBulkRow: box planes fully inside the array are copied row by row with 1-D bulk copies
-//             (cp.async.bulk: the 16-byte aligned span around each row; the row's data then
-//             starts at a per-row phase), other planes element by element at the same phase —
-//             any row length whose phase is the same for rows two apart (fp32: even rows).
-enum PfMode { kCpAsync = 0, kTmaPlane = 1, kBulkRow = 2 };
-
-// element phase of the 16-byte aligned copy of the row starting at element e (array base
-// 16-byte aligned): 0 except in kBulkRow mode
-// (for the row of plane p, row y, starting at column x of an e1 x e2 coset array: only the
-// low bits of its linear element index matter, so 32-bit unsigned wrap-around is exact)
-template <typename T, int kMode>
-__device__ __forceinline__ int row_phase(int p, int y, int x, int e1, int e2) {
-    if constexpr (kMode == kBulkRow) {
-        constexpr unsigned V = 16 / sizeof(T);
-        return (int)((((unsigned)p * (unsigned)e1 + (unsigned)y) * (unsigned)e2 + (unsigned)x) & (V - 1));
-    }
-    return 0;
-}
+enum PfMode { kCpAsync = 0, kTmaPlane = 1 };
 
 // Copy plane `p` (coset-cell index along axis 0) of box b's rows [y0 + lo1, ...) x
 // [x0 + lo2, ...) into ring slot `slot` with cp.async (4 / 8-byte elements, zero-filled for the
 // 'zero' policy outside the array, clamp / mirror indices otherwise): warp per row.
-template <typename T, int kMode>
+template <typename T>
 __device__ __forceinline__ void stage_plane(const sp::GridArgs<T>& g, const TileTaps<T>& tp, int b, int p, int slot,
                                             int y0, int x0, int hv, int wv, T* sm, int lane, int warp) {
     const int s = tp.box_src[b];
@@ -126,10 +108,9 @@ __device__ __forceinline__ void stage_plane(const sp::GridArgs<T>& g, const Tile
     const int e0 = g.ext[s][0], e1 = g.ext[s][1], e2 = g.ext[s][2];
     const bool inside = p >= 0 && p < e0 && s1 >= 0 && s2 >= 0 && s1 + ex1c <= e1 && s2 + ex2c <= e2;
     for (int i1 = warp; i1 < ex1c; i1 += kThreadsPF / 32) {
-        const long long row = ((long long)p * e1 + (s1 + i1)) * e2 + s2;
-        T* drow = dst + i1 * tp.pitch[b] + row_phase<T, kMode>(p, s1 + i1, s2, e1, e2);
+        T* drow = dst + i1 * tp.pitch[b];
         if (inside) {
-            const T* rp = src + row;
+            const T* rp = src + ((long long)p * e1 + (s1 + i1)) * e2 + s2;
             for (int c = lane; c < ex2c; c += 32) sp::cp_async_elem<sizeof(T)>(drow + c, rp + c, (int)sizeof(T));
         } else {
             for (int c = lane; c < ex2c; c += 32) {
@@ -139,30 +120,6 @@ __device__ __forceinline__ void stage_plane(const sp::GridArgs<T>& g, const Tile
             }
         }
     }
-}
-
-// kBulkRow: can box b's plane p be bulk-copied (fully inside, not touching the array's last row)?
-template <typename T>
-__device__ __forceinline__ bool bulk_ok(const sp::GridArgs<T>& g, const TileTaps<T>& tp, int b, int p, int y0, int x0) {
-    const int s = tp.box_src[b];
-    const int e0 = g.ext[s][0], e1 = g.ext[s][1], e2 = g.ext[s][2];
-    const int s1 = y0 + tp.box_lo[b][1], s2 = x0 + tp.box_lo[b][2];
-    return p >= 0 && p < e0 && s1 >= 0 && s2 >= 0 && s1 + tp.box_ex[b][1] <= e1 && s2 + tp.box_ex[b][2] <= e2 &&
-           !(p == e0 - 1 && s1 + tp.box_ex[b][1] == e1);
-}
-
-template <typename T>
-__device__ __forceinline__ unsigned bulk_row_bytes(long long row, int ex2) {
-    const unsigned long long a = (unsigned long long)row * sizeof(T);
-    return (unsigned)(((a + (unsigned long long)ex2 * sizeof(T) + 15) & ~15ull) - (a & ~15ull));
-}
-
-__device__ __forceinline__ void pf_bulk_row(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
-                 "l"(src), "r"(bytes), "r"(b)
-                 : "memory");
 }
 
 // Tensor maps of the TMA variant: one per (output coset, source box), box = one plane of the
@@ -213,7 +170,7 @@ __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArg
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* sm = reinterpret_cast<T*>(smem_raw);
     __shared__ __align__(8) unsigned long long mbar[2];
-    constexpr bool kAsyncBar = kMode != kCpAsync;  // mbarrier-tracked copies
+    constexpr bool kAsyncBar = kMode == kTmaPlane;  // mbarrier-tracked copies
     const int k = blockIdx.z % g.M;
     const int zc = blockIdx.z / g.M;
     const TileTaps<T>& tp = P.c[k];
@@ -238,7 +195,7 @@ __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArg
             for (int b = 0; b < tp.nbox; ++b)
                 for (int i = 0; i < nplanes; ++i) {
                     const int p = plane_of(b, i);
-                    if (p != INT_MIN) stage_plane<T, kMode>(g, tp, b, p, slot_of(b, p), y0, x0, hv, wv, sm, lane, warp);
+                    if (p != INT_MIN) stage_plane<T>(g, tp, b, p, slot_of(b, p), y0, x0, hv, wv, sm, lane, warp);
                 }
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         } else if constexpr (kMode == kTmaPlane) {
@@ -257,48 +214,6 @@ __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArg
                                          &maps.m[k * maps.nbox_max + b], bar, x0 + tp.box_lo[b][2], y0 + tp.box_lo[b][1], p);
                     }
             }
-        } else {  // kBulkRow: warp 0 bulk-copies the rows of inside planes, everyone else element-copies
-            if (warp == 0) {
-                unsigned bytes = 0;  // this lane's rows, then summed over the warp
-                for (int b = 0; b < tp.nbox; ++b)
-                    for (int i = 0; i < nplanes; ++i) {
-                        const int p = plane_of(b, i);
-                        if (p == INT_MIN || !bulk_ok(g, tp, b, p, y0, x0)) continue;
-                        const int s = tp.box_src[b];
-                        for (int r = lane; r < tp.box_ex[b][1]; r += 32) {
-                            const long long row =
-                                ((long long)p * g.ext[s][1] + (y0 + tp.box_lo[b][1] + r)) * g.ext[s][2] + x0 + tp.box_lo[b][2];
-                            bytes += bulk_row_bytes<T>(row, tp.box_ex[b][2]);
-                        }
-                    }
-                bytes = __reduce_add_sync(0xffffffffu, bytes);
-                if (lane == 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    pf_mbar_expect(bar, bytes);
-                }
-                __syncwarp();
-                for (int b = 0; b < tp.nbox; ++b)
-                    for (int i = 0; i < nplanes; ++i) {
-                        const int p = plane_of(b, i);
-                        if (p == INT_MIN || !bulk_ok(g, tp, b, p, y0, x0)) continue;
-                        const int s = tp.box_src[b];
-                        T* dst = sm + tp.box_off[b] + slot_of(b, p) * tp.slot_elems[b];
-                        for (int r = lane; r < tp.box_ex[b][1]; r += 32) {
-                            const long long row =
-                                ((long long)p * g.ext[s][1] + (y0 + tp.box_lo[b][1] + r)) * g.ext[s][2] + x0 + tp.box_lo[b][2];
-                            const T* sp_ = g.data[s] + row;
-                            pf_bulk_row(dst + r * tp.pitch[b], reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(sp_) & ~(uintptr_t)15),
-                                        bulk_row_bytes<T>(row, tp.box_ex[b][2]), bar);
-                        }
-                    }
-            }
-            for (int b = 0; b < tp.nbox; ++b)
-                for (int i = 0; i < nplanes; ++i) {
-                    const int p = plane_of(b, i);
-                    if (p != INT_MIN && !bulk_ok(g, tp, b, p, y0, x0))
-                        stage_plane<T, kMode>(g, tp, b, p, slot_of(b, p), y0, x0, hv, wv, sm, lane, warp);
-                }
-            asm volatile("cp.async.commit_group;\n" ::: "memory");
         }
     };
     // prologue: set 0 = planes za + lo0 .. za + hi0 of every box (mbar[0]); set a < kAhead = the
@@ -332,13 +247,9 @@ __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArg
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
                     const int b = tp.tap_box[t];
-                    const int s = tp.box_src[b];
                     pitch[t] = tp.pitch[b];
-                    // rows ty, ty + 2, ... share the copy phase (kBulkRow requirement)
-                    const int ph = row_phase<T, kMode>(z0 + tp.tap_dz0[t], y0 + tp.box_lo[b][1] + ty + tp.tap_row[t],
-                                                       x0 + tp.box_lo[b][2], g.ext[s][1], g.ext[s][2]);
                     base[t] = tp.box_off[b] + slot_of(b, z0 + tp.tap_dz0[t]) * tp.slot_elems[b] + tp.tap_off[t] +
-                              ty * pitch[t] + tx + ph;
+                              ty * pitch[t] + tx;
                     w[t] = tp.w[t];
                 }
 #pragma unroll
@@ -358,11 +269,8 @@ __global__ void __launch_bounds__(kThreadsPF) prefilter_zmarch(const sp::GridArg
                     T acc = T(0);
                     for (int t = 0; t < tp.n; ++t) {
                         const int b = tp.tap_box[t];
-                        const int s = tp.box_src[b];
-                        const int ph = row_phase<T, kMode>(z0 + tp.tap_dz0[t], y0 + tp.box_lo[b][1] + r + tp.tap_row[t],
-                                                           x0 + tp.box_lo[b][2], g.ext[s][1], g.ext[s][2]);
                         const int pl = tp.box_off[b] + slot_of(b, z0 + tp.tap_dz0[t]) * tp.slot_elems[b];
-                        acc = add_rn(acc, mul_rn(tp.w[t], sm[pl + tp.tap_off[t] + r * tp.pitch[b] + tx + ph]));
+                        acc = add_rn(acc, mul_rn(tp.w[t], sm[pl + tp.tap_off[t] + r * tp.pitch[b] + tx]));
                     }
                     out[(long long)r * e2] = acc;
                 }
@@ -461,16 +369,16 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
         return SP_OK;
     }
     // 2. staging mode: TMA planes when the policy is 'zero' (the TMA unit zero-fills out of
-    //    range) and every coset row is a multiple of 16 bytes (tensor-map strides); 1-D bulk row
-    //    copies when rows two apart share their 16-byte phase; else element-wise cp.async.
-    //    Each mode's ring layout must fit shared memory, else the next mode is tried.
+    //    range) and every coset row is a multiple of 16 bytes (tensor-map strides), else
+    //    element-wise cp.async; the TMA layout (aligned, wider boxes) must fit shared memory.
+    //    (1-D bulk row copies and 16-byte cp.async of the aligned row spans were measured slower
+    //    than element-wise cp.async on 1,624-byte rows and are not kept.)
     constexpr int kVecE = 16 / (int)sizeof(T);
     PfEncodeFn enc = pf_encoder();
-    bool aligned16 = true, phase2 = true;
+    bool aligned16 = true;
     for (int k = 0; k < in->M; ++k) {
         aligned16 &= (in->extent[k][2] * (long long)sizeof(T)) % 16 == 0;
-        phase2 &= (2 * in->extent[k][2] * (long long)sizeof(T)) % 16 == 0;
-        if ((reinterpret_cast<uintptr_t>(in->data[k]) & 15) != 0) aligned16 = phase2 = false;
+        if ((reinterpret_cast<uintptr_t>(in->data[k]) & 15) != 0) aligned16 = false;
     }
     const TileParams<T> P0 = P;
     // lay out mode `m` into P; returns the shared-memory bytes, or -1 if the mode does not apply
@@ -488,8 +396,7 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
                     tp.box_lo[b][2] = al;
                     if (tp.box_ex[b][2] > 256 || tp.box_ex[b][1] > 256) return -1;
                 }
-                // bulk rows: the aligned span around a row is up to 2 vectors longer than the row
-                tp.pitch[b] = m == kBulkRow ? (tp.box_ex[b][2] + 2 * kVecE + kVecE - 1) / kVecE * kVecE : tp.box_ex[b][2];
+                tp.pitch[b] = tp.box_ex[b][2];
                 tp.ring[b] = 1;
                 while (tp.ring[b] < tp.box_ex[b][0] + kAhead) tp.ring[b] *= 2;  // kAhead planes ahead; slot = plane & (ring-1)
                 const int plane = tp.box_ex[b][1] * tp.pitch[b];
@@ -506,7 +413,6 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
                 tp.tap_box[t] = bx;
                 tp.tap_dz0[t] = dz[0];
                 tp.tap_off[t] = (dz[1] - tp.box_lo[bx][1]) * tp.pitch[bx] + (dz[2] - tp.box_lo[bx][2]);
-                tp.tap_row[t] = dz[1] - tp.box_lo[bx][1];
                 tp.w[t] = (T)st->weight[t0 + t];
             }
         }
@@ -517,11 +423,6 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
     if (in->boundary == SP_ZERO && enc != nullptr && in->M * nbox_max <= kMaxMaps && aligned16 &&
         (smem_need = layout(kTmaPlane)) >= 0)
         mode = kTmaPlane;
-    // kBulkRow measured slower than element-wise cp.async on the C5 grid (BCC 2x406^3 fp32: 1.02
-    // vs 0.78 ms: 34 small row copies per plane set, edge tiles staged element-wise); opt-in
-    const char* bulk_env = getenv("SP_PF_BULK");
-    const bool bulk_ok_mode = phase2 && bulk_env && atoi(bulk_env) != 0;
-    if (mode < 0 && bulk_ok_mode && (smem_need = layout(kBulkRow)) >= 0) mode = kBulkRow;
     if (mode < 0 && (smem_need = layout(kCpAsync)) >= 0) mode = kCpAsync;
     if (mode < 0) return pfail(SP_ERR_UNSUPPORTED, "prefilter: tap offsets span too large a box");
     bool use_tma = mode == kTmaPlane;
@@ -551,8 +452,7 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
     }
     if (mode == kTmaPlane && !use_tma) {  // tensor-map encoding refused: next mode
         mode = -1;
-        if (bulk_ok_mode && (smem_need = layout(kBulkRow)) >= 0) mode = kBulkRow;
-        if (mode < 0 && (smem_need = layout(kCpAsync)) >= 0) mode = kCpAsync;
+        if ((smem_need = layout(kCpAsync)) >= 0) mode = kCpAsync;
         if (mode < 0) return pfail(SP_ERR_UNSUPPORTED, "prefilter: tap offsets span too large a box");
     }
     const int smem_bytes = (int)smem_need;
@@ -570,14 +470,12 @@ int run(const sp_grid_desc* in, const sp_stencil_desc* st, void* const* out, cud
 #define SP_PF_CASE(N)                                                                  \
     case N:                                                                            \
         if (mode == kTmaPlane) launch(prefilter_zmarch<T, N, kTmaPlane>);              \
-        else if (mode == kBulkRow) launch(prefilter_zmarch<T, N, kBulkRow>);           \
         else launch(prefilter_zmarch<T, N, kCpAsync>);                                 \
         break;
         SP_PF_CASE(1) SP_PF_CASE(2) SP_PF_CASE(3) SP_PF_CASE(4) SP_PF_CASE(5) SP_PF_CASE(7) SP_PF_CASE(9)
         SP_PF_CASE(27)
         default:
             if (mode == kTmaPlane) launch(prefilter_zmarch<T, 0, kTmaPlane>);
-            else if (mode == kBulkRow) launch(prefilter_zmarch<T, 0, kBulkRow>);
             else launch(prefilter_zmarch<T, 0, kCpAsync>);
             break;
 #undef SP_PF_CASE
