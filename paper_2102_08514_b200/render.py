@@ -197,7 +197,7 @@ def render_volume(job: RenderJob, interp: PlanInterpreter | None = None) -> Rend
         _native.check(lib.sp_ray_points(ctypes.byref(cam), job.width, job.height, k0, k1, pts.data_ptr(),
                                         ctypes.c_void_p(stream.cuda_stream)))
         p = pts[:m] if grid.dtype == torch.float32 else pts[:m].to(grid.dtype)
-        interp.eval_batch(grid, p, out=vals[:m], check=False, stream=stream)
+        interp.eval_batch(grid, p, out=vals[:m], check=False, order="given", stream=stream)  # coherent by construction
         _native.check(lib.sp_composite(vals.data_ptr(), dt, npx, k1 - k0, ctypes.byref(tfd), state.data_ptr(),
                                        ctypes.c_void_p(stream.cuda_stream)))
     rad, img = finish((state[:, :3], state[:, 3]), job.background, job.height, job.width)

@@ -678,20 +678,29 @@ def choose_order(pts: torch.Tensor, pairs: int = 4096) -> str:
     of consecutive points: "morton" if >= 99.9 % of them are non-decreasing in Morton order
     of their unit cells (protocol A layout), "given" if the median Chebyshev jump between
     consecutive cells is <= 2 (coherent input, e.g. rays or raster scans: chunk staging
-    works), else "sort" (protocol B).  One small device-to-host copy; no effect on values."""
+    works), else "sort" (protocol B).  On a CUDA tensor the statistics are computed on the
+    device (sp_morton_keys) and two numbers cross to the host; no effect on values."""
     n = pts.shape[0]
     if n < 2:
         return "given"
     m = min(pairs, n - 1)
     idx = torch.linspace(0, n - 2, m, device=pts.device).round().long()
-    ab = torch.stack([pts[idx], pts[idx + 1]], 0).to(torch.float64).cpu().numpy()
-    with np.errstate(invalid="ignore"):
-        cells = np.floor(np.nan_to_num(ab, nan=0.0, posinf=2.0**30, neginf=-2.0**30)).clip(-2**30, 2**30).astype(np.int64)
-    ka, kb = _morton64(cells[0]), _morton64(cells[1])
-    if np.mean(kb >= ka) >= 0.999:
+    ab = torch.cat([pts[idx], pts[idx + 1]], 0).to(torch.float64)
+    ab = torch.nan_to_num(ab, nan=0.0, posinf=2.0**30, neginf=-2.0**30).clamp(-2.0**30, 2.0**30)
+    cells = torch.floor(ab)
+    jump = (cells[m:] - cells[:m]).abs().amax(1)
+    if pts.device.type == "cuda":
+        keys = torch.empty(2 * m, dtype=torch.int64, device=pts.device)
+        _native.check(_native.lib().sp_morton_keys(ab.contiguous().data_ptr(), 2 * m, _native.SP_F64, keys.data_ptr(),
+                                                   torch.cuda.current_stream(pts.device).cuda_stream))
+        frac, med = torch.stack([(keys[m:] >= keys[:m]).double().mean(), jump.median()]).tolist()
+    else:
+        c = cells.numpy().astype(np.int64)
+        ka, kb = _morton64(c[:m]), _morton64(c[m:])
+        frac, med = float(np.mean(kb >= ka)), float(jump.median())
+    if frac >= 0.999:
         return "morton"
-    jump = np.abs(cells[1] - cells[0]).max(1)
-    return "given" if np.median(jump) <= 2 else "sort"
+    return "given" if med <= 2 else "sort"
 
 
 def _sort_frame(grid: CoefficientGrid, log2_brick: int):
