@@ -65,7 +65,9 @@ struct BWeights<3> {
     }
 };
 
-template <typename T, int DEG>
+// S0, S1 > 0: the row-vector tile's pitches as compile-time constants (the headline TMA
+// configuration), so the (DEG+1)^2 row loads use immediate offsets.
+template <typename T, int DEG, int S0 = 0, int S1 = 0>
 struct TensorBSplineEval {
     static constexpr int kMinBlocks = sizeof(T) == 4 ? 4 : 3;  // <= 64 / 80 registers
     static constexpr bool kSig = false;
@@ -90,7 +92,7 @@ struct TensorBSplineEval {
         T acc = T(0);
         if constexpr (F::kIsTile && vec_width<T>() > 0) {
             // staged row-vector tile: one vector load per (a0, a1) row
-            const int s0 = ctx.vst0, s1 = ctx.vst1;
+            const int s0 = S0 > 0 ? S0 : ctx.vst0, s1 = S1 > 0 ? S1 : ctx.vst1;
             const auto* p = f.vtile + (ctx.vbase + cell[0] * s0 + cell[1] * s1 + cell[2] - DEG * (s0 + s1 + 1));
 #pragma unroll
             for (int a0 = 0; a0 <= DEG; ++a0) {

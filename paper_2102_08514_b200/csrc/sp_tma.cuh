@@ -68,15 +68,35 @@ __device__ __forceinline__ void build_vtile(const T* tile, typename VecT<T, kVec
     }
 }
 
+// G = geometry known at compile time (0: runtime arguments): {log2b, bx, by, bz, vx, vy}.
+template <int L2B = 0, int BX = 0, int BY = 0, int BZ = 0, int VX = 0, int VY = 0>
+struct TmaGeom {};
+
+template <class G, int I>
+struct GeomVal;
+template <int L2B, int BX, int BY, int BZ, int VX, int VY, int I>
+struct GeomVal<TmaGeom<L2B, BX, BY, BZ, VX, VY>, I> {
+    static constexpr int v[6] = {L2B, BX, BY, BZ, VX, VY};
+    static constexpr int value = v[I];
+};
+// compile-time value when the geometry fixes it, else the runtime argument
+template <class G, int I>
+__device__ __forceinline__ int geom_or(int runtime) {
+    constexpr int c = GeomVal<G, I>::value;
+    return c > 0 ? c : runtime;
+}
+
 // Single-coset (M = 1) brick kernel, T = float, evaluators with a row-vector tile.
 // box = (bz, by, bx) coset cells; bx is a multiple of 4 (16-byte TMA rows) and 3 wider than
 // needed, because the box's innermost start coordinate must be 16-byte aligned; the host may
 // widen bx / by further so that the row loads are bank-conflict free (choose_box_pitch).
-template <typename T, class Ev>
+template <typename T, class Ev, class G = TmaGeom<>>
 __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     brick_kernel_tma(const EvalArgs<T> a, const __grid_constant__ CUtensorMap tmap,
-                     const long long* __restrict__ brick_start, int nbricks, int log2b, int bx, int by, int bz, int vx,
-                     int vy) {
+                     const long long* __restrict__ brick_start, int nbricks, int log2b_, int bx_, int by_, int bz_,
+                     int vx_, int vy_) {
+    const int log2b = geom_or<G, 0>(log2b_), bx = geom_or<G, 1>(bx_), by = geom_or<G, 2>(by_);
+    const int bz = geom_or<G, 3>(bz_), vx = geom_or<G, 4>(vx_), vy = geom_or<G, 5>(vy_);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ TileGeom geom;
     __shared__ __align__(8) unsigned long long mbar[2];

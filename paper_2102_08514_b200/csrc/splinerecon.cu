@@ -636,11 +636,11 @@ EncodeTiledFn encode_tiled() {
     return fn;
 }
 
-template <int DEG>
+template <int DEG, int S0 = 0, int S1 = 0, class G = sp::TmaGeom<>>
 cudaError_t launch_tma(const sp::EvalArgs<float>& a, const CUtensorMap& map, const long long* bstart, int nbricks,
                        int log2b, int bx, int by, int bz, int vx, int vy, size_t smem, int num_sms, cudaStream_t st) {
-    using Ev = sp::TensorBSplineEval<float, DEG>;
-    auto kern = sp::brick_kernel_tma<float, Ev>;
+    using Ev = sp::TensorBSplineEval<float, DEG, S0, S1>;
+    auto kern = sp::brick_kernel_tma<float, Ev, G>;
     const int per_sm = sp::cached_occupancy(kern, smem);  // also sets the dynamic smem limit
     const int blocks = std::max(1, std::min(nbricks, num_sms * per_sm));
     kern<<<blocks, sp::kThreads, smem, st>>>(a, map, bstart, nbricks, log2b, bx, by, bz, vx, vy);
@@ -742,8 +742,15 @@ int try_bricks_tma(const sp_plan* p, const sp_grid_desc* g, const sp::EvalArgs<f
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return 0;
     const long long* bs = reinterpret_cast<const long long*>(bstart);
-    cudaError_t e = p->tp_degree == 1 ? launch_tma<1>(a, map, bs, nbricks, log2b, bx, by, bz, vx, vy, smem, p->num_sms, st)
-                                      : launch_tma<3>(a, map, bs, nbricks, log2b, bx, by, bz, vx, vy, smem, p->num_sms, st);
+    // the headline configuration (tricubic, 8^3 bricks -> 18 x 11 conflict-free pitches) has a
+    // specialisation with compile-time tile pitches; SP_TMA_FIXED=0 disables it
+    const bool fixed = p->tp_degree == 3 && log2b == 3 && bx == 16 && by == 11 && bz == 11 && vx == 18 && vy == 11 &&
+                       env_int("SP_TMA_FIXED", 1) != 0;
+    cudaError_t e = p->tp_degree == 1
+                        ? launch_tma<1>(a, map, bs, nbricks, log2b, bx, by, bz, vx, vy, smem, p->num_sms, st)
+                    : fixed ? launch_tma<3, 18 * 11, 18, sp::TmaGeom<3, 16, 11, 11, 18, 11>>(a, map, bs, nbricks, log2b, bx, by,
+                                                                                          bz, vx, vy, smem, p->num_sms, st)
+                            : launch_tma<3>(a, map, bs, nbricks, log2b, bx, by, bz, vx, vy, smem, p->num_sms, st);
     if (e != cudaSuccess) return fail(SP_ERR_CUDA, "TMA brick kernel launch: %s", cudaGetErrorString(e));
     return 1;
 }
