@@ -66,6 +66,7 @@ struct EvalArgs {
     int trec_bytes;             // per-(coset, class) tile records (generated kernels), in smem
     int vec_cap;                // row-vector tile capacity in elements (0: no row-vector tile)
     const int* nbricks_dev;     // nullable: brick count in device memory (sync-free brick runs)
+    int prefetch_pts;           // TMA brick kernel: bulk-prefetch each next brick's points into L2
 };
 
 struct TileGeom {
@@ -566,6 +567,21 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
 }
 
 
+// Bulk-prefetch points [p0, p1) into L2 (16-byte granules inside the array, <= 1 MiB each):
+// issued for the CTA's next brick, so that brick's per-point loads hit L2 instead of HBM.
+template <typename T>
+__device__ __forceinline__ void prefetch_points_l2(const EvalArgs<T>& a, long long p0, long long p1) {
+    if ((reinterpret_cast<uintptr_t>(a.pts) & 15) != 0) return;
+    const unsigned long long lo = ((unsigned long long)p0 * 3 * sizeof(T) + 15) & ~15ull;
+    const unsigned long long hi =
+        min((unsigned long long)p1 * 3 * sizeof(T) + 15, (unsigned long long)a.n * 3 * sizeof(T)) & ~15ull;
+    const char* base = reinterpret_cast<const char*>(a.pts);
+    for (unsigned long long o = lo; o < hi; o += 1u << 20) {
+        const unsigned sz = (unsigned)min(hi - o, 1ull << 20);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"(sz) : "memory");
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void store_out(const EvalArgs<T>& a, long long j, T v) {
     if (a.out_index) a.out[a.out_index[j]] = v;
@@ -736,6 +752,8 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
 
     for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
         const long long p0 = brick_start[b], p1 = brick_start[b + 1];
+        if (tid == 0 && a.prefetch_pts && b + (int)gridDim.x < nbricks)
+            prefetch_points_l2(a, brick_start[b + gridDim.x], brick_start[b + gridDim.x + 1]);
         if (tid < 32) {
             if (lane == 0) {
                 const T* x = a.pts + 3 * p0;

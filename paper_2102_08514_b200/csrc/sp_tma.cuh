@@ -141,6 +141,9 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&mbar[slot], (unsigned)(boxv * sizeof(T)));
         tma_load_3d(buf(slot), &tmap, &mbar[slot], z2, z1, z0);
+        // and the brick's points into L2 (bulk prefetch, 16-byte granules inside the array): the
+        // per-point loads of the brick then hit L2 instead of waiting on HBM
+        if (a.prefetch_pts) prefetch_points_l2(a, brick_start[b], brick_start[b + 1]);
     };
 
     if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);

@@ -766,6 +766,7 @@ int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, 
     a.out_index = reinterpret_cast<const long long*>(out_index);
     a.out_index32 = out_index32;
     a.nbricks_dev = nbricks_dev;
+    a.prefetch_pts = env_int("SP_PREFETCH_PTS", 1);
     if constexpr (sizeof(T) == 4) {
         const int t = try_bricks_tma(p, g, a, bstart, nbricks, log2b, st);
         if (t != 0) return t > 0 ? SP_OK : t;
