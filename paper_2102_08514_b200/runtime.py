@@ -541,6 +541,24 @@ class PlanInterpreter:
             raise RuntimeError_("sigma sentinel hit in batch evaluation")
         return res
 
+    def graph(self, grid: CoefficientGrid, pts, *, out: torch.Tensor):
+        """One eval_batch (a PointBatch, or device points in the given order) captured in a
+        CUDA graph — `graph(...).replay()` re-evaluates the same buffers with one graph launch,
+        which removes the host-side cost of the call for launch-bound batches (≲ 10^7
+        points).  No sigma-sentinel check inside the graph (use eval_batch for that)."""
+        order = None if isinstance(pts, PointBatch) else "given"
+        kw = {} if order is None else {"order": order}
+        dev = grid.device
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm-up outside capture: handles, tensor maps, occupancy caches
+            self.eval_batch(grid, pts, out=out, check=False, **kw)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.eval_batch(grid, pts, out=out, check=False, **kw)
+        return g
+
     def _eval_sorted32(self, grid, p, res, b, frame, st, err):
         """Protocol B without host round trips: sp_sort_points (30-bit Morton keys in the
         grid's frame, CUB pair sort, gather, brick runs) then sp_eval_bricks_perm32 (results

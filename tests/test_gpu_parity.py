@@ -411,3 +411,26 @@ def test_auto_order_routes_and_matches(cuda):
     host = iid.cpu().pin_memory()  # pinned host batch: the pipelined path with the chosen order
     torch.testing.assert_close(interp.eval_batch(grid, host).to(cuda), interp.eval_batch(grid, iid, order="given"),
                                rtol=0, atol=0)
+
+
+def test_cuda_graph_replay_matches_eval_batch(cuda):
+    """PlanInterpreter.graph: a captured eval_batch (brick batch / chunk order) replays to the
+    same values, and follows new point values written into the captured buffers."""
+    g, plan, grid = _setup("cc_tricubic", "zero", torch.float32, cuda)
+    interp = PlanInterpreter(plan)
+    pts = torch.from_numpy(g["pts"]).to(cuda)
+    want = interp.eval_batch(grid, pts)
+    batch = interp.prepare(grid, pts)
+    out = torch.empty_like(want)
+    gr = interp.graph(grid, batch, out=out)
+    out.zero_()
+    gr.replay()
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out, want, rtol=0, atol=0)
+    p2 = pts.clone()
+    out2 = torch.empty_like(want)
+    gr2 = interp.graph(grid, p2, out=out2)
+    p2.add_(0.25)
+    gr2.replay()
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out2, interp.eval_batch(grid, pts + 0.25), rtol=0, atol=0)
