@@ -702,7 +702,8 @@ def choose_order(pts: torch.Tensor, pairs: int = 4096) -> str:
     if n < 2:
         return "given"
     m = min(pairs, n - 1)
-    idx = torch.linspace(0, n - 2, m, device=pts.device).round().long()
+    # evenly spaced in int64 (a float32 linspace rounds n - 2 up to n for n ~ 1e8)
+    idx = torch.arange(m, device=pts.device, dtype=torch.int64) * (n - 2) // max(m - 1, 1)
     ab = torch.cat([pts[idx], pts[idx + 1]], 0).to(torch.float64)
     ab = torch.nan_to_num(ab, nan=0.0, posinf=2.0**30, neginf=-2.0**30).clamp(-2.0**30, 2.0**30)
     cells = torch.floor(ab)

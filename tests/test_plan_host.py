@@ -203,3 +203,14 @@ def test_choose_order_heuristic():
             + torch.linspace(0, 50, 300, dtype=torch.float64)[None, :, None] * torch.tensor([0.3, 0.5, 0.8]))
     assert choose_order(rays.reshape(-1, 3)) == "given"
     assert choose_order(iid[:1]) == "given"
+
+
+def test_choose_order_sample_indices_stay_in_range():
+    """Sampling indices are exact integers for any batch size (a float32 linspace rounded
+    n - 2 up to n for n = 1e8): a large strided view keeps the memory small."""
+    import torch
+
+    from paper_2102_08514_b200.runtime import choose_order
+
+    big = (torch.rand(1, 3, dtype=torch.float64) * 50).expand(100_000_000, 3)  # 1e8 rows, stride-0 view
+    assert choose_order(big) == "morton"  # identical points: every pair is non-decreasing
