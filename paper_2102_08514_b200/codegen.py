@@ -170,11 +170,9 @@ def _group_body(g, d: int, gname: str, tnames: list, body_lines: list, ops: list
     if ns == 0:
         body.append(f"        acc = fma({gname}, f.get({sd[0][0]}, {sd[0][1]}, {sd[0][2]}), acc);")
         ops[0] += 1
-    elif ns == 1:
-        body.append(f"        const T c0 = f.get({sd[0][0]}, {sd[0][1]}, {sd[0][2]});")
-        body.append(f"        const T c1 = f.get({sd[1][0]}, {sd[1][1]}, {sd[1][2]});")
-        body.append(f"        acc = fma({gname}, c0, acc);")
-        body.append(f"        acc = fma({tnames[0]}, c1 - c0, acc);")
+    elif ns == 1:  # exact fetchers: g*c0 + t_num*(c1 - c0); the texture fetcher: one filtered fetch
+        body.append(f"        acc = f.lerp2(acc, {gname}, {tnames[0]}, {sd[0][0]}, {sd[0][1]}, {sd[0][2]}, "
+                    f"{sd[1][0]}, {sd[1][1]}, {sd[1][2]});")
         ops[0] += 3
     else:
         body.append(f"        const T gz = {gname};")
@@ -783,6 +781,7 @@ extern const sp::GenEntry kGen_{ident} = {{
     &sp::occupancy_bricks<float, sp::gen_{ident}::Eval<float>>,
     &sp::occupancy_bricks<double, sp::gen_{ident}::Eval<double>>,
     sp::gen_{ident}::Eval<float>::kTrecBytes,
+    &sp::launch_tex<sp::gen_{ident}::Eval<float>>,
 }};
 """
     return src, {"ident": ident, "flops_per_coset": kflops, "words": len(words), "affine": aff is not None}

@@ -187,6 +187,14 @@ struct TileFetch {
         a0 = tg.off[k] + (base[0] - tg.lo[k][0]) * c0 + (base[1] - tg.lo[k][1]) * c1 + (base[2] - tg.lo[k][2]);
     }
     __device__ __forceinline__ T get(int s0, int s1, int s2) const { return tile[a0 + s0 * c0 + s1 * c1 + s2 * c2]; }
+    // a 2-site fetch group (the paper's linear-fetch merge, §4.4) done exactly in software:
+    // acc + g*c0 + t_num*(c1 - c0)  (plancompile.py:669-697 up to the local-lerp rounding)
+    __device__ __forceinline__ T lerp2(T acc, T g, T tn, int a0_, int a1_, int a2_, int b0_, int b1_, int b2_) const {
+        const T c0 = get(a0_, a1_, a2_);
+        const T c1 = get(b0_, b1_, b2_);
+        acc = fma(g, c0, acc);
+        return fma(tn, c1 - c0, acc);
+    }
 };
 
 template <typename T>
@@ -221,6 +229,62 @@ struct GlobalFetch {
         const int z1 = b1 + s0 * p[0][1] + s1 * p[1][1] + s2 * p[2][1];
         const int z2 = b2 + s0 * p[0][2] + s1 * p[1][2] + s2 * p[2][2];
         return policy_read_slow(data, e0, e1, e2, boundary, z0, z1, z2);
+    }
+    // a 2-site fetch group (the paper's linear-fetch merge, §4.4) done exactly in software:
+    // acc + g*c0 + t_num*(c1 - c0)  (plancompile.py:669-697 up to the local-lerp rounding)
+    __device__ __forceinline__ T lerp2(T acc, T g, T tn, int a0_, int a1_, int a2_, int b0_, int b1_, int b2_) const {
+        const T c0 = get(a0_, a1_, a2_);
+        const T c1 = get(b0_, b1_, b2_);
+        acc = fma(g, c0, acc);
+        return fma(tn, c1 - c0, acc);
+    }
+};
+
+// Hardware-texture fetcher (the paper's GPU path, PAPER.md:334 / §4.4): one texture object
+// per coset (cudaFilterModeLinear, unnormalised coordinates, texel i = array index i, centre
+// at i + 0.5; border = 'zero', clamp = 'clamp').  get() samples a texel centre (exact); a
+// 2-site group is ONE filtered fetch at c0's centre + (t_num/g) toward c1 — the filtering
+// weight is 9-bit fixed point, so this variant is NOT exact (reported separately).
+struct TexArgs {
+    cudaTextureObject_t tex[SP_MAX_COSETS];
+};
+struct TexFetch {
+    static constexpr bool kIsTile = false;
+    const TexArgs* targs;
+    cudaTextureObject_t t;
+    int b0, b1, b2;
+    int p[3][3];
+    __device__ __forceinline__ void frame(const GridArgs<float>& grid, int kk, const int base[3], const int rho[3],
+                                          const int tau[3]) {
+        t = targs->tex[kk];
+        b0 = base[0] - grid.org[kk][0];
+        b1 = base[1] - grid.org[kk][1];
+        b2 = base[2] - grid.org[kk][2];
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) p[j][i] = rho[i] == j ? tau[i] : 0;
+    }
+    __device__ __forceinline__ void index(int s0, int s1, int s2, int z[3]) const {
+        z[0] = b0 + s0 * p[0][0] + s1 * p[1][0] + s2 * p[2][0];
+        z[1] = b1 + s0 * p[0][1] + s1 * p[1][1] + s2 * p[2][1];
+        z[2] = b2 + s0 * p[0][2] + s1 * p[1][2] + s2 * p[2][2];
+    }
+    __device__ __forceinline__ float get(int s0, int s1, int s2) const {
+        int z[3];
+        index(s0, s1, s2, z);
+        return tex3D<float>(t, (float)z[2] + 0.5f, (float)z[1] + 0.5f, (float)z[0] + 0.5f);
+    }
+    __device__ __forceinline__ float lerp2(float acc, float g, float tn, int a0_, int a1_, int a2_, int b0_, int b1_,
+                                           int b2_) const {
+        int za[3], zb[3];
+        index(a0_, a1_, a2_, za);
+        index(b0_, b1_, b2_, zb);
+        const float tt = g == 0.0f ? 0.5f : tn / g;
+        const float v = tex3D<float>(t, (float)za[2] + 0.5f + tt * (float)(zb[2] - za[2]),
+                                     (float)za[1] + 0.5f + tt * (float)(zb[1] - za[1]),
+                                     (float)za[0] + 0.5f + tt * (float)(zb[0] - za[0]));
+        return fma(g, v, acc);
     }
 };
 
@@ -843,6 +907,10 @@ __device__ __forceinline__ void bind(TileFetch<T, V>& f, const EvalArgs<T>& a, c
 template <typename T>
 __device__ __forceinline__ void bind(GlobalFetch<T>& f, const EvalArgs<T>& a, const TileGeom& g, int k,
                                      const int base[3], const int rho[3], const int tau[3]) {
+    f.frame(a.grid, k, base, rho, tau);
+}
+__device__ __forceinline__ void bind(TexFetch& f, const EvalArgs<float>& a, const TileGeom& g, int k, const int base[3],
+                                     const int rho[3], const int tau[3]) {
     f.frame(a.grid, k, base, rho, tau);
 }
 template <typename T, typename V>

@@ -1,6 +1,7 @@
 // sp_launch.cuh — kernel launch helpers and the generated-kernel registry entry type.
 #pragma once
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -70,6 +71,51 @@ static int occupancy_blocks(size_t smem) {
     return cached_occupancy(eval_kernel<T, Ev>, smem);
 }
 
+// Texture-filtered variant of a generated plan (TexFetch, sp_eval_texture): thread per point,
+// plan tables in shared memory, every fetch from the cosets' texture objects.
+template <class Ev>
+__global__ void __launch_bounds__(kThreads) tex_eval_kernel(const EvalArgs<float> a, const TexArgs targs) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ TileGeom geom;  // not read by the texture fetcher
+    const int tb = (a.table_bytes + 15) & ~15;
+    if (a.table_bytes > 0) {
+        const int4* src = reinterpret_cast<const int4*>(a.tables);
+        int4* dst = reinterpret_cast<int4*>(smem);
+        for (int i = threadIdx.x; i < tb / 16; i += kThreads) dst[i] = src[i];
+    }
+    __syncthreads();
+    EvalCtx<float, Ev> ctx;
+    ctx.a = &a;
+    ctx.tables = smem;
+    ctx.geom = &geom;
+    ctx.trec = nullptr;
+    ctx.err = 0;
+    for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < a.n; i += (long long)gridDim.x * kThreads) {
+        const float x[3] = {a.pts[3 * i], a.pts[3 * i + 1], a.pts[3 * i + 2]};
+        float v = NAN;
+        if (isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2])) {
+            ctx.index = i;
+            ctx.X[0] = clamp_cell(x[0]);
+            ctx.X[1] = clamp_cell(x[1]);
+            ctx.X[2] = clamp_cell(x[2]);
+            TexFetch f;
+            f.targs = &targs;
+            v = Ev::template eval<TexFetch>(x, f, ctx);
+        }
+        a.out[i] = v;
+    }
+    if (ctx.err && a.err) atomicOr(a.err, 1);
+}
+
+using TexLaunchFn = cudaError_t (*)(const EvalArgs<float>&, const TexArgs&, cudaStream_t);
+
+template <class Ev>
+static cudaError_t launch_tex(const EvalArgs<float>& a, const TexArgs& t, cudaStream_t st) {
+    const long long blocks = std::min<long long>((a.n + kThreads - 1) / kThreads, 148ll * 16);
+    tex_eval_kernel<Ev><<<(int)std::max<long long>(1, blocks), kThreads, (a.table_bytes + 15) & ~15, st>>>(a, t);
+    return cudaGetLastError();
+}
+
 struct GenEntry {
     const char* name;
     const uint64_t* blob;
@@ -83,6 +129,7 @@ struct GenEntry {
     int (*bocc_f32)(size_t);
     int (*bocc_f64)(size_t);
     int trec_bytes;  // per-tile address records (+ tables) in smem
+    TexLaunchFn tex_f32;  // hardware-texture variant (float32)
 };
 
 }  // namespace sp

@@ -19,16 +19,21 @@
 
 #include "../../include/splinerecon.h"
 #include "sp_evaluators.cuh"
+#include "sp_launch.cuh"
 
 struct sp_texture {
-    cudaArray_t array = nullptr;
-    cudaTextureObject_t tex = 0;
-    int origin[3] = {0, 0, 0};
-    int boundary = SP_ZERO;
+    int M = 0;
+    cudaArray_t array[SP_MAX_COSETS] = {};
+    cudaTextureObject_t texs[SP_MAX_COSETS] = {};
+    cudaTextureObject_t tex = 0;  // coset 0 (tensor-product kernels)
+    int origin[3] = {0, 0, 0};    // coset 0
+    sp_grid_desc desc{};          // extents / origins / policy of every coset (data pointers unused)
 };
 
 namespace sp {
 void set_error(const std::string& msg);  // splinerecon.cu (feeds sp_last_error)
+int eval_texture_generated(const sp_plan* p, const sp_grid_desc* g, const TexArgs& targs, const void* pts, int64_t n,
+                           void* out, int32_t* err, cudaStream_t st);  // splinerecon.cu
 }
 
 namespace {
@@ -87,56 +92,69 @@ __global__ void __launch_bounds__(256) tex_tricubic(cudaTextureObject_t t, const
 
 }  // namespace
 
+extern "C" void sp_texture_destroy(sp_texture* t) {
+    if (!t) return;
+    for (int k = 0; k < t->M; ++k) {
+        if (t->texs[k]) cudaDestroyTextureObject(t->texs[k]);
+        if (t->array[k]) cudaFreeArray(t->array[k]);
+    }
+    delete t;
+}
+
 extern "C" int sp_texture_create(const sp_grid_desc* grid, sp_texture** out) {
     if (!grid || !out) return tfail(SP_ERR_INVALID, "null argument");
     *out = nullptr;
-    if (grid->s != 3 || grid->M != 1) return tfail(SP_ERR_UNSUPPORTED, "texture variant: single-coset 3-D grids only");
+    if (grid->s != 3 || grid->M < 1 || grid->M > SP_MAX_COSETS) return tfail(SP_ERR_UNSUPPORTED, "texture variant: 3-D grids only");
     if (grid->dtype != SP_F32) return tfail(SP_ERR_UNSUPPORTED, "texture variant: float32 grids only");
     if (grid->boundary == SP_MIRROR)
         return tfail(SP_ERR_UNSUPPORTED, "texture variant: hardware mirror (period 2n) differs from runtime.py:191-196");
     sp_texture* t = new sp_texture();
-    t->boundary = grid->boundary;
+    t->M = grid->M;
+    t->desc = *grid;
     for (int i = 0; i < 3; ++i) t->origin[i] = (int)grid->origin[0][i];
-    const cudaExtent ext = make_cudaExtent(grid->extent[0][2], grid->extent[0][1], grid->extent[0][0]);
-    cudaChannelFormatDesc ch = cudaCreateChannelDesc<float>();
-    cudaError_t e = cudaMalloc3DArray(&t->array, &ch, ext);
-    if (e != cudaSuccess) { delete t; return tfail(SP_ERR_CUDA, "cudaMalloc3DArray", e); }
-    cudaMemcpy3DParms cp = {};
-    cp.srcPtr = make_cudaPitchedPtr(const_cast<void*>(grid->data[0]), grid->extent[0][2] * sizeof(float),
-                                    grid->extent[0][2], grid->extent[0][1]);
-    cp.dstArray = t->array;
-    cp.extent = ext;
-    cp.kind = cudaMemcpyDeviceToDevice;
-    e = cudaMemcpy3D(&cp);
-    if (e != cudaSuccess) { cudaFreeArray(t->array); delete t; return tfail(SP_ERR_CUDA, "cudaMemcpy3D", e); }
-    cudaResourceDesc rd = {};
-    rd.resType = cudaResourceTypeArray;
-    rd.res.array.array = t->array;
-    cudaTextureDesc td = {};
-    const cudaTextureAddressMode am = grid->boundary == SP_ZERO ? cudaAddressModeBorder : cudaAddressModeClamp;
-    td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = am;
-    td.filterMode = cudaFilterModeLinear;
-    td.readMode = cudaReadModeElementType;
-    td.normalizedCoords = 0;
-    e = cudaCreateTextureObject(&t->tex, &rd, &td, nullptr);
-    if (e != cudaSuccess) { cudaFreeArray(t->array); delete t; return tfail(SP_ERR_CUDA, "cudaCreateTextureObject", e); }
+    for (int k = 0; k < grid->M; ++k) {  // one 3-D array + linear-filtered texture object per coset
+        const cudaExtent ext = make_cudaExtent(grid->extent[k][2], grid->extent[k][1], grid->extent[k][0]);
+        cudaChannelFormatDesc ch = cudaCreateChannelDesc<float>();
+        cudaError_t e = cudaMalloc3DArray(&t->array[k], &ch, ext);
+        if (e != cudaSuccess) { sp_texture_destroy(t); return tfail(SP_ERR_CUDA, "cudaMalloc3DArray", e); }
+        cudaMemcpy3DParms cp = {};
+        cp.srcPtr = make_cudaPitchedPtr(const_cast<void*>(grid->data[k]), grid->extent[k][2] * sizeof(float),
+                                        grid->extent[k][2], grid->extent[k][1]);
+        cp.dstArray = t->array[k];
+        cp.extent = ext;
+        cp.kind = cudaMemcpyDeviceToDevice;
+        e = cudaMemcpy3D(&cp);
+        if (e != cudaSuccess) { sp_texture_destroy(t); return tfail(SP_ERR_CUDA, "cudaMemcpy3D", e); }
+        cudaResourceDesc rd = {};
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = t->array[k];
+        cudaTextureDesc td = {};
+        const cudaTextureAddressMode am = grid->boundary == SP_ZERO ? cudaAddressModeBorder : cudaAddressModeClamp;
+        td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = am;
+        td.filterMode = cudaFilterModeLinear;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        e = cudaCreateTextureObject(&t->texs[k], &rd, &td, nullptr);
+        if (e != cudaSuccess) { sp_texture_destroy(t); return tfail(SP_ERR_CUDA, "cudaCreateTextureObject", e); }
+    }
+    t->tex = t->texs[0];
     *out = t;
     return SP_OK;
-}
-
-extern "C" void sp_texture_destroy(sp_texture* t) {
-    if (!t) return;
-    if (t->tex) cudaDestroyTextureObject(t->tex);
-    if (t->array) cudaFreeArray(t->array);
-    delete t;
 }
 
 extern "C" int sp_eval_texture(const sp_plan* plan, const sp_texture* t, const void* pts, int64_t n, void* out,
                                void* stream) {
     if (!plan || !t) return tfail(SP_ERR_INVALID, "null plan or texture");
     if (n <= 0) return SP_OK;
-    if (sp_plan_kernel_kind(plan) != SP_KIND_TENSOR_BSPLINE)
-        return tfail(SP_ERR_UNSUPPORTED, "texture variant: tensor-product B-spline plans only");
+    cudaStream_t st0 = reinterpret_cast<cudaStream_t>(stream);
+    if (sp_plan_kernel_kind(plan) == SP_KIND_GENERATED) {  // box splines: per-coset textures, TexFetch
+        sp::TexArgs targs{};
+        for (int k = 0; k < t->M; ++k) targs.tex[k] = t->texs[k];
+        sp_grid_desc g = t->desc;
+        return sp::eval_texture_generated(plan, &g, targs, pts, n, out, nullptr, st0);
+    }
+    if (sp_plan_kernel_kind(plan) != SP_KIND_TENSOR_BSPLINE || t->M != 1)
+        return tfail(SP_ERR_UNSUPPORTED, "texture variant: tensor-product or compiled box-spline plans only");
     const std::string name = sp_plan_kernel_name(plan);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const long long blocks = std::min<long long>((n + 255) / 256, 148ll * 32);

@@ -810,6 +810,24 @@ extern "C" int sp_eval(const sp_plan* plan, const sp_grid_desc* grid, const void
     return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
 }
 
+// Texture-filtered evaluation of a generated plan (called by sp_eval_texture, sp_texture.cu):
+// `g` describes the cosets' extents / origins / policy (data pointers unused), `targs` the
+// texture objects.
+namespace sp {
+int eval_texture_generated(const sp_plan* p, const sp_grid_desc* g, const TexArgs& targs, const void* pts, int64_t n,
+                           void* out, int32_t* err, cudaStream_t st) {
+    if (p->kind != SP_KIND_GENERATED || !p->gen || !p->gen->tex_f32)
+        return fail(SP_ERR_UNSUPPORTED, "texture variant: no compiled texture kernel for this plan");
+    EvalArgs<float> a;
+    int vec = 0;
+    int rc = build_args<float>(p, g, pts, n, out, nullptr, err, a, vec);
+    if (rc != SP_OK) return rc;
+    cudaError_t e = p->gen->tex_f32(a, targs, st);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "texture kernel launch: %s", cudaGetErrorString(e));
+    return SP_OK;
+}
+}  // namespace sp
+
 extern "C" int sp_debug_stats(int enable, uint64_t* out) {
     if (out) {
         if (g_stats) {

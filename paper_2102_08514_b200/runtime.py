@@ -590,7 +590,9 @@ class PlanInterpreter:
                            stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         """Hardware-texture-filtered variant (sp_eval_texture): the paper's GPU fetch path with
         9-bit texture filtering weights — NOT within the exact tolerances; reported
-        separately with its measured error.  fp32 single-coset grids, TP degree 1 or 3."""
+        separately with its measured error.  fp32 grids, 'zero' / 'clamp' policies;
+        tensor-product plans of degree 1 or 3 (8 filtered fetches per tricubic point) and the
+        compiled box-spline plans (one filtered fetch per 2-site fetch group, TexFetch)."""
         self._check_grid(grid)
         lib = _native.lib()
         h = self._handle(grid.device)

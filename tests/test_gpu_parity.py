@@ -222,8 +222,27 @@ def test_texture_variant_error_is_bounded(name, deg, cuda):
     ok = torch.isfinite(exact)
     err = (tex[ok] - exact[ok]).abs().max().item() / exact[ok].abs().max().item()
     assert err < 2e-2
+    with pytest.raises(NotImplementedError):  # no texture kernel for the table-driven generic path
+        PlanInterpreter(plan, kernel="generic").eval_batch_texture(grid, pts)
+
+
+@pytest.mark.parametrize("name,boundary", [("bcc_linear_rd", "zero"), ("bcc_quintic_rd", "clamp"),
+                                           ("fcc_cubic", "zero"), ("bcc_quartic", "zero")])
+def test_box_spline_texture_variant_error_is_bounded(name, boundary, cuda):
+    """Box splines through hardware linear fetches (one filtered texture fetch per 2-site group,
+    the paper's §4.4 merge in hardware): tracks the exact kernel to the 9-bit weight precision,
+    is not exact, and the classification / sites are unchanged (exact where groups are 1-site)."""
+    g, plan, grid = _setup(name, boundary, torch.float32, cuda)
+    interp = PlanInterpreter(plan)
+    pts = torch.from_numpy(g["pts"]).to(cuda)
+    exact = interp.eval_batch(grid, pts)
+    tex = interp.eval_batch_texture(grid, pts)
+    ok = torch.isfinite(exact)
+    assert torch.equal(torch.isfinite(tex), ok)
+    err = (tex[ok] - exact[ok]).abs().max().item() / exact[ok].abs().max().item()
+    assert 1e-6 < err < 2e-2, err
     with pytest.raises(NotImplementedError):
-        _, p2, g2 = _setup("bcc_linear_rd", "zero", torch.float32, cuda)
+        _, p2, g2 = _setup(name, "mirror", torch.float32, cuda)
         PlanInterpreter(p2).eval_batch_texture(g2, pts)
 
 
