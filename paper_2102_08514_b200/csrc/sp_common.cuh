@@ -632,7 +632,9 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
 
 
 // Bulk-prefetch points [p0, p1) into L2 (16-byte granules inside the array, <= 1 MiB each):
-// issued for the CTA's next brick, so that brick's per-point loads hit L2 instead of HBM.
+// issued by the TMA brick kernel for the CTA's next brick, so that brick's per-point loads hit
+// L2 instead of HBM (+3 % tricubic).  Not used by the generic brick kernel: with its larger
+// bricks the prefetched points evict lattice lines (ncu: +40 % DRAM traffic for +0-1.5 %).
 template <typename T>
 __device__ __forceinline__ void prefetch_points_l2(const EvalArgs<T>& a, long long p0, long long p1) {
     if ((reinterpret_cast<uintptr_t>(a.pts) & 15) != 0) return;
@@ -816,8 +818,6 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
 
     for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
         const long long p0 = brick_start[b], p1 = brick_start[b + 1];
-        if (tid == 0 && a.prefetch_pts && b + (int)gridDim.x < nbricks)
-            prefetch_points_l2(a, brick_start[b + gridDim.x], brick_start[b + gridDim.x + 1]);
         if (tid < 32) {
             if (lane == 0) {
                 const T* x = a.pts + 3 * p0;
