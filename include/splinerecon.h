@@ -161,7 +161,8 @@ int sp_eval_bricks_dev(const sp_plan* plan, const sp_grid_desc* grid, const void
  * with `bits` (<= 10) per axis — cells outside [lo, lo + 2^bits) are clamped, which only
  * affects the order (any brick partition is evaluated correctly) — a radix sort of (key,
  * index) pairs, the points gathered into key order (sorted_pts, same dtype/shape as pts),
- * the int32 permutation (perm[i] = caller index of sorted point i) and the brick runs
+ * (skipped when sorted_pts is NULL), the int32 permutation (perm[i] = caller index of sorted
+ * point i) and the brick runs
  * (brick_start [n+1], brick count in device memory), all stream-ordered; n < 2^31.
  * temp: device scratch of sp_sort_points_temp_bytes(n) bytes (NULL: stream-ordered alloc).
  * sp_eval_bricks_perm32: sp_eval_bricks_dev writing point i's value to out[perm[i]] — the
@@ -173,6 +174,12 @@ int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t lo0, int32
 int sp_eval_bricks_perm32(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
                           const int64_t* brick_start, const int32_t* n_bricks_dev, int32_t n_bricks_cap,
                           int32_t log2_brick, const int32_t* perm, void* out, int32_t* err_flag, void* stream);
+/* sp_eval_bricks_indirect: the same without the gathered copy — `pts` are the caller's
+ * (unsorted) points, brick-order point i is pts[perm[i]] and its value goes to out[perm[i]]
+ * (sp_sort_points may then be called with sorted_pts = NULL, skipping its gather). */
+int sp_eval_bricks_indirect(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+                            const int64_t* brick_start, const int32_t* n_bricks_dev, int32_t n_bricks_cap,
+                            int32_t log2_brick, const int32_t* perm, void* out, int32_t* err_flag, void* stream);
 
 /* Synchronous convenience: sp_eval + stream sync + sentinel check (SP_ERR_SENTINEL). */
 int sp_eval_sync(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,

@@ -63,6 +63,7 @@ struct EvalArgs {
     unsigned long long* stats;  // nullable: [0] staged chunks, [1] unstaged chunks, [2] staged elements
     const long long* out_index; // nullable: value of point i goes to out[out_index[i]]
     const int* out_index32;     // nullable: same with int32 indices (sp_sort_points' permutation)
+    const int* in_index32;      // nullable: brick-order point j is pts[in_index32[j]] (unsorted input, no gather)
     int trec_bytes;             // per-(coset, class) tile records (generated kernels), in smem
     int vec_cap;                // row-vector tile capacity in elements (0: no row-vector tile)
     const int* nbricks_dev;     // nullable: brick count in device memory (sync-free brick runs)
@@ -648,6 +649,12 @@ __device__ __forceinline__ void prefetch_points_l2(const EvalArgs<T>& a, long lo
     }
 }
 
+// brick-order point j (through the sort permutation when the points are not gathered)
+template <typename T>
+__device__ __forceinline__ const T* point_ptr(const EvalArgs<T>& a, long long j) {
+    return a.pts + 3 * (a.in_index32 ? (long long)a.in_index32[j] : j);
+}
+
 template <typename T>
 __device__ __forceinline__ void store_out(const EvalArgs<T>& a, long long j, T v) {
     if (a.out_index) a.out[a.out_index[j]] = v;
@@ -707,7 +714,9 @@ __device__ __forceinline__ void eval_brick_sig(const EvalArgs<T>& a, EvalCtx<T, 
 #pragma unroll
             for (int q = 0; q < 3 * kPer; ++q) {
                 const int e = tid + q * kThreads;
-                v[q] = e < 3 * n ? __ldg(src + e) : T(0);
+                v[q] = e >= 3 * n ? T(0)
+                       : a.in_index32 ? __ldg(a.pts + 3 * (long long)a.in_index32[seg + e / 3] + e % 3)
+                                      : __ldg(src + e);
             }
 #pragma unroll
             for (int q = 0; q < 3 * kPer; ++q) s_pts[tid + q * kThreads] = v[q];
@@ -820,7 +829,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         const long long p0 = brick_start[b], p1 = brick_start[b + 1];
         if (tid < 32) {
             if (lane == 0) {
-                const T* x = a.pts + 3 * p0;
+                const T* x = point_ptr(a, p0);
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
                     const int c = clamp_cell(x[i]);
@@ -851,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         // software-pipelined point loads: the next point is in flight while this one is evaluated
         T xn0 = T(0), xn1 = T(0), xn2 = T(0);
         if (p0 + tid < p1) {
-            const T* px = a.pts + 3 * (p0 + tid);
+            const T* px = point_ptr(a, p0 + tid);
             xn0 = __ldg(px);
             xn1 = __ldg(px + 1);
             xn2 = __ldg(px + 2);
@@ -868,7 +877,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
             ctx.index = j;
             const T x[3] = {xn0, xn1, xn2};
             if (j + kThreads < p1) {
-                const T* px = a.pts + 3 * (j + kThreads);
+                const T* px = point_ptr(a, j + kThreads);
                 xn0 = __ldg(px);
                 xn1 = __ldg(px + 1);
                 xn2 = __ldg(px + 2);

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
 
     // thread 0: brick corner from its first point, then the bulk tensor copy of its box
     auto issue = [&](int b, int slot) {
-        const T* x = a.pts + 3 * brick_start[b];
+        const T* x = point_ptr(a, brick_start[b]);
         int c[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         tma_load_3d(buf(slot), &tmap, &mbar[slot], z2, z1, z0);
         // and the brick's points into L2 (bulk prefetch, 16-byte granules inside the array): the
         // per-point loads of the brick then hit L2 instead of waiting on HBM
-        if (a.prefetch_pts) prefetch_points_l2(a, brick_start[b], brick_start[b + 1]);
+        if (a.prefetch_pts && !a.in_index32) prefetch_points_l2(a, brick_start[b], brick_start[b + 1]);
     };
 
     if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         const long long p0 = brick_start[b], p1 = brick_start[b + 1];
         T xn0 = T(0), xn1 = T(0), xn2 = T(0);
         if (p0 + tid < p1) {
-            const T* px = a.pts + 3 * (p0 + tid);
+            const T* px = point_ptr(a, p0 + tid);
             xn0 = __ldg(px);
             xn1 = __ldg(px + 1);
             xn2 = __ldg(px + 2);
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
             ctx.index = j;
             const T x[3] = {xn0, xn1, xn2};
             if (j + kThreads < p1) {
-                const T* px = a.pts + 3 * (j + kThreads);
+                const T* px = point_ptr(a, j + kThreads);
                 xn0 = __ldg(px);
                 xn1 = __ldg(px + 1);
                 xn2 = __ldg(px + 2);

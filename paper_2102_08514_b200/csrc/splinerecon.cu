@@ -758,13 +758,15 @@ int try_bricks_tma(const sp_plan* p, const sp_grid_desc* g, const sp::EvalArgs<f
 template <typename T>
 int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, const int64_t* bstart,
                       int32_t nbricks, int32_t log2b, const int64_t* out_index, void* out, int32_t* err,
-                      cudaStream_t st, const int32_t* nbricks_dev = nullptr, const int32_t* out_index32 = nullptr) {
+                      cudaStream_t st, const int32_t* nbricks_dev = nullptr, const int32_t* out_index32 = nullptr,
+                      const int32_t* in_index32 = nullptr) {
     sp::EvalArgs<T> a;
     int vec = 0;
     int rc = build_args<T>(p, g, pts, n, out, nullptr, err, a, vec);
     if (rc != SP_OK) return rc;
     a.out_index = reinterpret_cast<const long long*>(out_index);
     a.out_index32 = out_index32;
+    a.in_index32 = in_index32;
     a.nbricks_dev = nbricks_dev;
     a.prefetch_pts = env_int("SP_PREFETCH_PTS", 1);
     if constexpr (sizeof(T) == 4) {
@@ -1091,8 +1093,7 @@ extern "C" int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t
     if (bits < 0 || bits > 10) return fail(SP_ERR_INVALID, "bits must be in [0, 10]");
     if (log2_brick < 0 || log2_brick > bits) return fail(SP_ERR_INVALID, "log2_brick out of range");
     if (dtype != SP_F32 && dtype != SP_F64) return fail(SP_ERR_INVALID, "unknown dtype");
-    if (!brick_start || !n_bricks || (n > 0 && (!pts || !sorted_pts || !perm)))
-        return fail(SP_ERR_INVALID, "null argument");
+    if (!brick_start || !n_bricks || (n > 0 && (!pts || !perm))) return fail(SP_ERR_INVALID, "null argument");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (n == 0) {
         SP_CUDA(cudaMemsetAsync(n_bricks, 0, sizeof(int32_t), st));
@@ -1122,9 +1123,9 @@ extern "C" int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t
     size_t cb = cub_bytes;
     if (e == cudaSuccess) e = cub::DeviceRadixSort::SortPairs(cub_tmp, cb, k_in, k_out, iota, perm, (int)n, 0, end_bit, st);
     if (e == cudaSuccess) {
-        if (dtype == SP_F32)
+        if (sorted_pts && dtype == SP_F32)
             gather_points32_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, perm, n, (float*)sorted_pts);
-        else
+        else if (sorted_pts)
             gather_points32_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, perm, n, (double*)sorted_pts);
         thrust::counting_iterator<long long> idx(0);
         const BrickHead32 head{k_out, 3 * log2_brick};
@@ -1158,6 +1159,27 @@ extern "C" int sp_eval_bricks_perm32(const sp_plan* plan, const sp_grid_desc* gr
     if (dtype == SP_F64)
         return eval_bricks_typed<double>(plan, grid, pts, n, brick_start, n_bricks_cap, log2_brick, nullptr, out,
                                          err_flag, st, n_bricks_dev, perm);
+    return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
+extern "C" int sp_eval_bricks_indirect(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n,
+                                       int32_t dtype, const int64_t* brick_start, const int32_t* n_bricks_dev,
+                                       int32_t n_bricks_cap, int32_t log2_brick, const int32_t* perm, void* out,
+                                       int32_t* err_flag, void* stream) {
+    if (!plan) return fail(SP_ERR_INVALID, "null plan");
+    int rc = check_grid(plan, grid, dtype);
+    if (rc != SP_OK) return rc;
+    if (n < 0 || n_bricks_cap < 0) return fail(SP_ERR_INVALID, "negative size");
+    if (n == 0 || n_bricks_cap == 0) return SP_OK;
+    if (log2_brick < 0 || log2_brick > 20) return fail(SP_ERR_INVALID, "log2_brick out of range");
+    if (!pts || !out || !brick_start || !n_bricks_dev || !perm) return fail(SP_ERR_INVALID, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32)
+        return eval_bricks_typed<float>(plan, grid, pts, n, brick_start, n_bricks_cap, log2_brick, nullptr, out,
+                                        err_flag, st, n_bricks_dev, perm, perm);
+    if (dtype == SP_F64)
+        return eval_bricks_typed<double>(plan, grid, pts, n, brick_start, n_bricks_cap, log2_brick, nullptr, out,
+                                         err_flag, st, n_bricks_dev, perm, perm);
     return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
 }
 

@@ -22,6 +22,7 @@ relative; fp32 grids to ~1e-7 of max|f|.
 from __future__ import annotations
 
 import ctypes
+import os
 import itertools
 import math
 from typing import Callable, Sequence
@@ -420,8 +421,12 @@ class PlanInterpreter:
     # order="auto" sorts incoherent batches only for plans reading at least this many
     # coefficients per point: measured on B200 with 1e8 iid points, unstaged L2 gathers cost
     # ~0.9 ms per tap (tricubic 64 taps: 60 ms; BCC quintic 32: 24 ms; BCC linear 4: 4.4 ms)
-    # against ~11 ms for the sort + gather + scatter of protocol B
+    # against ~10 ms for the sort + permuted reads + scatter of protocol B
     auto_sort_min_taps = 12
+
+    # protocol B: gather the sorted points into a contiguous copy before the brick kernel
+    # (True) or let the brick kernel read them through the permutation (False)
+    sort_gather = os.environ.get("SP_SORT_GATHER", "0") == "1"
 
     def _taps_per_point(self) -> float:
         counts = self.plan.nearest_fetch_counts
@@ -561,8 +566,10 @@ class PlanInterpreter:
 
     def _eval_sorted32(self, grid, p, res, b, frame, st, err):
         """Protocol B without host round trips: sp_sort_points (30-bit Morton keys in the
-        grid's frame, CUB pair sort, gather, brick runs) then sp_eval_bricks_perm32 (results
-        scattered back to the caller's order by the brick kernel)."""
+        grid's frame, CUB pair sort, brick runs) then sp_eval_bricks_indirect (the brick
+        kernel reads the caller's points through the permutation and scatters the results
+        back to the caller's order); sort_gather = True gathers a sorted copy first and uses
+        sp_eval_bricks_perm32."""
         lib = _native.lib()
         dev = grid.device
         n = p.shape[0]
@@ -578,13 +585,15 @@ class PlanInterpreter:
         sp_, perm, start, count, tmp = ws
         h = self._handle(dev)
         gdesc = grid.descriptor()
+        gather = self.sort_gather
         with torch.cuda.stream(st):
-            _native.check(lib.sp_sort_points(p.data_ptr(), n, dtype, lo0, lo1, lo2, bits, b, sp_.data_ptr(),
-                                             perm.data_ptr(), start.data_ptr(), count.data_ptr(), tmp.data_ptr(),
-                                             tmp.numel(), st.cuda_stream))
-            _native.check(lib.sp_eval_bricks_perm32(h, ctypes.byref(gdesc), sp_.data_ptr(), n, dtype, start.data_ptr(),
-                                                    count.data_ptr(), n, b, perm.data_ptr(), res.data_ptr(),
-                                                    None if err is None else err.data_ptr(), st.cuda_stream))
+            _native.check(lib.sp_sort_points(p.data_ptr(), n, dtype, lo0, lo1, lo2, bits, b,
+                                             sp_.data_ptr() if gather else None, perm.data_ptr(), start.data_ptr(),
+                                             count.data_ptr(), tmp.data_ptr(), tmp.numel(), st.cuda_stream))
+            fn = lib.sp_eval_bricks_perm32 if gather else lib.sp_eval_bricks_indirect
+            _native.check(fn(h, ctypes.byref(gdesc), (sp_ if gather else p).data_ptr(), n, dtype, start.data_ptr(),
+                             count.data_ptr(), n, b, perm.data_ptr(), res.data_ptr(),
+                             None if err is None else err.data_ptr(), st.cuda_stream))
 
     def eval_batch_texture(self, grid: CoefficientGrid, pts: torch.Tensor, *, out: torch.Tensor | None = None,
                            stream: torch.cuda.Stream | None = None) -> torch.Tensor:

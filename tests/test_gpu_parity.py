@@ -375,15 +375,18 @@ def test_sync_free_brick_runs_match(name, presorted, cuda):
 
 @pytest.mark.parametrize("name,dtype", [("cc_tricubic", torch.float32), ("bcc_quintic_rd", torch.float32),
                                         ("fcc_cubic", torch.float64), ("bcc_linear_rd", torch.float32)])
-def test_sorted32_protocol_b_matches_given_order(name, dtype, cuda):
-    """order='sort' (sp_sort_points: 30-bit keys in the grid frame, CUB pair sort, gather,
-    device brick runs; sp_eval_bricks_perm32 scatters back) is bit-identical to the chunk
-    kernel on shuffled points, including points outside the grid (clamped keys) and NaN;
-    a grid wider than 2^10 cells falls back to the 64-bit-key path."""
+@pytest.mark.parametrize("gather", [False, True])
+def test_sorted32_protocol_b_matches_given_order(name, dtype, gather, cuda):
+    """order='sort' (sp_sort_points: 30-bit keys in the grid frame, CUB pair sort, device
+    brick runs; then either a gathered copy + sp_eval_bricks_perm32, or
+    sp_eval_bricks_indirect reading the caller's points through the permutation; both scatter
+    back) is bit-identical to the chunk kernel on shuffled points, including points outside
+    the grid (clamped keys) and NaN."""
     from paper_2102_08514_b200.runtime import _sort_frame
 
     g, plan, grid = _setup(name, "mirror", dtype, cuda)
     interp = PlanInterpreter(plan)
+    interp.sort_gather = gather
     rng = np.random.default_rng(17)
     hi = max(a.shape[0] for a in grid.arrays) * plan.diag[0]
     pts = rng.uniform(-3, hi + 3, size=(200_000, 3))

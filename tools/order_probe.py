@@ -40,8 +40,12 @@ def main():
     n = pts.shape[0]
     out = torch.empty(n, dtype=grid.dtype, device=dev)
     res = {}
-    for order in ("given", "sort"):
-        res[order] = timed(lambda: interp.eval_batch(grid, pts, out=out, check=False, order=order), a.iters)
+    res["given"] = timed(lambda: interp.eval_batch(grid, pts, out=out, check=False, order="given"), a.iters)
+    for gather in (False, True):
+        interp.sort_gather = gather
+        res[f"sort gather={int(gather)}"] = timed(
+            lambda: interp.eval_batch(grid, pts, out=out, check=False, order="sort"), a.iters)
+    interp.sort_gather = False
     batch = interp.prepare(grid, pts)
     sorted_pts = batch.pts
     pre = interp.prepare(grid, sorted_pts, presorted=True)
