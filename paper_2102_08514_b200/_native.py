@@ -16,7 +16,9 @@ import numpy as np
 from .packing import SP_MAX_DIM, PackedPlan
 
 SP_MAX_COSETS = 8
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsplinerecon.so")
+# SP_CHECKED=1 loads the bounds-checked build (build.py --checked) instead
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                        "libsplinerecon_checked.so" if os.environ.get("SP_CHECKED") == "1" else "libsplinerecon.so")
 
 SP_OK = 0
 SP_ERR_INVALID = -1
@@ -211,7 +213,8 @@ def lib():
         if _lib is None:
             if not os.path.exists(LIB_PATH):
                 raise ImportError(
-                    f"{LIB_PATH} is missing: build it with `python -m paper_2102_08514_b200.build` "
+                    f"{LIB_PATH} is missing: build it with `python -m paper_2102_08514_b200.build"
+                    f"{' --checked' if LIB_PATH.endswith('_checked.so') else ''}` "
                     "(there is no CPU fallback)"
                 )
             handle = ctypes.CDLL(LIB_PATH)

@@ -17,6 +17,7 @@
 // interpreter) only see the Fetch interface below.
 #pragma once
 
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -69,6 +70,26 @@ struct EvalArgs {
     const int* nbricks_dev;     // nullable: brick count in device memory (sync-free brick runs)
     int prefetch_pts;           // TMA brick kernel: bulk-prefetch each next brick's points into L2
 };
+
+// Checked build (build.py --checked -> libsplinerecon_checked.so, loaded with SP_CHECKED=1):
+// shared-tile, point and output indices are bounds-checked and a violation traps with a
+// message (compute-sanitizer is not available on the GPU pool).  Compiled out otherwise.
+#ifdef SP_BOUNDS_CHECK
+#define SP_CHECK(cond)                                                                              \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("splinerecon bounds check failed: %s (%s:%d) block %d thread %d\n", #cond,      \
+                   __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x);                          \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#define SP_TILE_LIMIT(f, n) ((f).lim = (n))
+#else
+#define SP_CHECK(cond) \
+    do {               \
+    } while (0)
+#define SP_TILE_LIMIT(f, n) ((void)0)
+#endif
 
 struct TileGeom {
     int staged;
@@ -160,6 +181,9 @@ struct TileFetch {
     const V* vtile;  // row-vector copy of the tile (evaluators with vec_width > 0)
     int a0;
     int c0, c1, c2;
+#ifdef SP_BOUNDS_CHECK
+    int lim;  // staged scalar tile elements
+#endif
 
     __device__ __forceinline__ void frame(const TileGeom& tg, int k, const int base[3], const int rho[3],
                                           const int tau[3]) {
@@ -187,7 +211,10 @@ struct TileFetch {
         c2 = 1;
         a0 = tg.off[k] + (base[0] - tg.lo[k][0]) * c0 + (base[1] - tg.lo[k][1]) * c1 + (base[2] - tg.lo[k][2]);
     }
-    __device__ __forceinline__ T get(int s0, int s1, int s2) const { return tile[a0 + s0 * c0 + s1 * c1 + s2 * c2]; }
+    __device__ __forceinline__ T get(int s0, int s1, int s2) const {
+        SP_CHECK((unsigned)(a0 + s0 * c0 + s1 * c1 + s2 * c2) < (unsigned)lim);
+        return tile[a0 + s0 * c0 + s1 * c1 + s2 * c2];
+    }
     // a 2-site fetch group (the paper's linear-fetch merge, §4.4) done exactly in software:
     // acc + g*c0 + t_num*(c1 - c0)  (plancompile.py:669-697 up to the local-lerp rounding)
     __device__ __forceinline__ T lerp2(T acc, T g, T tn, int a0_, int a1_, int a2_, int b0_, int b1_, int b2_) const {
@@ -619,6 +646,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks) eval_kernel(const Ev
                 TileFetch<T, V> f;
                 f.tile = tile;
                 f.vtile = vtile;
+                SP_TILE_LIMIT(f, ctx.geom->total);
                 v = Ev::template eval<TileFetch<T, V>>(x, f, ctx);
             } else {
                 GlobalFetch<T> f;
@@ -652,11 +680,16 @@ __device__ __forceinline__ void prefetch_points_l2(const EvalArgs<T>& a, long lo
 // brick-order point j (through the sort permutation when the points are not gathered)
 template <typename T>
 __device__ __forceinline__ const T* point_ptr(const EvalArgs<T>& a, long long j) {
+    SP_CHECK(j >= 0 && j < a.n);
+    SP_CHECK(!a.in_index32 || (unsigned)a.in_index32[j] < (unsigned long long)a.n);
     return a.pts + 3 * (a.in_index32 ? (long long)a.in_index32[j] : j);
 }
 
 template <typename T>
 __device__ __forceinline__ void store_out(const EvalArgs<T>& a, long long j, T v) {
+    SP_CHECK(j >= 0 && j < a.n);
+    SP_CHECK(!a.out_index || (a.out_index[j] >= 0 && a.out_index[j] < a.n));
+    SP_CHECK(!a.out_index32 || (unsigned)a.out_index32[j] < (unsigned long long)a.n);
     if (a.out_index) a.out[a.out_index[j]] = v;
     else if (a.out_index32) a.out[a.out_index32[j]] = v;
     else a.out[j] = v;
@@ -674,6 +707,7 @@ __device__ __forceinline__ T eval_one(const T x[3], bool staged, int c0, int c1,
         TileFetch<T, V> f;
         f.tile = tile;
         f.vtile = vtile;
+        SP_TILE_LIMIT(f, ctx.geom->total);
         return Ev::template eval<TileFetch<T, V>>(x, f, ctx);
     }
     GlobalFetch<T> f;
@@ -781,6 +815,7 @@ __device__ __forceinline__ void eval_brick_sig(const EvalArgs<T>& a, EvalCtx<T, 
                 TileFetch<T, V> f;
                 f.tile = tile;
                 f.vtile = vtile;
+                SP_TILE_LIMIT(f, ctx.geom->total);
                 v = Ev::template eval_word<TileFetch<T, V>>(x, s_word[i], f, ctx);
             } else if (!(isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]))) {
                 v = T(NAN);
@@ -895,6 +930,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
                 TileFetch<T, V> f;
                 f.tile = tile;
                 f.vtile = vtile;
+                SP_TILE_LIMIT(f, ctx.geom->total);
                 v = Ev::template eval<TileFetch<T, V>>(x, f, ctx);
             } else {
                 GlobalFetch<T> f;

@@ -94,6 +94,8 @@ struct TensorBSplineEval {
             // staged row-vector tile: one vector load per (a0, a1) row
             const int s0 = S0 > 0 ? S0 : ctx.vst0, s1 = S1 > 0 ? S1 : ctx.vst1;
             const auto* p = f.vtile + (ctx.vbase + cell[0] * s0 + cell[1] * s1 + cell[2] - DEG * (s0 + s1 + 1));
+            SP_CHECK(ctx.vbase + cell[0] * s0 + cell[1] * s1 + cell[2] - DEG * (s0 + s1 + 1) >= 0 &&
+                     ctx.vbase + cell[0] * s0 + cell[1] * s1 + cell[2] < ctx.geom->vtotal);
 #pragma unroll
             for (int a0 = 0; a0 <= DEG; ++a0) {
                 T acc1 = T(0);
