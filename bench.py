@@ -520,8 +520,9 @@ def run_ours(args):
         },
         "e2e": e2e,
         "unsorted_e2e_device": {"value": world * n / (ms_b * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_b,
-                                "note": "protocol B: shuffled points; Morton keys + sort + gather + brick runs + eval "
-                                        "+ scatter to caller order, all timed"},
+                                "note": "protocol B: shuffled points; Morton keys + sort + brick runs + eval reading "
+                                        "the points through the permutation + scatter to caller order, all "
+                                        "timed"},
         "roofline_onchip": onchip_roofline(plan, esize, n / (ms * 1e-3), clk.summary().get("sm_mhz")),
         "texture_variant": texture,
         "gpu_launches": int(args.steps * launches_per_step),
