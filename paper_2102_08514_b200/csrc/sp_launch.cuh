@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <utility>
 
 #include "sp_common.cuh"
@@ -11,22 +12,48 @@
 
 namespace sp {
 
-// Blocks per SM of `kern` at `smem` bytes, memoised per (kernel, smem): the occupancy query
-// costs tens of microseconds of host time, which short launches cannot hide.
+// cudaFuncSetAttribute acts on the current device: done once per (kernel, device).  Keyed by
+// the kernel address (kernels of one signature share any per-instantiation static).
+template <typename K>
+static cudaError_t ensure_smem_limit(K kern, int dev) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, cudaError_t> done;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+    auto it = done.find(key);
+    if (it != done.end()) return it->second;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess) done[key] = e;
+    return e;
+}
+
+template <typename K>
+static cudaError_t ensure_smem_limit(K kern) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return ensure_smem_limit(kern, dev);
+}
+
+// Blocks per SM of `kern` at `smem` bytes, memoised per (kernel, smem, device): the occupancy
+// query costs tens of microseconds of host time, which short launches cannot hide.  Also
+// raises the kernel's dynamic shared-memory limit on this device.
 template <typename K>
 static int cached_occupancy(K kern, size_t smem) {
-    // keyed by the kernel too: every kernel of one signature shares this instantiation
+    int dev = 0;
+    cudaGetDevice(&dev);
     static std::mutex mu;
-    static std::map<std::pair<const void*, size_t>, int> memo;
-    std::lock_guard<std::mutex> lock(mu);
-    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), smem);
-    auto it = memo.find(key);
-    if (it != memo.end()) return it->second;
+    static std::map<std::tuple<const void*, size_t, int>, int> memo;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = memo.find(std::make_tuple(reinterpret_cast<const void*>(kern), smem, dev));
+        if (it != memo.end()) return it->second;
+    }
     int per_sm = 0;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    ensure_smem_limit(kern, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-    memo[key] = per_sm;
+    std::lock_guard<std::mutex> lock(mu);
+    memo[std::make_tuple(reinterpret_cast<const void*>(kern), smem, dev)] = per_sm;
     return per_sm;
 }
 
@@ -35,12 +62,8 @@ using LaunchFn = cudaError_t (*)(const EvalArgs<T>&, int, size_t, cudaStream_t);
 
 template <typename T, class Ev>
 static cudaError_t launch_eval(const EvalArgs<T>& a, int blocks, size_t smem, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(eval_kernel<T, Ev>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    const cudaError_t e = ensure_smem_limit(eval_kernel<T, Ev>);
+    if (e != cudaSuccess) return e;
     eval_kernel<T, Ev><<<blocks, kThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
@@ -51,12 +74,8 @@ using BrickLaunchFn = cudaError_t (*)(const EvalArgs<T>&, const long long*, int,
 template <typename T, class Ev>
 static cudaError_t launch_bricks(const EvalArgs<T>& a, const long long* bstart, int nbricks, int log2b, int blocks,
                                  size_t smem, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(brick_kernel<T, Ev>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    const cudaError_t e = ensure_smem_limit(brick_kernel<T, Ev>);
+    if (e != cudaSuccess) return e;
     brick_kernel<T, Ev><<<blocks, kThreads, smem, st>>>(a, bstart, nbricks, log2b);
     return cudaGetLastError();
 }

@@ -290,16 +290,15 @@ typedef CUresult (*PfEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, vo
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 PfEncodeFn pf_encoder() {
-    static PfEncodeFn fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    // initialised once, thread-safely (function-local static)
+    static const PfEncodeFn fn = [] {
         cudaDriverEntryPointQueryResult q;
         void* f = nullptr;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PfEncodeFn>(f);
-    }
+            return reinterpret_cast<PfEncodeFn>(f);
+        return (PfEncodeFn) nullptr;
+    }();
     return fn;
 }
 

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 import itertools
 import math
 from typing import Callable, Sequence
@@ -252,6 +253,9 @@ class PlanInterpreter:
         self.plan = plan
         self.mode = mode
         self._handles: dict = {}
+        # guards the lazily built caches (plan handles, textures, workspaces): evaluation from
+        # many threads is safe; per-call device state is per thread and stream
+        self._lock = threading.RLock()
         self._tp = plan.tensor_bspline_degree()
         self._kernel = kernel
         # s = 2 plans run as their s = 3 lift (lift.py): same operations, third axis inert
@@ -264,6 +268,13 @@ class PlanInterpreter:
     # -- native plan handle (one per device) ----------------------------------
     def _handle(self, device: torch.device):
         key = device.index if device.index is not None else torch.cuda.current_device()
+        h = self._handles.get(key)
+        if h is not None:
+            return h
+        with self._lock:
+            return self._create_handle(key)
+
+    def _create_handle(self, key):
         h = self._handles.get(key)
         if h is None:
             if self.plan.s != 3:
@@ -428,6 +439,9 @@ class PlanInterpreter:
     # (True) or let the brick kernel read them through the permutation (False)
     sort_gather = os.environ.get("SP_SORT_GATHER", "0") == "1"
 
+    # protocol-B workspaces kept (one per thread x stream x batch shape, most recent first out)
+    sort_ws_keep = 4
+
     def _taps_per_point(self) -> float:
         counts = self.plan.nearest_fetch_counts
         counts = counts() if callable(counts) else counts
@@ -440,10 +454,12 @@ class PlanInterpreter:
     host_slots = 3
 
     def _pipeline_state(self, dev, dtype, s):
-        """Per (device, dtype) pipeline resources, created once: three streams (H2D copy,
-        compute, D2H copy) and a ring of `host_slots` chunk buffers with their events."""
-        key = (dev, dtype, s, self.host_chunk, self.host_slots)
-        st = self.__dict__.setdefault("_pipes", {}).get(key)
+        """Per (thread, device, dtype) pipeline resources, created once: three streams (H2D
+        copy, compute, D2H copy) and a ring of `host_slots` chunk buffers with their events
+        (per thread, so concurrent callers never share a ring)."""
+        key = (threading.get_ident(), dev, dtype, s, self.host_chunk, self.host_slots)
+        with self._lock:
+            st = self.__dict__.setdefault("_pipes", {}).get(key)
         if st is None:
             C = self.host_chunk
             slots = []
@@ -457,7 +473,8 @@ class PlanInterpreter:
                 })
             st = {"h2d": torch.cuda.Stream(dev), "comp": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
                   "slots": slots}
-            self._pipes[key] = st
+            with self._lock:
+                self._pipes[key] = st
         return st
 
     def _eval_host_pipelined(self, grid, pts, out, *, check, order, stream):
@@ -575,13 +592,22 @@ class PlanInterpreter:
         n = p.shape[0]
         dtype = _native.SP_F32 if grid.dtype == torch.float32 else _native.SP_F64
         (lo0, lo1, lo2), bits = frame
-        key = (dev.index, n, grid.dtype)
-        ws = self._sort_ws.get(key) if hasattr(self, "_sort_ws") else None
+        # one cached workspace per (thread, stream): reuse is stream-ordered, and concurrent
+        # callers never share one; allocated on `st` so that the caching
+        # allocator recycles it in that stream's order when it is dropped
+        key = (threading.get_ident(), st.cuda_stream, dev.index, n, grid.dtype, self.sort_gather)
+        with self._lock:
+            cache = self.__dict__.setdefault("_sort_ws", {})
+            ws = cache.pop(key, None)
         if ws is None:
-            ws = (torch.empty_like(p), torch.empty(n, dtype=torch.int32, device=dev),
-                  torch.empty(n + 1, dtype=torch.int64, device=dev), torch.empty(1, dtype=torch.int32, device=dev),
-                  torch.empty(max(1, int(lib.sp_sort_points_temp_bytes(n))), dtype=torch.uint8, device=dev))
-            self._sort_ws = {key: ws}  # one cached workspace (the last batch shape)
+            with torch.cuda.stream(st):
+                ws = (torch.empty_like(p) if self.sort_gather else None, torch.empty(n, dtype=torch.int32, device=dev),
+                      torch.empty(n + 1, dtype=torch.int64, device=dev), torch.empty(1, dtype=torch.int32, device=dev),
+                      torch.empty(max(1, int(lib.sp_sort_points_temp_bytes(n))), dtype=torch.uint8, device=dev))
+        with self._lock:
+            cache[key] = ws
+            while len(cache) > self.sort_ws_keep:
+                cache.pop(next(iter(cache)))
         sp_, perm, start, count, tmp = ws
         h = self._handle(dev)
         gdesc = grid.descriptor()
@@ -606,19 +632,8 @@ class PlanInterpreter:
         lib = _native.lib()
         h = self._handle(grid.device)
         key = (id(grid), tuple(a.data_ptr() for a in grid.arrays))
-        cache = self.__dict__.setdefault("_tex", {})
-        tex = cache.get(key)
-        if tex is None:
-            for old in cache.values():
-                lib.sp_texture_destroy(old)
-            cache.clear()
-            gd = grid.descriptor()
-            hnd = ctypes.c_void_p()
-            code = lib.sp_texture_create(ctypes.byref(gd), ctypes.byref(hnd))
-            if code == _native.SP_ERR_UNSUPPORTED:
-                raise NotImplementedError(lib.sp_last_error().decode())
-            _native.check(code)
-            tex = cache[key] = hnd.value
+        with self._lock:
+            tex = self._texture_for(grid, key, lib)
         p = pts.to(device=grid.device, dtype=torch.float32).contiguous()
         res = out if out is not None else torch.empty(p.shape[0], dtype=torch.float32, device=grid.device)
         st = stream if stream is not None else torch.cuda.current_stream(grid.device)
@@ -627,6 +642,25 @@ class PlanInterpreter:
             raise NotImplementedError(lib.sp_last_error().decode())
         _native.check(code)
         return res
+
+    def _texture_for(self, grid, key, lib):
+        """The texture objects of `grid` (up to 4 grids cached; an evicted one is destroyed
+        after a device synchronisation, since another thread's launch may still read it;
+        caller holds the lock)."""
+        cache = self.__dict__.setdefault("_tex", {})
+        tex = cache.get(key)
+        if tex is None:
+            if len(cache) >= 4:
+                torch.cuda.synchronize(grid.device)
+                lib.sp_texture_destroy(cache.pop(next(iter(cache))))
+            gd = grid.descriptor()
+            hnd = ctypes.c_void_p()
+            code = lib.sp_texture_create(ctypes.byref(gd), ctypes.byref(hnd))
+            if code == _native.SP_ERR_UNSUPPORTED:
+                raise NotImplementedError(lib.sp_last_error().decode())
+            _native.check(code)
+            tex = cache[key] = hnd.value
+        return tex
 
     def classify(self, grid: CoefficientGrid, pts: torch.Tensor):
         """Per point and coset: class id and coset cell kk/d (runtime.py:371-379), as

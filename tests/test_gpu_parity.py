@@ -456,3 +456,56 @@ def test_cuda_graph_replay_matches_eval_batch(cuda):
     gr2.replay()
     torch.cuda.synchronize()
     torch.testing.assert_close(out2, interp.eval_batch(grid, pts + 0.25), rtol=0, atol=0)
+
+
+def test_concurrent_threads_and_streams(cuda):
+    """Evaluation from many threads at once is safe: four threads share one
+    interpreter per plan, each on its own stream, mixing order='given' / 'sort' / a sorted
+    PointBatch / pinned host buffers (the pipelined path) and the texture variant; every
+    result equals the serial one bit for bit."""
+    import threading
+
+    rng = np.random.default_rng(23)
+    setups = []
+    for name in ("cc_tricubic", "fcc_cubic", "bcc_linear_rd"):
+        g, plan, grid = _setup(name, "zero", torch.float32, cuda)
+        interp = PlanInterpreter(plan)
+        hi = max(a.shape[0] for a in grid.arrays) * plan.diag[0]
+        pts = torch.from_numpy(rng.uniform(-2, hi + 2, size=(60_000, 3))).to(cuda, torch.float32)
+        setups.append((interp, grid, pts, interp.eval_batch(grid, pts, order="given").cpu()))
+    interp0, grid0, pts0, _ = setups[0]
+    interp0.host_chunk = 1 << 13  # several pipelined chunks per call
+    tex_want = interp0.eval_batch_texture(grid0, pts0).cpu()
+    errors = []
+
+    def worker(tid):
+        try:
+            st = torch.cuda.Stream(cuda)
+            with torch.cuda.stream(st):
+                for it in range(6):
+                    interp, grid, pts, want = setups[(tid + it) % len(setups)]
+                    mode = (tid + it) % 4
+                    if mode == 0:
+                        got = interp.eval_batch(grid, pts, order="given", stream=st)
+                    elif mode == 1:
+                        got = interp.eval_batch(grid, pts, order="sort", stream=st)
+                    elif mode == 2:
+                        got = interp.eval_batch(grid, interp.prepare(grid, pts), stream=st)
+                    else:
+                        host = pts.cpu().pin_memory()
+                        got = interp.eval_batch(grid, host, out=torch.empty(host.shape[0]).pin_memory(), stream=st)
+                    st.synchronize()
+                    torch.testing.assert_close(got.cpu(), want, rtol=0, atol=0)
+                    if tid == 0:
+                        tex = interp0.eval_batch_texture(grid0, pts0, stream=st)
+                        st.synchronize()
+                        torch.testing.assert_close(tex.cpu(), tex_want, rtol=0, atol=0)
+        except Exception as e:  # noqa: BLE001
+            errors.append((tid, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
