@@ -488,6 +488,11 @@ def run_ours(args):
         interp.eval_batch(grid, shuffled, out=out, check=False, order="sort")
 
     ms_b = measure(unsorted_step, max(2, min(args.steps // 4, 10)), 1, stream, dist)
+
+    def unordered_step():  # values left in brick order, paired with the permutation
+        interp.eval_batch_unordered(grid, shuffled, check=False, stream=stream)
+
+    ms_u = measure(unordered_step, max(2, min(args.steps // 4, 10)), 1, stream, dist)
     del shuffled
     torch.cuda.empty_cache()
 
@@ -523,6 +528,10 @@ def run_ours(args):
                                 "note": "protocol B: shuffled points; Morton keys + sort + brick runs + eval reading "
                                         "the points through the permutation + scatter to caller order, all "
                                         "timed"},
+        "unsorted_unordered_device": {"value": world * n / (ms_u * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_u,
+                                      "note": "protocol B for reductions: shuffled points; sort + brick kernel "
+                                              "reading through the permutation, values returned in brick order with "
+                                              "the permutation (eval_batch_unordered), all timed"},
         "roofline_onchip": onchip_roofline(plan, esize, n / (ms * 1e-3), clk.summary().get("sm_mhz")),
         "texture_variant": texture,
         "gpu_launches": int(args.steps * launches_per_step),

@@ -181,6 +181,14 @@ int sp_eval_bricks_indirect(const sp_plan* plan, const sp_grid_desc* grid, const
                             const int64_t* brick_start, const int32_t* n_bricks_dev, int32_t n_bricks_cap,
                             int32_t log2_brick, const int32_t* perm, void* out, int32_t* err_flag, void* stream);
 
+/* sp_eval_bricks_unordered: as sp_eval_bricks_indirect, but the value of brick-order point i
+ * (= pts[perm[i]]) is written to out[i] — results stay in brick order, pairing with perm,
+ * for callers that reduce over the batch (error norms, sums) and need no caller order: the
+ * random result writes (a read-modify-write of a whole DRAM burst per 4-byte value) vanish. */
+int sp_eval_bricks_unordered(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
+                             const int64_t* brick_start, const int32_t* n_bricks_dev, int32_t n_bricks_cap,
+                             int32_t log2_brick, const int32_t* perm, void* out, int32_t* err_flag, void* stream);
+
 /* Synchronous convenience: sp_eval + stream sync + sentinel check (SP_ERR_SENTINEL). */
 int sp_eval_sync(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
                  void* out, void* stream);

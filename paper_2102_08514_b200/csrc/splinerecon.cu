@@ -1182,6 +1182,29 @@ extern "C" int sp_eval_bricks_indirect(const sp_plan* plan, const sp_grid_desc* 
     return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
 }
 
+// Unordered protocol B: brick-order point i is pts[perm[i]], its value goes to out[i] (brick
+// order, coalesced) — no scatter back to the caller's order.
+extern "C" int sp_eval_bricks_unordered(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n,
+                                        int32_t dtype, const int64_t* brick_start, const int32_t* n_bricks_dev,
+                                        int32_t n_bricks_cap, int32_t log2_brick, const int32_t* perm, void* out,
+                                        int32_t* err_flag, void* stream) {
+    if (!plan) return fail(SP_ERR_INVALID, "null plan");
+    int rc = check_grid(plan, grid, dtype);
+    if (rc != SP_OK) return rc;
+    if (n < 0 || n_bricks_cap < 0) return fail(SP_ERR_INVALID, "negative size");
+    if (n == 0 || n_bricks_cap == 0) return SP_OK;
+    if (log2_brick < 0 || log2_brick > 20) return fail(SP_ERR_INVALID, "log2_brick out of range");
+    if (!pts || !out || !brick_start || !n_bricks_dev || !perm) return fail(SP_ERR_INVALID, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == SP_F32)
+        return eval_bricks_typed<float>(plan, grid, pts, n, brick_start, n_bricks_cap, log2_brick, nullptr, out,
+                                        err_flag, st, n_bricks_dev, nullptr, perm);
+    if (dtype == SP_F64)
+        return eval_bricks_typed<double>(plan, grid, pts, n, brick_start, n_bricks_cap, log2_brick, nullptr, out,
+                                         err_flag, st, n_bricks_dev, nullptr, perm);
+    return fail(SP_ERR_INVALID, "unknown dtype %d", dtype);
+}
+
 extern "C" int sp_morton_keys(const void* pts, int64_t n, int32_t dtype, uint64_t* keys, void* stream) {
     if (n <= 0) return SP_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

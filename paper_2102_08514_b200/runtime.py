@@ -581,7 +581,40 @@ class PlanInterpreter:
             self.eval_batch(grid, pts, out=out, check=False, **kw)
         return g
 
-    def _eval_sorted32(self, grid, p, res, b, frame, st, err):
+    def eval_batch_unordered(self, grid: CoefficientGrid, pts: torch.Tensor, *, check: bool = True,
+                             stream: torch.cuda.Stream | None = None):
+        """Protocol B without the return to caller order: (values, perm) with values[k] the
+        reconstruction at pts[perm[k]] (perm int64 on the grid's device; Morton brick order),
+        bit-identical to eval_batch(grid, pts)[perm].  For reductions over the batch (error
+        norms, sums, histograms) the random per-value result writes of eval_batch(order=
+        "sort") are skipped (sp_eval_bricks_unordered).  Device points, 3-D plans."""
+        self._check_grid(grid)
+        if self._lift is not None or self.plan.s != 3:
+            raise NotImplementedError("eval_batch_unordered: 3-D plans only")
+        if not isinstance(pts, torch.Tensor) or pts.device != grid.device or pts.dim() != 2 or pts.shape[1] != 3:
+            raise RuntimeError_("points must be an (n, 3) tensor on the grid's device")
+        p = pts.to(dtype=grid.dtype).contiguous()
+        n = p.shape[0]
+        st = stream if stream is not None else torch.cuda.current_stream(grid.device)
+        b = self.brick_log2(grid)
+        frame = _sort_frame(grid, b) if b >= 0 else None
+        if frame is None or not 0 < n < (1 << 31):  # no brick mode / wide grid: caller order
+            with torch.cuda.stream(st):
+                perm = torch.arange(n, device=grid.device)
+            return self.eval_batch(grid, p, check=check, order="given", stream=st), perm
+        err = torch.zeros(1, dtype=torch.int32, device=grid.device) if check else None
+        with torch.cuda.stream(st):
+            res = torch.empty(n, dtype=grid.dtype, device=grid.device)
+        perm32 = self._eval_sorted32(grid, p, res, b, frame, st, err, unordered=True)
+        with torch.cuda.stream(st):
+            perm = perm32.to(torch.int64)
+        if check:
+            st.synchronize()
+            if int(err.item()):
+                raise RuntimeError_("sigma sentinel hit in batch evaluation")
+        return res, perm
+
+    def _eval_sorted32(self, grid, p, res, b, frame, st, err, unordered=False):
         """Protocol B without host round trips: sp_sort_points (30-bit Morton keys in the
         grid's frame, CUB pair sort, brick runs) then sp_eval_bricks_indirect (the brick
         kernel reads the caller's points through the permutation and scatters the results
@@ -613,9 +646,18 @@ class PlanInterpreter:
         gdesc = grid.descriptor()
         gather = self.sort_gather
         with torch.cuda.stream(st):
+            if unordered:  # the permutation is returned: not the cached workspace's
+                perm = torch.empty(n, dtype=torch.int32, device=dev)
+                gather = False
             _native.check(lib.sp_sort_points(p.data_ptr(), n, dtype, lo0, lo1, lo2, bits, b,
                                              sp_.data_ptr() if gather else None, perm.data_ptr(), start.data_ptr(),
                                              count.data_ptr(), tmp.data_ptr(), tmp.numel(), st.cuda_stream))
+            if unordered:
+                _native.check(lib.sp_eval_bricks_unordered(h, ctypes.byref(gdesc), p.data_ptr(), n, dtype,
+                                                           start.data_ptr(), count.data_ptr(), n, b, perm.data_ptr(),
+                                                           res.data_ptr(), None if err is None else err.data_ptr(),
+                                                           st.cuda_stream))
+                return perm
             fn = lib.sp_eval_bricks_perm32 if gather else lib.sp_eval_bricks_indirect
             _native.check(fn(h, ctypes.byref(gdesc), (sp_ if gather else p).data_ptr(), n, dtype, start.data_ptr(),
                              count.data_ptr(), n, b, perm.data_ptr(), res.data_ptr(),

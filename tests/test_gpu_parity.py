@@ -402,6 +402,31 @@ def test_sorted32_protocol_b_matches_given_order(name, dtype, gather, cuda):
     torch.testing.assert_close(got2, want[:1000], rtol=0, atol=0, equal_nan=True)
 
 
+@pytest.mark.parametrize("name,dtype", [("cc_tricubic", torch.float32), ("bcc_quintic_rd", torch.float64),
+                                        ("fcc_cubic", torch.float32)])
+def test_unordered_protocol_b_matches_permuted_values(name, dtype, cuda):
+    """eval_batch_unordered (sp_sort_points + sp_eval_bricks_unordered: values left in brick
+    order) returns a permutation of the points and values bit-identical to eval_batch at
+    those points, including points outside the grid and NaN; a sentinel-free batch passes
+    check=True."""
+    g, plan, grid = _setup(name, "zero", dtype, cuda)
+    interp = PlanInterpreter(plan)
+    rng = np.random.default_rng(23)
+    hi = max(a.shape[0] for a in grid.arrays) * plan.diag[0]
+    pts = rng.uniform(-3, hi + 3, size=(150_000, 3))
+    pts[:40] = rng.uniform(-1e4, 1e4, size=(40, 3))
+    pts[40:50, 1] = np.nan
+    rng.shuffle(pts)
+    p = torch.from_numpy(pts).to(cuda, dtype)
+    want = interp.eval_batch(grid, p, order="given")
+    vals, perm = interp.eval_batch_unordered(grid, p)
+    assert perm.dtype == torch.int64 and vals.dtype == dtype
+    assert torch.equal(torch.sort(perm).values, torch.arange(p.shape[0], device=cuda))
+    torch.testing.assert_close(vals, want[perm], rtol=0, atol=0, equal_nan=True)
+    v2, perm2 = interp.eval_batch_unordered(grid, p[:1000])  # another size
+    torch.testing.assert_close(v2, want[:1000][perm2], rtol=0, atol=0, equal_nan=True)
+
+
 def test_sort_frame_falls_back_for_wide_grids(cuda):
     from paper_2102_08514_b200.runtime import _sort_frame
 

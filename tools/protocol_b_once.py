@@ -16,15 +16,22 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default=bench.HEADLINE)
     ap.add_argument("--gather", type=int, default=0)
+    ap.add_argument("--unordered", type=int, default=0)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     plan, grid, pts, interp = bench.make_workload(a.workload, 0, dev, order="random")
     interp.sort_gather = bool(a.gather)
     out = torch.empty(pts.shape[0], dtype=grid.dtype, device=dev)
-    interp.eval_batch(grid, pts, out=out, check=False, order="sort")
+    def step():
+        if a.unordered:
+            interp.eval_batch_unordered(grid, pts, check=False)
+        else:
+            interp.eval_batch(grid, pts, out=out, check=False, order="sort")
+
+    step()
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
-    interp.eval_batch(grid, pts, out=out, check=False, order="sort")
+    step()
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
 
