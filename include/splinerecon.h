@@ -160,7 +160,8 @@ int sp_eval_bricks_dev(const sp_plan* plan, const sp_grid_desc* grid, const void
  * sp_sort_points: 30-bit Morton keys of the points' unit cells relative to (lo0, lo1, lo2)
  * with `bits` (<= 10) per axis — cells outside [lo, lo + 2^bits) are clamped, which only
  * affects the order (any brick partition is evaluated correctly) — a radix sort of (key,
- * index) pairs, the points gathered into key order (sorted_pts, same dtype/shape as pts),
+ * index) pairs over whole 8-bit digits (the lowest 3*bits % 8 key bits, inside a brick, are
+ * left unsorted), the points gathered into key order (sorted_pts, same dtype/shape as pts),
  * (skipped when sorted_pts is NULL), the int32 permutation (perm[i] = caller index of sorted
  * point i) and the brick runs
  * (brick_start [n+1], brick count in device memory), all stream-ordered; n < 2^31.

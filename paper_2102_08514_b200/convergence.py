@@ -114,8 +114,11 @@ def run_convergence(plan, target: Target, *, prefilter: Mapping | None = None, h
         if prefilter is not None:
             grid = apply_prefilter(grid, prefilter)
         y = x / h + torch.tensor(center, dtype=torch.float64, device=device)
-        s = interp.eval_batch(grid, y.to(dtype), order="sort").to(torch.float64)
-        err = s - fx
+        if plan.s == 3:  # norms need no caller order: values in brick order + permutation
+            s, perm = interp.eval_batch_unordered(grid, y.to(dtype))
+            err = s.to(torch.float64) - fx[perm]
+        else:
+            err = interp.eval_batch(grid, y.to(dtype), order="sort").to(torch.float64) - fx
         rep.scales.append(h)
         rep.errors.append(float(torch.sqrt((err * err).mean())))
         rep.max_errors.append(float(err.abs().max()))

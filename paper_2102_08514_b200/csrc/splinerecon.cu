@@ -1120,7 +1120,15 @@ extern "C" int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t
         morton32_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, n, lo0, lo1, lo2, bits, k_in);
     iota32_kernel<<<grid_for(n), 256, 0, st>>>(iota, n);
     size_t cb = cub_bytes;
-    if (e == cudaSuccess) e = cub::DeviceRadixSort::SortPairs(cub_tmp, cb, k_in, k_out, iota, perm, (int)n, 0, end_bit, st);
+    // The lowest end_bit % 8 key bits (the finest Morton levels inside a brick) stay unsorted
+    // so that the radix sort runs whole 8-bit passes only: 27-bit keys sort in 3 passes, not 4
+    // (tools/sort_bits_probe.py: -0.45 ms per 1e8 points, brick kernel unaffected).  Brick runs
+    // need the brick bits sorted, so at most 3*log2_brick bits are left; SP_SORT_BEGIN_BIT
+    // overrides (experiments).
+    static const int begin_env = env_int("SP_SORT_BEGIN_BIT", -1);
+    const int bb = std::min(begin_env >= 0 ? std::min(begin_env, 9) : end_bit % 8, 3 * log2_brick);
+    if (e == cudaSuccess)
+        e = cub::DeviceRadixSort::SortPairs(cub_tmp, cb, k_in, k_out, iota, perm, (int)n, bb, end_bit, st);
     if (e == cudaSuccess) {
         if (sorted_pts && dtype == SP_F32)
             gather_points32_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, perm, n, (float*)sorted_pts);

@@ -584,7 +584,8 @@ class PlanInterpreter:
     def eval_batch_unordered(self, grid: CoefficientGrid, pts: torch.Tensor, *, check: bool = True,
                              stream: torch.cuda.Stream | None = None):
         """Protocol B without the return to caller order: (values, perm) with values[k] the
-        reconstruction at pts[perm[k]] (perm int64 on the grid's device; Morton brick order),
+        reconstruction at pts[perm[k]] (perm int32 on the grid's device — a valid index tensor,
+        int64 from 2^31 points; Morton brick order),
         bit-identical to eval_batch(grid, pts)[perm].  For reductions over the batch (error
         norms, sums, histograms) the random per-value result writes of eval_batch(order=
         "sort") are skipped (sp_eval_bricks_unordered).  Device points, 3-D plans."""
@@ -600,14 +601,12 @@ class PlanInterpreter:
         frame = _sort_frame(grid, b) if b >= 0 else None
         if frame is None or not 0 < n < (1 << 31):  # no brick mode / wide grid: caller order
             with torch.cuda.stream(st):
-                perm = torch.arange(n, device=grid.device)
+                perm = torch.arange(n, dtype=torch.int32 if n < (1 << 31) else torch.int64, device=grid.device)
             return self.eval_batch(grid, p, check=check, order="given", stream=st), perm
         err = torch.zeros(1, dtype=torch.int32, device=grid.device) if check else None
         with torch.cuda.stream(st):
             res = torch.empty(n, dtype=grid.dtype, device=grid.device)
-        perm32 = self._eval_sorted32(grid, p, res, b, frame, st, err, unordered=True)
-        with torch.cuda.stream(st):
-            perm = perm32.to(torch.int64)
+        perm = self._eval_sorted32(grid, p, res, b, frame, st, err, unordered=True)
         if check:
             st.synchronize()
             if int(err.item()):

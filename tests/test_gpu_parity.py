@@ -420,8 +420,8 @@ def test_unordered_protocol_b_matches_permuted_values(name, dtype, cuda):
     p = torch.from_numpy(pts).to(cuda, dtype)
     want = interp.eval_batch(grid, p, order="given")
     vals, perm = interp.eval_batch_unordered(grid, p)
-    assert perm.dtype == torch.int64 and vals.dtype == dtype
-    assert torch.equal(torch.sort(perm).values, torch.arange(p.shape[0], device=cuda))
+    assert perm.dtype == torch.int32 and vals.dtype == dtype
+    assert torch.equal(torch.sort(perm).values, torch.arange(p.shape[0], dtype=torch.int32, device=cuda))
     torch.testing.assert_close(vals, want[perm], rtol=0, atol=0, equal_nan=True)
     v2, perm2 = interp.eval_batch_unordered(grid, p[:1000])  # another size
     torch.testing.assert_close(v2, want[:1000][perm2], rtol=0, atol=0, equal_nan=True)
