@@ -1051,6 +1051,34 @@ extern "C" int sp_brick_runs(const uint64_t* keys, int64_t n, int32_t log2_brick
     return SP_OK;
 }
 
+// Brick heads of sorted 32-bit keys scattered by brick id (head[b] = first index of brick b,
+// -1 for empty bricks); a compaction over the brick ids then yields the runs in order
+// without a pass of stream compaction over all n points.
+__global__ void brick_heads32_kernel(const int32_t* __restrict__ keys, long long n, int shift, int* __restrict__ head) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int b = keys[i] >> shift;
+        if (i == 0 || b != (keys[i - 1] >> shift)) head[b] = (int)i;
+    }
+}
+
+struct IsHead {
+    __host__ __device__ bool operator()(int v) const { return v >= 0; }
+};
+
+// morton32 keys fused with the iota of the (key, index) pairs
+template <typename T>
+__global__ void morton32_iota_kernel(const T* __restrict__ pts, long long n, int lo0, int lo1, int lo2, int bits,
+                                     int* __restrict__ keys, int* __restrict__ iota) {
+    const int hi = (1 << bits) - 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int c0 = min(max(sp::clamp_cell(pts[3 * i]) - lo0, 0), hi);
+        const int c1 = min(max(sp::clamp_cell(pts[3 * i + 1]) - lo1, 0), hi);
+        const int c2 = min(max(sp::clamp_cell(pts[3 * i + 2]) - lo2, 0), hi);
+        keys[i] = (int)(spread3((uint32_t)c2) | (spread3((uint32_t)c1) << 1) | (spread3((uint32_t)c0) << 2));
+        iota[i] = (int)i;
+    }
+}
+
 // 32-bit brick heads for sp_sort_points
 struct BrickHead32 {
     const int32_t* keys;
@@ -1115,10 +1143,10 @@ extern "C" int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t
     void* cub_tmp = base + 3 * seg;
     cudaError_t e = cudaSuccess;
     if (dtype == SP_F32)
-        morton32_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, n, lo0, lo1, lo2, bits, k_in);
+        morton32_iota_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, n, lo0, lo1, lo2, bits, k_in, iota);
     else
-        morton32_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, n, lo0, lo1, lo2, bits, k_in);
-    iota32_kernel<<<grid_for(n), 256, 0, st>>>(iota, n);
+        morton32_iota_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, n, lo0, lo1, lo2, bits, k_in,
+                                                                   iota);
     size_t cb = cub_bytes;
     // The lowest end_bit % 8 key bits (the finest Morton levels inside a brick) stay unsorted
     // so that the radix sort runs whole 8-bit passes only: 27-bit keys sort in 3 passes, not 4
@@ -1134,10 +1162,28 @@ extern "C" int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t
             gather_points32_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, perm, n, (float*)sorted_pts);
         else if (sorted_pts)
             gather_points32_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, perm, n, (double*)sorted_pts);
-        thrust::counting_iterator<long long> idx(0);
-        const BrickHead32 head{k_out, 3 * log2_brick};
-        cb = cub_bytes;
-        e = cub::DeviceSelect::If(cub_tmp, cb, idx, brick_start, n_bricks, (int)n, head, st);
+        // brick runs: scatter of the heads by brick id + compaction over the (<= n) brick ids
+        // when the frame has at most n bricks (the iota segment is free after the sort), else
+        // stream compaction over the n sorted keys
+        const int nbf = 3 * (bits - log2_brick);
+        const long long nb = 1ll << nbf;
+        size_t sel = 0;
+        if (nb <= n)
+            cub::DeviceSelect::If(nullptr, sel, iota, brick_start, n_bricks, (int)nb, IsHead{}, st);
+        if (nb <= n && sel <= cub_bytes) {
+            e = cudaMemsetAsync(iota, 0xff, (size_t)nb * 4, st);
+            if (e == cudaSuccess) {
+                brick_heads32_kernel<<<grid_for(n), 256, 0, st>>>(k_out, n, 3 * log2_brick, iota);
+                e = cudaGetLastError();
+            }
+            cb = cub_bytes;
+            if (e == cudaSuccess) e = cub::DeviceSelect::If(cub_tmp, cb, iota, brick_start, n_bricks, (int)nb, IsHead{}, st);
+        } else {
+            thrust::counting_iterator<long long> idx(0);
+            const BrickHead32 head{k_out, 3 * log2_brick};
+            cb = cub_bytes;
+            e = cub::DeviceSelect::If(cub_tmp, cb, idx, brick_start, n_bricks, (int)n, head, st);
+        }
     }
     if (e == cudaSuccess) {
         brick_runs_tail<<<1, 1, 0, st>>>(n, n_bricks, brick_start);
