@@ -214,3 +214,21 @@ def test_choose_order_sample_indices_stay_in_range():
 
     big = (torch.rand(1, 3, dtype=torch.float64) * 50).expand(100_000_000, 3)  # 1e8 rows, stride-0 view
     assert choose_order(big) == "morton"  # identical points: every pair is non-decreasing
+
+
+def test_eval_batch_unordered_rejects_host_inputs():
+    """eval_batch_unordered (protocol B, values in brick order + permutation) has no CPU
+    host fallback: non-tensor and wrongly shaped points are refused loudly."""
+    import torch
+
+    from paper_2102_08514_b200 import corpus
+    from paper_2102_08514_b200.runtime import CoefficientGrid, PlanInterpreter, RuntimeError_
+
+    plan = corpus.build_plan("cc_trilinear")
+    _, cos = corpus.lattice_of("cc_trilinear")
+    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [7, 7, 7], device="cpu", dtype=torch.float32)
+    interp = PlanInterpreter(plan)
+    with pytest.raises(RuntimeError_):
+        interp.eval_batch_unordered(grid, torch.zeros(4, 2))
+    with pytest.raises(RuntimeError_):
+        interp.eval_batch_unordered(grid, np.zeros((4, 3)))
