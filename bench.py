@@ -50,10 +50,12 @@ WORKLOADS = {
     "bcc_quintic_2x203_fp32": ("bcc_quintic_rd", 405, "float32", 100_000_000),
     "fcc6_4x161_fp32": ("fcc_cubic", 321, "float32", 100_000_000),
     "zp3_cc256_fp32": ("cc_zp3", 255, "float32", 100_000_000),
-    # C5 geometry (BCC 2x406^3 = 512^3-equivalent samples, 10^9 points per GPU); the Voronoi
-    # splines themselves have no PP data in the reference, so the BCC
-    # linear box spline stands in for the throughput/scaling measurement
-    "c5_bcc_linear_2x406_1e9_fp32": ("bcc_linear_rd", 811, "float32", 1_000_000_000),
+    # C5: Voronoi splines V1 at 512^3-equivalent samples (BCC 2x406^3, FCC 4x322^3), 10^9 points
+    # per GPU.  PP data: tools/voronoi_pp.py (reference exact tools), plans: reference compiler.
+    "c5_fcc_voronoi1_4x322_1e9_fp32": ("fcc_voronoi1", 643, "float32", 1_000_000_000),
+    "c5_bcc_voronoi1_2x406_1e9_fp32": ("bcc_voronoi1", 811, "float32", 1_000_000_000),
+    # the BCC linear box spline on the C5 BCC geometry (HBM-bound reference point)
+    "bcc_linear_2x406_1e9_fp32": ("bcc_linear_rd", 811, "float32", 1_000_000_000),
 }
 HEADLINE = "tricubic_cc256_fp32"
 

@@ -34,6 +34,7 @@ PLANS = os.path.join(ROOT, "paper_2102_08514_b200", "plans")
 E3 = [(1, 0, 0), (0, 1, 0), (0, 0, 1)]
 DIAG = [(1, 1, 1), (-1, 1, 1), (1, -1, 1), (1, 1, -1)]
 EXTRA = {"cc_tricubic": E3 * 4, "cc_zp3": E3 + DIAG, "bcc_quartic": DIAG + E3 + E3}
+VORONOI_LAT = {"fcc_voronoi1": "FCC", "bcc_voronoi1": "BCC"}
 EXTRA_LAT = {"cc_tricubic": "CC3", "cc_zp3": "CC3", "bcc_quartic": "BCC"}
 
 # grid hi per lattice (lo = 0): small enough for brute force, large enough for halos
@@ -48,6 +49,11 @@ def _sol(name, ref):
 
     if name in corpus.DIRECTION_SETS:
         return corpus.build_pair(name)
+    if name in VORONOI_LAT:
+        # PP data made by tools/voronoi_pp.py, imported through spline.py:667-713
+        sp = import_pp_spline(open(os.path.join(HERE, "voronoi", f"{name}.spp")).read(), validate=False)
+        lat = named_lattice(VORONOI_LAT[name])
+        return SplineOnLattice(sp, lat, decompose_cartesian(lat))
     cache = os.path.join(os.environ["SPLINEPLAN_CACHE"], f"{name}.spp")
     if not os.path.exists(cache):
         return None

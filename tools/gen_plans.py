@@ -27,6 +27,10 @@ EXTRA = {
     "cc_zp3": (E3 + DIAG, "CC3"),
     "bcc_quartic": (DIAG + E3 + E3, "BCC"),
 }
+# Voronoi splines: PP data built by tools/voronoi_pp.py from the reference's exact tools
+# and imported through the reference's own import path (spline.py:667-713).
+VORONOI = {"fcc_voronoi1": "FCC", "bcc_voronoi1": "BCC"}
+SPP_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "voronoi")
 
 
 def build(name: str, grouped: bool = True):
@@ -40,6 +44,19 @@ def build(name: str, grouped: bool = True):
     t0 = time.time()
     if name in corpus.DIRECTION_SETS:
         plan = corpus.build_plan(name)
+    elif name in VORONOI:
+        from splineplan.plancompile import PlanOptions
+        from splineplan.spline import import_pp_spline
+
+        sp = import_pp_spline(open(os.path.join(SPP_DIR, f"{name}.spp")).read(), validate=True)
+        print(f"[{name}] imported {len(sp.pieces)} pieces in {time.time()-t0:.1f}s", flush=True)
+        lat = named_lattice(VORONOI[name])
+        sol = SplineOnLattice(sp, lat, decompose_cartesian(lat))
+        roe = enumerate_subregions(sol)
+        print(f"[{name}] N={roe.N} Q={roe.Q} r={roe.r} ({time.time()-t0:.1f}s)", flush=True)
+        sym = search_symmetry(roe)
+        print(f"[{name}] K={sym.K} ({time.time()-t0:.1f}s)", flush=True)
+        plan = compile_plan(sol, roe, sym, options=PlanOptions(grouped=grouped))
     else:
         cols, latname = EXTRA[name]
         cache = os.path.join(os.environ["SPLINEPLAN_CACHE"], f"{name}.spp")
