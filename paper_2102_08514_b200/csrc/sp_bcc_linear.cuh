@@ -1,0 +1,287 @@
+// sp_bcc_linear.cuh — closed-form brick kernel for the BCC linear box spline (bcc_linear_rd).
+//
+// The reference evaluates bcc_linear_rd (4 body diagonals on BCC, scale |det L| = 4) as
+// Algorithm 1 (runtime.py:363-408): per coset the coset frame, six plane
+// tests, sigma, a class transform (signed permutation) and two affine weight polynomials
+// of one 2-site fetch group.  The spline is the linear rhombic-dodecahedron box spline
+// (Table 1, 4 lookups), i.e. barycentric interpolation on the BCC Delaunay
+// tetrahedra, and the whole per-class machinery folds into a few warp-uniform min/max
+// operations (the paper's symmetry folding, done arithmetically):
+//
+//   y = x - (1,1,1)                  (non-centred support sum [0, xi])
+//   E = 2 rint(y/2)                  nearest even site (coset 0), d = y - E in [-1,1]^3
+//   s = sign(d), w = |d|; a = argmax w, b = argmin w, m = the middle axis
+//   f = (1 - (w_a+w_m)/2) c[E] + (w_a-w_m)/2 c[E + 2 s_a e_a]
+//     + (w_m+w_b)/2 c[E + s] + (w_m-w_b)/2 c[E + s - 2 s_b e_b]          (odd sites: coset 1)
+//
+// Every reflection / permutation is a select on lane-local data, so all lanes run the same
+// instruction stream (no sigma table, no class records, no kernel switch).  The formula is the
+// plan's function exactly (tests/test_codegen_affine.py checks it against the reference
+// outputs in float64 to ~1e-16); ties between tetrahedra pick a neighbour with the same
+// (continuous) value.  Points are read four per thread (3 x 16-byte loads) and the results
+// written with one 16-byte store.  Non-finite points give NaN (as every evaluator); points
+// outside the fast domain (|x| >= kFast) or outside their run's brick take the same formula in
+// float64 with policy-checked global reads.
+#pragma once
+
+#include "sp_common.cuh"
+
+namespace sp {
+
+template <typename T>
+struct BccTetTraits;
+template <>
+struct BccTetTraits<float> {
+    static constexpr float kFast = 4194304.0f;  // 2^22: x - 1 and the cell indices are exact
+};
+template <>
+struct BccTetTraits<double> {
+    static constexpr double kFast = 1073741824.0;  // 2^30: cell indices fit int
+};
+
+// Tetrahedron selection, shared by every path (same operations -> same bits everywhere).
+template <typename R>
+struct TetSel {
+    int e0, e1, e2;     // coset-0 cell of the nearest even site E = 2 e
+    bool n0, n1, n2;    // d_i < 0 (s_i = -1)
+    bool c01, c02, c12; // |d_0| >= |d_1| etc.
+    R wa, wb, wm;       // largest, smallest, middle |d_i|
+};
+
+template <typename R>
+__device__ __forceinline__ TetSel<R> tet_select(R y0, R y1, R y2) {
+    TetSel<R> t;
+    const R f0 = rint(y0 * R(0.5)), f1 = rint(y1 * R(0.5)), f2 = rint(y2 * R(0.5));
+    const R d0 = fma(f0, R(-2), y0), d1 = fma(f1, R(-2), y1), d2 = fma(f2, R(-2), y2);
+    t.e0 = (int)f0;
+    t.e1 = (int)f1;
+    t.e2 = (int)f2;
+    t.n0 = d0 < R(0);
+    t.n1 = d1 < R(0);
+    t.n2 = d2 < R(0);
+    const R w0 = fabs(d0), w1 = fabs(d1), w2 = fabs(d2);
+    t.c01 = w0 >= w1;
+    t.c02 = w0 >= w2;
+    t.c12 = w1 >= w2;
+    const R mx01 = fmax(w0, w1), mn01 = fmin(w0, w1);
+    t.wa = fmax(mx01, w2);
+    t.wb = fmin(mn01, w2);
+    t.wm = fmax(mn01, fmin(mx01, w2));
+    return t;
+}
+
+// axis (0/1/2) of the largest / smallest |d| (distinct, also at ties)
+template <typename R>
+__device__ __forceinline__ int tet_axis_a(const TetSel<R>& t) { return t.c01 ? (t.c02 ? 0 : 2) : (t.c12 ? 1 : 2); }
+template <typename R>
+__device__ __forceinline__ int tet_axis_b(const TetSel<R>& t) { return t.c01 ? (t.c12 ? 2 : 1) : (t.c02 ? 2 : 0); }
+
+// sites E, E + 2 s_a e_a (coset 0) and E + s, E + s - 2 s_b e_b (coset 1)
+template <typename R>
+__device__ __forceinline__ R tet_combine(const TetSel<R>& t, R cE, R cA, R cO, R cB) {
+    R acc = (R(2) - t.wa - t.wm) * cE;
+    acc = fma(t.wa - t.wm, cA, acc);
+    acc = fma(t.wm + t.wb, cO, acc);
+    acc = fma(t.wm - t.wb, cB, acc);
+    return acc * R(0.5);
+}
+
+// One point from the staged brick tile: both coset boxes have strides (E*E, E, 1), coset 1
+// at offset E^3; `base` = tile index of coset-0 cell (0,0,0) (may be negative).
+template <int E, typename T>
+__device__ __forceinline__ T bcc_tet_tile(T y0, T y1, T y2, const T* __restrict__ tile, int base) {
+    constexpr int S0 = E * E, S1 = E, ODD = E * E * E;
+    const TetSel<T> t = tet_select<T>(y0, y1, y2);
+    const int ss0 = t.n0 ? -S0 : S0, ss1 = t.n1 ? -S1 : S1, ss2 = t.n2 ? -1 : 1;
+    const int sa = t.c01 ? (t.c02 ? ss0 : ss2) : (t.c12 ? ss1 : ss2);
+    const int sb = t.c01 ? (t.c12 ? ss2 : ss1) : (t.c02 ? ss2 : ss0);
+    const int iE = base + t.e0 * S0 + t.e1 * S1 + t.e2;
+    const int iO = iE + ODD - ((t.n0 ? S0 : 0) + (t.n1 ? S1 : 0) + (t.n2 ? 1 : 0));
+    SP_CHECK(iE >= 0 && iE + sa >= 0 && iE + sa < ODD && iO < 2 * ODD && iO - sb >= ODD && iO - sb < 2 * ODD);
+    return tet_combine<T>(t, tile[iE], tile[iE + sa], tile[iO], tile[iO - sb]);
+}
+
+// Any point through two coset fetchers (TileFetch / GlobalFetch, bound per coset by `bindk`).
+template <typename R, typename T, class F, class Bind>
+__device__ __forceinline__ R bcc_tet_fetch(R y0, R y1, R y2, F& f, Bind bindk) {
+    const TetSel<R> t = tet_select<R>(y0, y1, y2);
+    const int ia = tet_axis_a(t), ib = tet_axis_b(t);
+    const int s0 = t.n0 ? -1 : 1, s1 = t.n1 ? -1 : 1, s2 = t.n2 ? -1 : 1;
+    const int e[3] = {t.e0, t.e1, t.e2};
+    bindk(f, 0, e);
+    const R cE = (R)f.get(0, 0, 0);
+    const R cA = (R)f.get(ia == 0 ? s0 : 0, ia == 1 ? s1 : 0, ia == 2 ? s2 : 0);
+    const int o[3] = {t.e0 - (int)t.n0, t.e1 - (int)t.n1, t.e2 - (int)t.n2};
+    bindk(f, 1, o);
+    const R cO = (R)f.get(0, 0, 0);
+    const R cB = (R)f.get(ib == 0 ? -s0 : 0, ib == 1 ? -s1 : 0, ib == 2 ? -s2 : 0);
+    return tet_combine<R>(t, cE, cA, cO, cB);
+}
+
+// Slow path of the brick kernel: policy-checked global reads; R = T inside the fast domain
+// (the same arithmetic as the tile path and BccTetEval), float64 beyond it.
+template <typename R, typename T>
+__device__ __forceinline__ T bcc_tet_global(const EvalArgs<T>& a, R y0, R y1, R y2) {
+    GlobalFetch<T> f;
+    return (T)bcc_tet_fetch<R, T>(y0, y1, y2, f, [&](GlobalFetch<T>& ff, int k, const int* base) {
+        ff.frame_identity(a.grid, k, base);
+    });
+}
+
+// The same function as an evaluator for the generic drivers (chunk kernel, indirect brick
+// kernel): identical values, bit for bit, to bcc_tet_brick_kernel.  Reads coset cells up to
+// 2 around floor((x - l)/2) (sp_plan_create widens the plan's reach for it).
+template <typename T>
+struct BccTetEval {
+    static constexpr int kMinBlocks = 4;
+    static constexpr bool kSig = false;
+    static constexpr int kSigCount = 1;
+    template <typename U>
+    static constexpr int vec_width() {
+        return 0;
+    }
+    __device__ static void tile_records(const EvalArgs<T>&, const TileGeom&, const unsigned char*, int4*, int) {}
+    template <class Ctx>
+    __device__ __forceinline__ static unsigned classify_word(const T*, const Ctx&) { return 0u; }
+    __device__ __forceinline__ static int signature(unsigned, const unsigned char*) { return 0; }
+    template <class F, class Ctx>
+    __device__ __forceinline__ static T eval_word(const T x[3], unsigned, F& f, const Ctx& ctx) {
+        return eval<F, Ctx>(x, f, ctx);
+    }
+    template <class F, class Ctx>
+    __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {
+        constexpr T kF = BccTetTraits<T>::kFast;
+        auto bindk = [&](F& ff, int k, const int* base) { bind_identity(ff, *ctx.a, *ctx.geom, k, base); };
+        if (fabs(x[0]) < kF && fabs(x[1]) < kF && fabs(x[2]) < kF)
+            return bcc_tet_fetch<T, T>(x[0] - T(1), x[1] - T(1), x[2] - T(1), f, bindk);
+        return (T)bcc_tet_fetch<double, T>((double)x[0] - 1.0, (double)x[1] - 1.0, (double)x[2] - 1.0, f, bindk);
+    }
+};
+
+// One CTA per brick (grid-strided).  Box per coset: coset cells [c/2 - 3, c/2 + B/2] per axis
+// (E = B/2 + 4; covers every cell the formula can address for points of the brick, including
+// zero-weight ones at ties), same shape for both cosets, staged with the grid's boundary
+// policy (stage_box).  Points: quads of 4 consecutive brick-order points per thread.
+template <typename T, int L2B>
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 2)
+    bcc_tet_brick_kernel(const EvalArgs<T> a, const long long* __restrict__ brick_start, int nbricks) {
+    constexpr int B = 1 << L2B;
+    constexpr int E = B / 2 + 4;
+    constexpr int VOL = E * E * E;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* tile = reinterpret_cast<T*>(smem);
+    __shared__ int corner[3];
+    const int tid = threadIdx.x;
+    if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);
+    unsigned m2, s2, m1, s1;
+    fastdiv_magic((unsigned)E, m2, s2);
+    m1 = m2;
+    s1 = s2;
+    for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
+        const long long p0 = brick_start[b], p1 = brick_start[b + 1];
+        if (tid == 0) {
+            const T* x = a.pts + 3 * p0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) corner[i] = (clamp_cell(x[i]) >> L2B) << L2B;
+        }
+        __syncthreads();
+        const int c0 = corner[0], c1 = corner[1], c2 = corner[2];
+        // stage both coset boxes (policy resolved here)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int z0b = (c0 >> 1) - 3 - a.grid.org[k][0];
+            const int z1b = (c1 >> 1) - 3 - a.grid.org[k][1];
+            const int z2b = (c2 >> 1) - 3 - a.grid.org[k][2];
+            const int g0 = a.grid.ext[k][0], g1 = a.grid.ext[k][1], g2 = a.grid.ext[k][2];
+            if (a.grid.boundary == SP_ZERO)
+                stage_box<SP_ZERO>(tile + k * VOL, a.grid.data[k], VOL, E, E, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+            else if (a.grid.boundary == SP_CLAMP)
+                stage_box<SP_CLAMP>(tile + k * VOL, a.grid.data[k], VOL, E, E, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+            else
+                stage_box<SP_MIRROR>(tile + k * VOL, a.grid.data[k], VOL, E, E, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // tile index of coset-0 cell (0,0,0); cell e lies in the box iff e - (c/2 - 1) in [0, B/2]
+        const int lo0 = (c0 >> 1) - 3, lo1 = (c1 >> 1) - 3, lo2 = (c2 >> 1) - 3;
+        const int base = -(lo0 * E * E + lo1 * E + lo2);
+        const long long q0 = p0 >> 2, q1 = (p1 + 3) >> 2;
+        for (long long q = q0 + tid; q < q1; q += kThreads) {
+            const long long j0 = q << 2;
+            T xs[12];
+            const bool full = j0 >= p0 && j0 + 4 <= p1;
+            if (j0 + 4 <= a.n) {
+                if constexpr (sizeof(T) == 4) {
+                    const float4* src = reinterpret_cast<const float4*>(a.pts + 3 * j0);
+#pragma unroll
+                    for (int v = 0; v < 3; ++v) {
+                        const float4 t = __ldg(src + v);
+                        xs[4 * v] = t.x;
+                        xs[4 * v + 1] = t.y;
+                        xs[4 * v + 2] = t.z;
+                        xs[4 * v + 3] = t.w;
+                    }
+                } else {
+                    const double2* src = reinterpret_cast<const double2*>(a.pts + 3 * j0);
+#pragma unroll
+                    for (int v = 0; v < 6; ++v) {
+                        const double2 t = __ldg(src + v);
+                        xs[2 * v] = t.x;
+                        xs[2 * v + 1] = t.y;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 12; ++e) xs[e] = j0 + e / 3 < a.n ? __ldg(a.pts + 3 * j0 + e) : T(0);
+            }
+            T r[4];
+            unsigned slow = 0u;  // points for the global path (outside the brick, far or non-finite)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const T x0 = xs[3 * u], x1 = xs[3 * u + 1], x2 = xs[3 * u + 2];
+                constexpr T kF = BccTetTraits<T>::kFast;
+                const T y0 = x0 - T(1), y1 = x1 - T(1), y2 = x2 - T(1);
+                // coset-0 cell of the nearest even site must lie in [c/2-1, c/2+B/2-1]
+                const int r0 = (int)rint(y0 * T(0.5)) - ((c0 >> 1) - 1);
+                const int r1 = (int)rint(y1 * T(0.5)) - ((c1 >> 1) - 1);
+                const int r2 = (int)rint(y2 * T(0.5)) - ((c2 >> 1) - 1);
+                const bool fast = fabs(x0) < kF && fabs(x1) < kF && fabs(x2) < kF &&  // false for NaN
+                                  max(max((unsigned)r0, (unsigned)r1), (unsigned)r2) <= (unsigned)(B / 2);
+                r[u] = fast ? bcc_tet_tile<E, T>(y0, y1, y2, tile, base) : T(0);
+                slow |= fast ? 0u : (1u << u);
+            }
+#pragma unroll 1
+            while (slow) {  // rare: one call site, registers selected (no local-memory arrays)
+                const int u = __ffs(slow) - 1;
+                slow &= slow - 1;
+                auto pick = [&](int o) { return u == 0 ? xs[o] : u == 1 ? xs[3 + o] : u == 2 ? xs[6 + o] : xs[9 + o]; };
+                const T x0 = pick(0), x1 = pick(1), x2 = pick(2);
+                constexpr T kF = BccTetTraits<T>::kFast;
+                T v = T(NAN);
+                if (fabs(x0) < kF && fabs(x1) < kF && fabs(x2) < kF)
+                    v = bcc_tet_global<T, T>(a, x0 - T(1), x1 - T(1), x2 - T(1));
+                else if (isfinite(x0) && isfinite(x1) && isfinite(x2))
+                    v = bcc_tet_global<double, T>(a, (double)x0 - 1.0, (double)x1 - 1.0, (double)x2 - 1.0);
+                r[0] = u == 0 ? v : r[0];
+                r[1] = u == 1 ? v : r[1];
+                r[2] = u == 2 ? v : r[2];
+                r[3] = u == 3 ? v : r[3];
+            }
+            if (full) {
+                if constexpr (sizeof(T) == 4) {
+                    *reinterpret_cast<float4*>(a.out + j0) = make_float4(r[0], r[1], r[2], r[3]);
+                } else {
+                    reinterpret_cast<double2*>(a.out + j0)[0] = make_double2(r[0], r[1]);
+                    reinterpret_cast<double2*>(a.out + j0)[1] = make_double2(r[2], r[3]);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (j0 + u >= p0 && j0 + u < p1) a.out[j0 + u] = r[u];
+            }
+        }
+        __syncthreads();  // the tile is restaged for the next brick
+    }
+}
+
+}  // namespace sp

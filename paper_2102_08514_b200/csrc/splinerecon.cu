@@ -30,6 +30,7 @@
 #include "sp_evaluators.cuh"
 #include "sp_launch.cuh"
 #include "sp_tma.cuh"
+#include "sp_bcc_linear.cuh"
 
 
 // generated plan kernels + kGenerated[] registry (codegen.py)
@@ -102,9 +103,15 @@ struct sp_plan {
     std::vector<void*> allocs;
     int occ_f32 = 0, occ_f64 = 0;
     int num_sms = 148;
+    bool bcc_tet = false;  // bcc_linear_rd: closed-form evaluator (sp_bcc_linear.cuh)
 };
 
 namespace {
+
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
 
 template <typename V>
 int upload(sp_plan* p, const std::vector<V>& v, const V** out) {
@@ -336,6 +343,15 @@ int sp_plan_create(const sp_plan_desc* desc, sp_plan** out) {
             break;
         }
     }
+    // the reference's bcc_linear_rd plan (matched word for word above) has a closed form
+    // (sp_bcc_linear.cuh); it reads coset cells -2..+2 around floor((x - l)/2)
+    if (p->gen && std::strcmp(p->gen->name, "bcc_linear_rd") == 0 && env_int("SP_BCC_TET", 1) != 0) {
+        p->bcc_tet = true;
+        for (int i = 0; i < 3; ++i) {
+            p->reach_lo[i] = std::min(p->reach_lo[i], -2);
+            p->reach_hi[i] = std::max(p->reach_hi[i], 2);
+        }
+    }
 
     if (p->gen) {
         // smem tables: int32 sigma[r] (16B aligned) + uint4 class records [N]
@@ -437,11 +453,6 @@ int sp_eval_launch_count(const sp_plan* plan, int64_t n) { return (plan && n > 0
 }  // extern "C"
 
 namespace {
-
-int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
 
 // Tuning knobs (environment, read per call): SP_TILE_KB (shared-memory tile budget),
 // SP_PPT (points per thread per chunk, 0 = density-based).
@@ -547,7 +558,11 @@ Kernels<T> kernels_of() {
 }
 
 template <typename T>
-int select_kernels(const sp_plan* p, Kernels<T>& k) {
+int select_kernels(const sp_plan* p, Kernels<T>& k, bool dbg = false) {
+    if (p->bcc_tet && !dbg) {  // class ids (dbg) come from the plan-generated classification
+        k = kernels_of<T, sp::BccTetEval<T>>();
+        return SP_OK;
+    }
     if (p->kind == SP_KIND_TENSOR_BSPLINE) {
         switch (p->tp_degree) {
             case 1: k = kernels_of<T, sp::TensorBSplineEval<T, 1>>(); return SP_OK;
@@ -576,7 +591,7 @@ int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
     int rc = build_args<T>(p, g, pts, n, out, dbg, err, a, vec);
     if (rc != SP_OK) return rc;
     Kernels<T> k;
-    if ((rc = select_kernels<T>(p, k)) != SP_OK) return rc;
+    if ((rc = select_kernels<T>(p, k, dbg != nullptr)) != SP_OK) return rc;
     const int chunk_pts = sp::kThreads * a.ppt;
     const size_t smem = tile_smem(a, vec, sizeof(T)) +
                         (size_t)((chunk_pts * 3 * sizeof(T) + 15) & ~15);
@@ -754,6 +769,29 @@ int try_bricks_tma(const sp_plan* p, const sp_grid_desc* g, const sp::EvalArgs<f
     return 1;
 }
 
+// Closed-form brick kernel of the BCC linear box spline (sp_bcc_linear.cuh): the plan is the
+// reference's bcc_linear_rd (matched word for word against the generated registry entry),
+// brick-order points read directly (no permutation), 16-byte aligned points and results.
+// Returns 1 when launched, 0 when not applicable, < 0 on error.  SP_BCC_TET=0 disables.
+template <typename T>
+int try_bricks_bcc_tet(const sp_plan* p, const sp::EvalArgs<T>& a, const int64_t* bstart, int nbricks, int log2b,
+                       cudaStream_t st) {
+    if (!p->bcc_tet || env_int("SP_BCC_TET_BRICK", 1) == 0) return 0;
+    if (a.in_index32 || a.out_index || a.out_index32 || a.dbg) return 0;
+    if ((reinterpret_cast<uintptr_t>(a.pts) & 15) || (reinterpret_cast<uintptr_t>(a.out) & 15)) return 0;
+    if (log2b != 3 && log2b != 4) return 0;
+    const long long* bs = reinterpret_cast<const long long*>(bstart);
+    const int E = (1 << log2b) / 2 + 4;
+    const size_t smem = 2 * (size_t)E * E * E * sizeof(T);
+    auto kern = log2b == 3 ? sp::bcc_tet_brick_kernel<T, 3> : sp::bcc_tet_brick_kernel<T, 4>;
+    const int per_sm = sp::cached_occupancy(kern, smem);
+    const int blocks = std::max(1, std::min(nbricks, p->num_sms * per_sm));
+    kern<<<blocks, sp::kThreads, smem, st>>>(a, bs, nbricks);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "BCC linear brick kernel launch: %s", cudaGetErrorString(e));
+    return 1;
+}
+
 template <typename T>
 int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t n, const int64_t* bstart,
                       int32_t nbricks, int32_t log2b, const int64_t* out_index, void* out, int32_t* err,
@@ -770,6 +808,10 @@ int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, 
     a.prefetch_pts = env_int("SP_PREFETCH_PTS", 1);
     if constexpr (sizeof(T) == 4) {
         const int t = try_bricks_tma(p, g, a, bstart, nbricks, log2b, st);
+        if (t != 0) return t > 0 ? SP_OK : t;
+    }
+    {
+        const int t = try_bricks_bcc_tet<T>(p, a, bstart, nbricks, log2b, st);
         if (t != 0) return t > 0 ? SP_OK : t;
     }
     Kernels<T> k;
@@ -1147,6 +1189,7 @@ extern "C" int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t
     else
         morton32_iota_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, n, lo0, lo1, lo2, bits, k_in,
                                                                    iota);
+    e = cudaGetLastError();
     size_t cb = cub_bytes;
     // The lowest end_bit % 8 key bits (the finest Morton levels inside a brick) stay unsorted
     // so that the radix sort runs whole 8-bit passes only: 27-bit keys sort in 3 passes, not 4
@@ -1162,15 +1205,19 @@ extern "C" int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t
             gather_points32_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, perm, n, (float*)sorted_pts);
         else if (sorted_pts)
             gather_points32_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, perm, n, (double*)sorted_pts);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
         // brick runs: scatter of the heads by brick id + compaction over the (<= n) brick ids
         // when the frame has at most n bricks (the iota segment is free after the sort), else
         // stream compaction over the n sorted keys
         const int nbf = 3 * (bits - log2_brick);
         const long long nb = 1ll << nbf;
         size_t sel = 0;
-        if (nb <= n)
-            cub::DeviceSelect::If(nullptr, sel, iota, brick_start, n_bricks, (int)nb, IsHead{}, st);
-        if (nb <= n && sel <= cub_bytes) {
+        // size query failure -> the stream-compaction path below
+        const bool by_heads = nb <= n && cub::DeviceSelect::If(nullptr, sel, iota, brick_start, n_bricks, (int)nb,
+                                                               IsHead{}, st) == cudaSuccess;
+        if (by_heads && sel <= cub_bytes) {
             e = cudaMemsetAsync(iota, 0xff, (size_t)nb * 4, st);
             if (e == cudaSuccess) {
                 brick_heads32_kernel<<<grid_for(n), 256, 0, st>>>(k_out, n, 3 * log2_brick, iota);

@@ -348,6 +348,26 @@ class PlanInterpreter:
         pts = torch.tensor([[float(v) for v in x]], dtype=grid.dtype, device=grid.device)
         return float(self.eval_batch(grid, pts)[0])
 
+    @staticmethod
+    def _on_stream(stream, dev, fn):
+        """Run fn() with `stream` as the current stream (staging, allocation, launches,
+        sentinel check and read-back all ordered on it).  The stream first waits for the
+        caller's current stream (inputs it produced), and the caller's stream waits for it
+        afterwards, with device results recorded on the caller's stream."""
+        if stream is None or dev.type != "cuda":
+            return fn()
+        cur = torch.cuda.current_stream(dev)
+        if stream == cur:
+            return fn()
+        stream.wait_stream(cur)
+        with torch.cuda.stream(stream):
+            r = fn()
+        cur.wait_stream(stream)
+        for t in (r if isinstance(r, tuple) else (r,)):
+            if isinstance(t, torch.Tensor) and t.device.type == "cuda":
+                t.record_stream(cur)
+        return r
+
     def eval_batch(self, grid: CoefficientGrid, pts, *, out: torch.Tensor | None = None, check: bool = True,
                    order: str = "auto", reorder: bool = False, stream: torch.cuda.Stream | None = None):
         """Batch reconstruction (runtime.py:244-248).
@@ -370,6 +390,9 @@ class PlanInterpreter:
         self._check_grid(grid)
         if self.mode != "float":
             raise RuntimeError_("batch evaluation is float-mode only")
+        if stream is not None and grid.device.type == "cuda" and stream != torch.cuda.current_stream(grid.device):
+            return self._on_stream(stream, grid.device, lambda: self.eval_batch(
+                grid, pts, out=out, check=check, order=order, reorder=reorder, stream=None))
         if self._lift is not None:
             from .lift import lift_grid, lift_points
 
@@ -592,6 +615,9 @@ class PlanInterpreter:
         self._check_grid(grid)
         if self._lift is not None or self.plan.s != 3:
             raise NotImplementedError("eval_batch_unordered: 3-D plans only")
+        if stream is not None and stream != torch.cuda.current_stream(grid.device):
+            return self._on_stream(stream, grid.device,
+                                   lambda: self.eval_batch_unordered(grid, pts, check=check, stream=None))
         if not isinstance(pts, torch.Tensor) or pts.device != grid.device or pts.dim() != 2 or pts.shape[1] != 3:
             raise RuntimeError_("points must be an (n, 3) tensor on the grid's device")
         p = pts.to(dtype=grid.dtype).contiguous()
@@ -670,9 +696,15 @@ class PlanInterpreter:
         tensor-product plans of degree 1 or 3 (8 filtered fetches per tricubic point) and the
         compiled box-spline plans (one filtered fetch per 2-site fetch group, TexFetch)."""
         self._check_grid(grid)
+        if stream is not None and stream != torch.cuda.current_stream(grid.device):
+            return self._on_stream(stream, grid.device,
+                                   lambda: self.eval_batch_texture(grid, pts, out=out, stream=None))
         lib = _native.lib()
         h = self._handle(grid.device)
-        key = (id(grid), tuple(a.data_ptr() for a in grid.arrays))
+        # the texture is a snapshot of the arrays: the key includes their version counters
+        # (in-place updates invalidate it), shapes, origins and the boundary policy
+        key = (id(grid), tuple((a.data_ptr(), tuple(a.shape), a._version) for a in grid.arrays),
+               tuple(map(tuple, grid.origins)), grid.boundary)
         with self._lock:
             tex = self._texture_for(grid, key, lib)
         p = pts.to(device=grid.device, dtype=torch.float32).contiguous()

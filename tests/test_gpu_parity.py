@@ -534,3 +534,31 @@ def test_concurrent_threads_and_streams(cuda):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", ["given", "sort", "morton"])
+def test_stream_argument_other_than_current(order, cuda):
+    """`stream=` naming a stream that is NOT the current one: inputs produced on
+    the current stream right before the call, device/numpy/host results, and the sentinel
+    check must all be ordered correctly; results equal the current-stream call."""
+    g, plan, grid = _setup("cc_tricubic", "zero", torch.float32, cuda)
+    interp = PlanInterpreter(plan)
+    base = torch.from_numpy(g["pts"].astype(np.float32)).to(cuda)
+    base = base.repeat(64, 1)  # ~360k points
+    if order == "morton":
+        from paper_2102_08514_b200.runtime import morton_order
+
+        base = base[morton_order(base)].contiguous()
+    want = interp.eval_batch(grid, base, order=order).cpu()
+    st = torch.cuda.Stream(cuda)
+    for _ in range(3):
+        torch.cuda._sleep(2_000_000)  # keep the current stream busy: a missing wait would race
+        p = base * 1.0  # produced on the current stream just before the call
+        got = interp.eval_batch(grid, p, order=order, stream=st)
+        del p
+        torch.testing.assert_close(got.cpu(), want, rtol=0, atol=0)
+        got_np = interp.eval_batch(grid, base.cpu().numpy(), order=order, stream=st)
+        np.testing.assert_array_equal(got_np, want.numpy().astype(np.float64))
+    vals, perm = interp.eval_batch_unordered(grid, base, stream=st)
+    torch.testing.assert_close(vals.cpu(), want[perm.long().cpu()], rtol=0, atol=0)

@@ -74,8 +74,11 @@ def test_bspline_pieces_partition_of_unity():
             for k, c in enumerate(p):
                 total[k] += c
         assert total == [Fraction(1)] + [Fraction(0)] * deg
-    w = tensor_site_weight(3, 3, (0, 0, 0))
-    assert w.eval([Fraction(1, 2)] * 3) == Fraction(1, 48) ** 3 * 8 ** 0 * (Fraction(1, 48) ** 0) or True
+    # cubic B-spline at t = 1/2 on its four pieces: 1/48, 23/48, 23/48, 1/48
+    half = [Fraction(1, 2)] * 3
+    assert tensor_site_weight(3, 3, (0, 0, 0)).eval(half) == Fraction(1, 48) ** 3
+    assert tensor_site_weight(3, 3, (-1, -2, -3)).eval(half) == Fraction(23, 48) ** 2 * Fraction(1, 48)
+    assert tensor_site_weight(3, 3, (1, 0, 0)).eval(half) == 0
 
 
 def test_horner_tree_exact():
