@@ -86,12 +86,11 @@ __device__ __forceinline__ R tet_combine(const TetSel<R>& t, R cE, R cA, R cO, R
     return acc * R(0.5);
 }
 
-// One point from the staged brick tile: both coset boxes have strides (E*E, E, 1), coset 1
-// at offset E^3; `base` = tile index of coset-0 cell (0,0,0) (may be negative).
+// One point from the staged brick tile (selection already made): both coset boxes have
+// strides (E*E, E, 1), coset 1 at offset E^3; `base` = tile index of coset-0 cell (0,0,0).
 template <int E, typename T>
-__device__ __forceinline__ T bcc_tet_tile(T y0, T y1, T y2, const T* __restrict__ tile, int base) {
+__device__ __forceinline__ T bcc_tet_tile(const TetSel<T>& t, const T* __restrict__ tile, int base) {
     constexpr int S0 = E * E, S1 = E, ODD = E * E * E;
-    const TetSel<T> t = tet_select<T>(y0, y1, y2);
     const int ss0 = t.n0 ? -S0 : S0, ss1 = t.n1 ? -S1 : S1, ss2 = t.n2 ? -1 : 1;
     const int sa = t.c01 ? (t.c02 ? ss0 : ss2) : (t.c12 ? ss1 : ss2);
     const int sb = t.c01 ? (t.c12 ? ss2 : ss1) : (t.c02 ? ss2 : ss0);
@@ -99,6 +98,39 @@ __device__ __forceinline__ T bcc_tet_tile(T y0, T y1, T y2, const T* __restrict_
     const int iO = iE + ODD - ((t.n0 ? S0 : 0) + (t.n1 ? S1 : 0) + (t.n2 ? 1 : 0));
     SP_CHECK(iE >= 0 && iE + sa >= 0 && iE + sa < ODD && iO < 2 * ODD && iO - sb >= ODD && iO - sb < 2 * ODD);
     return tet_combine<T>(t, tile[iE], tile[iE + sa], tile[iO], tile[iO - sb]);
+}
+
+// Stage an E^3 box of one coset (coset-cell origin z0b.. as array indices) with the policy
+// resolved per element; E is a compile-time constant (divisions fold to multiply-shifts).
+template <int POLICY, int E, typename T>
+__device__ __forceinline__ void stage_cube(T* dst, const T* __restrict__ base, int z0b, int z1b, int z2b, int g0,
+                                           int g1, int g2, int tid) {
+    constexpr int VOL = E * E * E;
+#pragma unroll 2
+    for (int e = tid; e < VOL; e += kThreads) {
+        const int i0 = e / (E * E);
+        const int r = e - i0 * (E * E);
+        const int i1 = r / E;
+        const int i2 = r - i1 * E;
+        int z0 = z0b + i0, z1 = z1b + i1, z2 = z2b + i2;
+        int bytes = (int)sizeof(T);
+        const bool in = (unsigned)z0 < (unsigned)g0 && (unsigned)z1 < (unsigned)g1 && (unsigned)z2 < (unsigned)g2;
+        if (POLICY == SP_ZERO) {
+            bytes = in ? bytes : 0;
+            z0 = in ? z0 : 0;
+            z1 = in ? z1 : 0;
+            z2 = in ? z2 : 0;
+        } else if (POLICY == SP_CLAMP) {
+            z0 = min(max(z0, 0), g0 - 1);
+            z1 = min(max(z1, 0), g1 - 1);
+            z2 = min(max(z2, 0), g2 - 1);
+        } else if (!in) {
+            z0 = mirror_index(z0, g0);
+            z1 = mirror_index(z1, g1);
+            z2 = mirror_index(z2, g2);
+        }
+        cp_async_elem<sizeof(T)>(dst + e, base + ((long long)z0 * g1 + z1) * (long long)g2 + z2, bytes);
+    }
 }
 
 // Any point through two coset fetchers (TileFetch / GlobalFetch, bound per coset by `bindk`).
@@ -158,96 +190,123 @@ struct BccTetEval {
     }
 };
 
-// One CTA per brick (grid-strided).  Box per coset: coset cells [c/2 - 3, c/2 + B/2] per axis
-// (E = B/2 + 4; covers every cell the formula can address for points of the brick, including
-// zero-weight ones at ties), same shape for both cosets, staged with the grid's boundary
-// policy (stage_box).  Points: quads of 4 consecutive brick-order points per thread.
-template <typename T, int L2B>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 2)
+// Persistent CTAs over bricks (grid-strided).  Box per coset: coset cells [c/2 - 3, c/2 + B/2]
+// per axis (E = B/2 + 4: every cell the formula can address for points of the brick, including
+// zero-weight ones at ties), same shape for both cosets, staged with the grid's boundary policy.
+// Staging is double-buffered: the next brick's boxes are in flight (cp.async group) while the
+// current brick is evaluated.  Points: quads of 4 consecutive brick-order points per thread
+// (3 x 16-byte loads, the next quad's loads issued before the current quad is evaluated).
+template <typename T, int L2B, bool PF = true, int MINB = (sizeof(T) == 4 ? 3 : 2), bool DB = true>
+__global__ void __launch_bounds__(kThreads, MINB)
     bcc_tet_brick_kernel(const EvalArgs<T> a, const long long* __restrict__ brick_start, int nbricks) {
     constexpr int B = 1 << L2B;
     constexpr int E = B / 2 + 4;
     constexpr int VOL = E * E * E;
+    constexpr T kF = BccTetTraits<T>::kFast;
     extern __shared__ __align__(16) unsigned char smem[];
-    T* tile = reinterpret_cast<T*>(smem);
-    __shared__ int corner[3];
+    T* const tiles = reinterpret_cast<T*>(smem);  // [2][2 * VOL]
     const int tid = threadIdx.x;
     if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);
-    unsigned m2, s2, m1, s1;
-    fastdiv_magic((unsigned)E, m2, s2);
-    m1 = m2;
-    s1 = s2;
-    for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
-        const long long p0 = brick_start[b], p1 = brick_start[b + 1];
-        if (tid == 0) {
-            const T* x = a.pts + 3 * p0;
+
+    auto corner_of = [&](int b, int c[3]) {  // uniform loads (broadcast)
+        const T* x = a.pts + 3 * brick_start[b];
 #pragma unroll
-            for (int i = 0; i < 3; ++i) corner[i] = (clamp_cell(x[i]) >> L2B) << L2B;
-        }
-        __syncthreads();
-        const int c0 = corner[0], c1 = corner[1], c2 = corner[2];
-        // stage both coset boxes (policy resolved here)
+        for (int i = 0; i < 3; ++i) c[i] = (clamp_cell(x[i]) >> L2B) << L2B;
+    };
+    auto stage = [&](int b, T* tile) {
+        int c[3];
+        corner_of(b, c);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const int z0b = (c0 >> 1) - 3 - a.grid.org[k][0];
-            const int z1b = (c1 >> 1) - 3 - a.grid.org[k][1];
-            const int z2b = (c2 >> 1) - 3 - a.grid.org[k][2];
+            const int z0b = (c[0] >> 1) - 3 - a.grid.org[k][0];
+            const int z1b = (c[1] >> 1) - 3 - a.grid.org[k][1];
+            const int z2b = (c[2] >> 1) - 3 - a.grid.org[k][2];
             const int g0 = a.grid.ext[k][0], g1 = a.grid.ext[k][1], g2 = a.grid.ext[k][2];
             if (a.grid.boundary == SP_ZERO)
-                stage_box<SP_ZERO>(tile + k * VOL, a.grid.data[k], VOL, E, E, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+                stage_cube<SP_ZERO, E>(tile + k * VOL, a.grid.data[k], z0b, z1b, z2b, g0, g1, g2, tid);
             else if (a.grid.boundary == SP_CLAMP)
-                stage_box<SP_CLAMP>(tile + k * VOL, a.grid.data[k], VOL, E, E, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+                stage_cube<SP_CLAMP, E>(tile + k * VOL, a.grid.data[k], z0b, z1b, z2b, g0, g1, g2, tid);
             else
-                stage_box<SP_MIRROR>(tile + k * VOL, a.grid.data[k], VOL, E, E, m2, s2, m1, s1, z0b, z1b, z2b, g0, g1, g2, tid);
+                stage_cube<SP_MIRROR, E>(tile + k * VOL, a.grid.data[k], z0b, z1b, z2b, g0, g1, g2, tid);
         }
-        cp_async_wait_all();
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto load_quad = [&](long long j0, T xs[12]) {
+        if (j0 + 4 <= a.n) {
+            if constexpr (sizeof(T) == 4) {
+                const float4* src = reinterpret_cast<const float4*>(a.pts + 3 * j0);
+#pragma unroll
+                for (int v = 0; v < 3; ++v) {
+                    const float4 t = __ldg(src + v);
+                    xs[4 * v] = t.x;
+                    xs[4 * v + 1] = t.y;
+                    xs[4 * v + 2] = t.z;
+                    xs[4 * v + 3] = t.w;
+                }
+            } else {
+                const double2* src = reinterpret_cast<const double2*>(a.pts + 3 * j0);
+#pragma unroll
+                for (int v = 0; v < 6; ++v) {
+                    const double2 t = __ldg(src + v);
+                    xs[2 * v] = t.x;
+                    xs[2 * v + 1] = t.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 12; ++e) xs[e] = j0 + e / 3 < a.n ? __ldg(a.pts + 3 * j0 + e) : T(0);
+        }
+    };
+
+    if (DB && (int)blockIdx.x < nbricks) stage(blockIdx.x, tiles);
+    int it = 0;
+    for (int b = blockIdx.x; b < nbricks; b += gridDim.x, ++it) {
+        T* tile = tiles + (DB ? (it & 1) * 2 * VOL : 0);
+        const int nb = b + gridDim.x;
+        if (!DB) {
+            stage(b, tile);
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        } else if (nb < nbricks) {
+            stage(nb, tiles + ((it + 1) & 1) * 2 * VOL);  // overlaps this brick's evaluation
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
         __syncthreads();
+        int c[3];
+        corner_of(b, c);
+        const long long p0 = brick_start[b], p1 = brick_start[b + 1];
         // tile index of coset-0 cell (0,0,0); cell e lies in the box iff e - (c/2 - 1) in [0, B/2]
-        const int lo0 = (c0 >> 1) - 3, lo1 = (c1 >> 1) - 3, lo2 = (c2 >> 1) - 3;
+        const int lo0 = (c[0] >> 1) - 3, lo1 = (c[1] >> 1) - 3, lo2 = (c[2] >> 1) - 3;
         const int base = -(lo0 * E * E + lo1 * E + lo2);
+        const int r0lo = (c[0] >> 1) - 1, r1lo = (c[1] >> 1) - 1, r2lo = (c[2] >> 1) - 1;
         const long long q0 = p0 >> 2, q1 = (p1 + 3) >> 2;
+        T xn[12];
+        if (PF && q0 + tid < q1) load_quad((q0 + tid) << 2, xn);
+#pragma unroll 1
         for (long long q = q0 + tid; q < q1; q += kThreads) {
             const long long j0 = q << 2;
             T xs[12];
-            const bool full = j0 >= p0 && j0 + 4 <= p1;
-            if (j0 + 4 <= a.n) {
-                if constexpr (sizeof(T) == 4) {
-                    const float4* src = reinterpret_cast<const float4*>(a.pts + 3 * j0);
+            if constexpr (PF) {
 #pragma unroll
-                    for (int v = 0; v < 3; ++v) {
-                        const float4 t = __ldg(src + v);
-                        xs[4 * v] = t.x;
-                        xs[4 * v + 1] = t.y;
-                        xs[4 * v + 2] = t.z;
-                        xs[4 * v + 3] = t.w;
-                    }
-                } else {
-                    const double2* src = reinterpret_cast<const double2*>(a.pts + 3 * j0);
-#pragma unroll
-                    for (int v = 0; v < 6; ++v) {
-                        const double2 t = __ldg(src + v);
-                        xs[2 * v] = t.x;
-                        xs[2 * v + 1] = t.y;
-                    }
-                }
+                for (int e = 0; e < 12; ++e) xs[e] = xn[e];
+                if (q + kThreads < q1) load_quad((q + kThreads) << 2, xn);
             } else {
-#pragma unroll
-                for (int e = 0; e < 12; ++e) xs[e] = j0 + e / 3 < a.n ? __ldg(a.pts + 3 * j0 + e) : T(0);
+                load_quad(j0, xs);
             }
             T r[4];
             unsigned slow = 0u;  // points for the global path (outside the brick, far or non-finite)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const T x0 = xs[3 * u], x1 = xs[3 * u + 1], x2 = xs[3 * u + 2];
-                constexpr T kF = BccTetTraits<T>::kFast;
-                const T y0 = x0 - T(1), y1 = x1 - T(1), y2 = x2 - T(1);
-                // coset-0 cell of the nearest even site must lie in [c/2-1, c/2+B/2-1]
-                const int r0 = (int)rint(y0 * T(0.5)) - ((c0 >> 1) - 1);
-                const int r1 = (int)rint(y1 * T(0.5)) - ((c1 >> 1) - 1);
-                const int r2 = (int)rint(y2 * T(0.5)) - ((c2 >> 1) - 1);
+                const TetSel<T> t = tet_select<T>(x0 - T(1), x1 - T(1), x2 - T(1));
+                // the nearest even site's coset-0 cell must lie in [c/2-1, c/2+B/2-1]
                 const bool fast = fabs(x0) < kF && fabs(x1) < kF && fabs(x2) < kF &&  // false for NaN
-                                  max(max((unsigned)r0, (unsigned)r1), (unsigned)r2) <= (unsigned)(B / 2);
-                r[u] = fast ? bcc_tet_tile<E, T>(y0, y1, y2, tile, base) : T(0);
+                                  max(max((unsigned)(t.e0 - r0lo), (unsigned)(t.e1 - r1lo)), (unsigned)(t.e2 - r2lo)) <=
+                                      (unsigned)(B / 2);
+                T v = T(0);
+                if (fast) v = bcc_tet_tile<E, T>(t, tile, base);
+                r[u] = v;
                 slow |= fast ? 0u : (1u << u);
             }
 #pragma unroll 1
@@ -256,7 +315,6 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 2)
                 slow &= slow - 1;
                 auto pick = [&](int o) { return u == 0 ? xs[o] : u == 1 ? xs[3 + o] : u == 2 ? xs[6 + o] : xs[9 + o]; };
                 const T x0 = pick(0), x1 = pick(1), x2 = pick(2);
-                constexpr T kF = BccTetTraits<T>::kFast;
                 T v = T(NAN);
                 if (fabs(x0) < kF && fabs(x1) < kF && fabs(x2) < kF)
                     v = bcc_tet_global<T, T>(a, x0 - T(1), x1 - T(1), x2 - T(1));
@@ -267,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 2)
                 r[2] = u == 2 ? v : r[2];
                 r[3] = u == 3 ? v : r[3];
             }
-            if (full) {
+            if (j0 >= p0 && j0 + 4 <= p1) {
                 if constexpr (sizeof(T) == 4) {
                     *reinterpret_cast<float4*>(a.out + j0) = make_float4(r[0], r[1], r[2], r[3]);
                 } else {
@@ -280,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 2)
                     if (j0 + u >= p0 && j0 + u < p1) a.out[j0 + u] = r[u];
             }
         }
-        __syncthreads();  // the tile is restaged for the next brick
+        __syncthreads();  // this buffer is restaged two bricks later
     }
 }
 

@@ -518,7 +518,9 @@ int build_args(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
         a.tile_cap = tile_bytes() / (int)(sizeof(T) * (1 + (pad ? vec * 3 / 2 : vec)));
         a.vec_cap = pad ? a.tile_cap * 3 / 2 : a.tile_cap;
     } else {
-        a.tile_cap = tile_bytes() / (int)sizeof(T);
+        // the closed-form BCC linear plan uses 32^3 fp32 bricks (brick_log2_typed): 80 KB tile
+        // for the generic drivers (protocol B) so that those bricks still stage
+        a.tile_cap = (p->bcc_tet ? std::max(tile_bytes(), 80 * 1024) : tile_bytes()) / (int)sizeof(T);
         a.vec_cap = 0;
     }
     a.stats = g_stats;
@@ -607,6 +609,9 @@ int eval_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
 // the tile; -1 when even 4^3 bricks do not fit.
 template <typename T>
 int brick_log2_typed(const sp_plan* p) {
+    // closed-form BCC linear kernel (sp_bcc_linear.cuh): 32^3 bricks for fp32 (64 KB tile,
+    // barriers and staging amortised over ~8x more points than 16^3); SP_BCC_TET_L2B overrides
+    if (p->bcc_tet && env_int("SP_BCC_TET_BRICK", 1) != 0) return env_int("SP_BCC_TET_L2B", sizeof(T) == 4 ? 5 : 4);
     const int vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
     const long long cap = tile_bytes() / (long long)(sizeof(T) * (1 + vec * 3 / 2));
     bool shifted = false;
@@ -779,11 +784,18 @@ int try_bricks_bcc_tet(const sp_plan* p, const sp::EvalArgs<T>& a, const int64_t
     if (!p->bcc_tet || env_int("SP_BCC_TET_BRICK", 1) == 0) return 0;
     if (a.in_index32 || a.out_index || a.out_index32 || a.dbg) return 0;
     if ((reinterpret_cast<uintptr_t>(a.pts) & 15) || (reinterpret_cast<uintptr_t>(a.out) & 15)) return 0;
-    if (log2b != 3 && log2b != 4) return 0;
+    if (log2b < 3 || log2b > 5 || (log2b == 5 && sizeof(T) != 4)) return 0;
     const long long* bs = reinterpret_cast<const long long*>(bstart);
     const int E = (1 << log2b) / 2 + 4;
-    const size_t smem = 2 * (size_t)E * E * E * sizeof(T);
-    auto kern = log2b == 3 ? sp::bcc_tet_brick_kernel<T, 3> : sp::bcc_tet_brick_kernel<T, 4>;
+    // SP_BCC_TET_VARIANT (tuning, 16^3 bricks): 0 = prefetch, 3 CTAs/SM; 1 = no prefetch, 4 CTAs/SM
+    static const int variant = env_int("SP_BCC_TET_VARIANT", 0);
+    // 32^3 bricks (fp32 default, sp_brick_log2): single-buffered 64 KB tile, 3 CTAs/SM
+    const bool db = log2b != 5;
+    const size_t smem = (db ? 4 : 2) * (size_t)E * E * E * sizeof(T);  // two cosets (x2 double-buffered)
+    auto kern = log2b == 3   ? sp::bcc_tet_brick_kernel<T, 3>
+                : log2b == 5 ? sp::bcc_tet_brick_kernel<T, 5, false, 3, false>
+                : variant == 1 ? sp::bcc_tet_brick_kernel<T, 4, false, sizeof(T) == 4 ? 4 : 2>
+                               : sp::bcc_tet_brick_kernel<T, 4>;
     const int per_sm = sp::cached_occupancy(kern, smem);
     const int blocks = std::max(1, std::min(nbricks, p->num_sms * per_sm));
     kern<<<blocks, sp::kThreads, smem, st>>>(a, bs, nbricks);
