@@ -96,8 +96,11 @@ __device__ __forceinline__ T bcc_tet_tile(const TetSel<T>& t, const T* __restric
     const int sb = t.c01 ? (t.c12 ? ss2 : ss1) : (t.c02 ? ss2 : ss0);
     const int iE = base + t.e0 * S0 + t.e1 * S1 + t.e2;
     const int iO = iE + ODD - ((t.n0 ? S0 : 0) + (t.n1 ? S1 : 0) + (t.n2 ? 1 : 0));
-    SP_CHECK(iE >= 0 && iE + sa >= 0 && iE + sa < ODD && iO < 2 * ODD && iO - sb >= ODD && iO - sb < 2 * ODD);
-    return tet_combine<T>(t, tile[iE], tile[iE + sa], tile[iO], tile[iO - sb]);
+    // E + s - 2 s_b e_b leaves the spline's support only when its weight w_m - w_b is 0
+    // (all |d_i| = 1): read E + s instead (tet_guard_b), so the box is exactly the support
+    const int iB = t.wm > t.wb ? iO - sb : iO;
+    SP_CHECK(iE >= 0 && iE + sa >= 0 && iE + sa < ODD && iO < 2 * ODD && iB >= ODD && iB < 2 * ODD);
+    return tet_combine<T>(t, tile[iE], tile[iE + sa], tile[iO], tile[iB]);
 }
 
 // Stage an E^3 box of one coset (coset-cell origin z0b.. as array indices) with the policy
@@ -146,7 +149,8 @@ __device__ __forceinline__ R bcc_tet_fetch(R y0, R y1, R y2, F& f, Bind bindk) {
     const int o[3] = {t.e0 - (int)t.n0, t.e1 - (int)t.n1, t.e2 - (int)t.n2};
     bindk(f, 1, o);
     const R cO = (R)f.get(0, 0, 0);
-    const R cB = (R)f.get(ib == 0 ? -s0 : 0, ib == 1 ? -s1 : 0, ib == 2 ? -s2 : 0);
+    const bool gb = t.wm > t.wb;  // same guard as bcc_tet_tile
+    const R cB = (R)f.get(gb && ib == 0 ? -s0 : 0, gb && ib == 1 ? -s1 : 0, gb && ib == 2 ? -s2 : 0);
     return tet_combine<R>(t, cE, cA, cO, cB);
 }
 
@@ -190,21 +194,23 @@ struct BccTetEval {
     }
 };
 
-// Persistent CTAs over bricks (grid-strided).  Box per coset: coset cells [c/2 - 3, c/2 + B/2]
-// per axis (E = B/2 + 4: every cell the formula can address for points of the brick, including
-// zero-weight ones at ties), same shape for both cosets, staged with the grid's boundary policy.
-// Staging is double-buffered: the next brick's boxes are in flight (cp.async group) while the
-// current brick is evaluated.  Points: quads of 4 consecutive brick-order points per thread
-// (3 x 16-byte loads, the next quad's loads issued before the current quad is evaluated).
-template <typename T, int L2B, bool PF = true, int MINB = (sizeof(T) == 4 ? 3 : 2), bool DB = true>
+// Persistent CTAs over bricks (grid-strided).  Box per coset: coset cells [c/2 - 1, c/2 + B/2]
+// per axis (E = B/2 + 2) — exactly the spline's support for unit cells [c, c+B) (with the
+// zero-weight guard of bcc_tet_tile) — same shape for both cosets, staged with the grid's
+// boundary policy; optionally double-buffered (the next brick's boxes in flight while the
+// current one is evaluated).  Points: quads of 4 consecutive brick-order points per thread
+// (3 x 16-byte loads; PF: the next quad's loads issued before the current one is evaluated).
+// A point takes the tile path iff c <= x < c + B on every axis (false for NaN) and the brick
+// lies inside the fast domain (|x| < kFast); others take the global path.
+template <typename T, int L2B, bool PF = true, int MINB = (sizeof(T) == 4 ? 3 : 2), bool DB = false>
 __global__ void __launch_bounds__(kThreads, MINB)
     bcc_tet_brick_kernel(const EvalArgs<T> a, const long long* __restrict__ brick_start, int nbricks) {
     constexpr int B = 1 << L2B;
-    constexpr int E = B / 2 + 4;
+    constexpr int E = B / 2 + 2;
     constexpr int VOL = E * E * E;
     constexpr T kF = BccTetTraits<T>::kFast;
     extern __shared__ __align__(16) unsigned char smem[];
-    T* const tiles = reinterpret_cast<T*>(smem);  // [2][2 * VOL]
+    T* const tiles = reinterpret_cast<T*>(smem);  // [1 or 2][2 * VOL]
     const int tid = threadIdx.x;
     if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);
 
@@ -218,9 +224,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
         corner_of(b, c);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const int z0b = (c[0] >> 1) - 3 - a.grid.org[k][0];
-            const int z1b = (c[1] >> 1) - 3 - a.grid.org[k][1];
-            const int z2b = (c[2] >> 1) - 3 - a.grid.org[k][2];
+            const int z0b = (c[0] >> 1) - 1 - a.grid.org[k][0];
+            const int z1b = (c[1] >> 1) - 1 - a.grid.org[k][1];
+            const int z2b = (c[2] >> 1) - 1 - a.grid.org[k][2];
             const int g0 = a.grid.ext[k][0], g1 = a.grid.ext[k][1], g2 = a.grid.ext[k][2];
             if (a.grid.boundary == SP_ZERO)
                 stage_cube<SP_ZERO, E>(tile + k * VOL, a.grid.data[k], z0b, z1b, z2b, g0, g1, g2, tid);
@@ -276,10 +282,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
         int c[3];
         corner_of(b, c);
         const long long p0 = brick_start[b], p1 = brick_start[b + 1];
-        // tile index of coset-0 cell (0,0,0); cell e lies in the box iff e - (c/2 - 1) in [0, B/2]
-        const int lo0 = (c[0] >> 1) - 3, lo1 = (c[1] >> 1) - 3, lo2 = (c[2] >> 1) - 3;
+        // tile index of coset-0 cell (0,0,0)
+        const int lo0 = (c[0] >> 1) - 1, lo1 = (c[1] >> 1) - 1, lo2 = (c[2] >> 1) - 1;
         const int base = -(lo0 * E * E + lo1 * E + lo2);
-        const int r0lo = (c[0] >> 1) - 1, r1lo = (c[1] >> 1) - 1, r2lo = (c[2] >> 1) - 1;
+        // tile path: c <= x < c + B per axis, brick inside the fast domain
+        const bool dom = (T)c[0] > -kF && (T)c[1] > -kF && (T)c[2] > -kF && (T)(c[0] + B) < kF &&
+                         (T)(c[1] + B) < kF && (T)(c[2] + B) < kF;
+        const T blo0 = dom ? (T)c[0] : kF, blo1 = (T)c[1], blo2 = (T)c[2];  // dom false: no point passes
+        const T bhi0 = (T)(c[0] + B), bhi1 = (T)(c[1] + B), bhi2 = (T)(c[2] + B);
         const long long q0 = p0 >> 2, q1 = (p1 + 3) >> 2;
         T xn[12];
         if (PF && q0 + tid < q1) load_quad((q0 + tid) << 2, xn);
@@ -299,13 +309,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const T x0 = xs[3 * u], x1 = xs[3 * u + 1], x2 = xs[3 * u + 2];
-                const TetSel<T> t = tet_select<T>(x0 - T(1), x1 - T(1), x2 - T(1));
-                // the nearest even site's coset-0 cell must lie in [c/2-1, c/2+B/2-1]
-                const bool fast = fabs(x0) < kF && fabs(x1) < kF && fabs(x2) < kF &&  // false for NaN
-                                  max(max((unsigned)(t.e0 - r0lo), (unsigned)(t.e1 - r1lo)), (unsigned)(t.e2 - r2lo)) <=
-                                      (unsigned)(B / 2);
+                const bool fast = x0 >= blo0 && x0 < bhi0 && x1 >= blo1 && x1 < bhi1 && x2 >= blo2 && x2 < bhi2;
                 T v = T(0);
-                if (fast) v = bcc_tet_tile<E, T>(t, tile, base);
+                if (fast) v = bcc_tet_tile<E, T>(tet_select<T>(x0 - T(1), x1 - T(1), x2 - T(1)), tile, base);
                 r[u] = v;
                 slow |= fast ? 0u : (1u << u);
             }
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     if (j0 + u >= p0 && j0 + u < p1) a.out[j0 + u] = r[u];
             }
         }
-        __syncthreads();  // this buffer is restaged two bricks later
+        __syncthreads();  // the tile is restaged for the next brick
     }
 }
 

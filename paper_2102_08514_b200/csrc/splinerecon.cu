@@ -784,18 +784,19 @@ int try_bricks_bcc_tet(const sp_plan* p, const sp::EvalArgs<T>& a, const int64_t
     if (!p->bcc_tet || env_int("SP_BCC_TET_BRICK", 1) == 0) return 0;
     if (a.in_index32 || a.out_index || a.out_index32 || a.dbg) return 0;
     if ((reinterpret_cast<uintptr_t>(a.pts) & 15) || (reinterpret_cast<uintptr_t>(a.out) & 15)) return 0;
-    if (log2b < 3 || log2b > 5 || (log2b == 5 && sizeof(T) != 4)) return 0;
+    if (log2b < 3 || log2b > 5) return 0;
     const long long* bs = reinterpret_cast<const long long*>(bstart);
-    const int E = (1 << log2b) / 2 + 4;
-    // SP_BCC_TET_VARIANT (tuning, 16^3 bricks): 0 = prefetch, 3 CTAs/SM; 1 = no prefetch, 4 CTAs/SM
+    const int E = (1 << log2b) / 2 + 2;
+    // SP_BCC_TET_VARIANT (tuning): 0 = register prefetch of the next quad, single-buffered
+    // tile (default); 1 = no prefetch, 4 CTAs/SM; 2 = prefetch + double-buffered tile
     static const int variant = env_int("SP_BCC_TET_VARIANT", 0);
-    // 32^3 bricks (fp32 default, sp_brick_log2): single-buffered 64 KB tile, 3 CTAs/SM
-    const bool db = log2b != 5;
+    const bool db = variant == 2;
     const size_t smem = (db ? 4 : 2) * (size_t)E * E * E * sizeof(T);  // two cosets (x2 double-buffered)
     auto kern = log2b == 3   ? sp::bcc_tet_brick_kernel<T, 3>
-                : log2b == 5 ? sp::bcc_tet_brick_kernel<T, 5, false, 3, false>
-                : variant == 1 ? sp::bcc_tet_brick_kernel<T, 4, false, sizeof(T) == 4 ? 4 : 2>
-                               : sp::bcc_tet_brick_kernel<T, 4>;
+                : log2b == 4 ? sp::bcc_tet_brick_kernel<T, 4>
+                : variant == 1 ? sp::bcc_tet_brick_kernel<T, 5, false, sizeof(T) == 4 ? 4 : 2>
+                : variant == 2 ? sp::bcc_tet_brick_kernel<T, 5, true, sizeof(T) == 4 ? 3 : 2, true>
+                               : sp::bcc_tet_brick_kernel<T, 5>;
     const int per_sm = sp::cached_occupancy(kern, smem);
     const int blocks = std::max(1, std::min(nbricks, p->num_sms * per_sm));
     kern<<<blocks, sp::kThreads, smem, st>>>(a, bs, nbricks);
