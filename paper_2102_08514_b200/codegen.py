@@ -445,10 +445,23 @@ struct Eval {{
 """
 
 
-_WORD_CLASS = """    __device__ __forceinline__ static int word_class(unsigned word, int k) {
-        const unsigned b = (word >> (8 * k)) & 0xffu;
-        return b == 0xffu ? -1 : (int)b;
-    }
+def _word_bits(plan: EvaluationPlan) -> int:
+    """Bits per coset class in a 32-bit class word (all-ones = sigma sentinel)."""
+    if plan.M * 8 <= 32 and plan.N < 255:
+        return 8
+    if plan.M * 16 <= 32 and plan.N < 65535:
+        return 16
+    return 0
+
+
+def _word_class(plan: EvaluationPlan) -> str:
+    b = _word_bits(plan) or 8
+    m = (1 << b) - 1
+    return f"""    static constexpr int kWordBits = {b};
+    __device__ __forceinline__ static int word_class(unsigned word, int k) {{
+        const unsigned b = (word >> ({b} * k)) & {m:#x}u;
+        return b == {m:#x}u ? -1 : (int)b;
+    }}
 """
 
 
@@ -459,7 +472,7 @@ def _signature_methods(plan: EvaluationPlan) -> str:
     kernel per coset instead of every kernel that occurs among their lanes."""
     return f"""    static constexpr bool kSig = true;
     static constexpr int kSigCount = {plan.K ** plan.M};
-""" + _WORD_CLASS + """    template <class Ctx>
+""" + _word_class(plan) + """    template <class Ctx>
     __device__ __forceinline__ static unsigned classify_word(const T x[3], const Ctx& ctx) {
         const int* sigma = reinterpret_cast<const int*>(ctx.tables);
         float frac[3] = {0.f, 0.f, 0.f};
@@ -477,7 +490,7 @@ def _signature_methods(plan: EvaluationPlan) -> str:
                 frame_f64<T>(x, k, cell, xp);
                 raw = class_of<double>(xp, sigma);
             }
-            w |= (unsigned)(raw & 0xff) << (8 * k);
+            w |= ((unsigned)raw & ((1u << kWordBits) - 1u)) << (kWordBits * k);
         }
         return w;
     }
@@ -542,8 +555,8 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
             f"                case {k}: acc = kernel{k}<T>(y0, y1, y2, f); break;" for k in range(plan.K)
         )
         dispatch = f"            T acc = T(0);\n            switch (kern) {{\n{cases}\n            }}"
-    sig_ok = plan.K > 1 and plan.M <= 4 and plan.N < 255 and plan.K ** plan.M <= 1024
-    sig_methods = _signature_methods(plan) if sig_ok else "    static constexpr bool kSig = false;\n" + _WORD_CLASS
+    sig_ok = plan.K > 1 and _word_bits(plan) > 0 and plan.K ** plan.M <= 1024
+    sig_methods = _signature_methods(plan) if sig_ok else "    static constexpr bool kSig = false;\n" + _word_class(plan)
     if aff is not None:
         eval_src = _affine_eval_source(plan, aff[0], aff[1], min_blocks)
     else:
@@ -593,7 +606,7 @@ struct Eval {{
     __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
         return eval_impl<false>(x, 0u, f, ctx);
     }}
-    // classes given (8 bits per coset, 0xff = sentinel), e.g. by classify_word: no plane tests
+    // classes given (kWordBits per coset, all ones = sentinel), e.g. by classify_word: no plane tests
     template <class F, class Ctx>
     __device__ __forceinline__ static T eval_word(const T x[3], unsigned word, F& f, const Ctx& ctx) {{
         return eval_impl<true>(x, word, f, ctx);
