@@ -472,6 +472,8 @@ def _signature_methods(plan: EvaluationPlan) -> str:
     kernel per coset instead of every kernel that occurs among their lanes."""
     return f"""    static constexpr bool kSig = true;
     static constexpr int kSigCount = {plan.K ** plan.M};
+    static constexpr int kProgCount = {len(set(kernel_programs(plan)))};
+    static constexpr int kMC = kM;
 """ + _word_class(plan) + """    template <class Ctx>
     __device__ __forceinline__ static unsigned classify_word(const T x[3], const Ctx& ctx) {
         const int* sigma = reinterpret_cast<const int*>(ctx.tables);
@@ -502,6 +504,37 @@ def _signature_methods(plan: EvaluationPlan) -> str:
         return sig;
     }
 """
+
+
+def _shift_select(plan: EvaluationPlan) -> str:
+    """Body of shift_i(k, i): nested selects over the plan's coset shifts."""
+    def axis(sh):
+        return f"(i == 0 ? {int(sh[0])} : (i == 1 ? {int(sh[1])} : {int(sh[2])}))"
+    expr = axis(plan.shifts[-1])
+    for k in range(plan.M - 2, -1, -1):
+        expr = f"(k == {k} ? {axis(plan.shifts[k])} : {expr})"
+    return f"    return {expr};"
+
+
+def kernel_programs(plan: EvaluationPlan) -> list:
+    """Program id per kernel: kernels whose generated weight programs are identical share one
+    (fcc_voronoi1's kernels 0 and 1), so the coset-item driver groups them together."""
+    progs, ids = {}, []
+    for k in range(plan.K):
+        lines, _ = _kernel_function(plan, k, plan.diag[0])
+        key = "\n".join(lines).replace(f"kernel{k}(", "kernelX(")
+        ids.append(progs.setdefault(key, len(progs)))
+    return ids
+
+
+def _prog_select(plan: EvaluationPlan) -> str:
+    ids = kernel_programs(plan)
+    if ids == list(range(plan.K)):
+        return "kern"
+    expr = str(ids[-1])
+    for k in range(plan.K - 2, -1, -1):
+        expr = f"(kern == {k} ? {ids[k]} : {expr})"
+    return expr
 
 
 def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple:
@@ -611,56 +644,80 @@ struct Eval {{
     __device__ __forceinline__ static T eval_word(const T x[3], unsigned word, F& f, const Ctx& ctx) {{
         return eval_impl<true>(x, word, f, ctx);
     }}
-    template <bool kWord, class F, class Ctx>
-    __device__ __forceinline__ static T eval_impl(const T x[3], unsigned word, F& f, const Ctx& ctx) {{
+    // one coset's contribution (runtime.py:384-407 for coset k): KC >= 0 a compile-time coset
+    // (unrolled loop of eval_impl), KC < 0 a runtime one (coset-item driver; tile geometry
+    // from shared memory).  Same operations either way: identical values.
+    template <bool kWord, int KC, class F, class Ctx>
+    __device__ __forceinline__ static T eval_coset(const T x[3], bool fast, const float frac[3], unsigned word, int k,
+                                                   F& f, const Ctx& ctx) {{
         const EvalArgs<T>& a = *ctx.a;
         const int* sigma = reinterpret_cast<const int*>(ctx.tables);
         const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
+        if (KC >= 0) k = KC;
+        int cell[3];
+        T yy[3];
+        uint4 rec;
+        int raw;
+        if (fast) {{
+            float xp[3];
+            frame_fast(frac, ctx.X, k, cell, xp);
+            raw = kWord ? word_class(word, k) : class_of<float>(xp, sigma);
+            y_of<float, T>(xp, raw, cls_tab, ctx.err, yy, rec);
+        }} else {{
+            double xp[3];
+            frame_f64<T>(x, k, cell, xp);
+            raw = kWord ? word_class(word, k) : class_of<double>(xp, sigma);
+            y_of<double, T>(xp, raw, cls_tab, ctx.err, yy, rec);
+        }}
+        write_dbg(a.dbg, ctx.index, kM, k, raw, cell);  // raw class: -1 for the sentinel
+        const int c = max(raw, 0);
+        const int kern = (int)(rec.x & 15u);
+        (void)kern;
+        const T y0 = yy[0], y1 = yy[1], y2 = yy[2];
+        if constexpr (F::kIsTile) {{
+            const int4 tr = ctx.trec[k * kN + c];
+            if (KC >= 0)
+                f.a0 = ctx.cbase[KC < 0 ? 0 : KC] + cell[0] * ctx.st0[KC < 0 ? 0 : KC] +
+                       cell[1] * ctx.st1[KC < 0 ? 0 : KC] + cell[2] + tr.w;
+            else
+                f.a0 = ctx.geom->cbase[k] + cell[0] * ctx.geom->st0[k] + cell[1] * ctx.geom->st1[k] + cell[2] + tr.w;
+            f.c0 = tr.x;
+            f.c1 = tr.y;
+            f.c2 = tr.z;
+        }} else {{
+            int rho[3], tau[3], base[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {{
+                rho[i] = (int)((rec.x >> (13 + 2 * i)) & 3u);
+                tau[i] = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
+                base[i] = cell[i] + (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
+            }}
+            bind(f, a, *ctx.geom, k, base, rho, tau);
+        }}
+{dispatch}
+        return acc;
+    }}
+    template <bool kWord, class F, class Ctx>
+    __device__ __forceinline__ static T eval_impl(const T x[3], unsigned word, F& f, const Ctx& ctx) {{
         float frac[3] = {{0.f, 0.f, 0.f}};
         const bool fast = fast_frame(x, frac);
         T total = T(0);
-#pragma unroll
-        for (int k = 0; k < kM; ++k) {{
-            int cell[3];
-            T yy[3];
-            uint4 rec;
-            int raw;
-            if (fast) {{
-                float xp[3];
-                frame_fast(frac, ctx.X, k, cell, xp);
-                raw = kWord ? word_class(word, k) : class_of<float>(xp, sigma);
-                y_of<float, T>(xp, raw, cls_tab, ctx.err, yy, rec);
-            }} else {{
-                double xp[3];
-                frame_f64<T>(x, k, cell, xp);
-                raw = kWord ? word_class(word, k) : class_of<double>(xp, sigma);
-                y_of<double, T>(xp, raw, cls_tab, ctx.err, yy, rec);
-            }}
-            write_dbg(a.dbg, ctx.index, kM, k, raw, cell);  // raw class: -1 for the sentinel
-            const int c = max(raw, 0);
-            const int kern = (int)(rec.x & 15u);
-            (void)kern;
-            const T y0 = yy[0], y1 = yy[1], y2 = yy[2];
-            if constexpr (F::kIsTile) {{
-                const int4 tr = ctx.trec[k * kN + c];
-                f.a0 = ctx.cbase[k] + cell[0] * ctx.st0[k] + cell[1] * ctx.st1[k] + cell[2] + tr.w;
-                f.c0 = tr.x;
-                f.c1 = tr.y;
-                f.c2 = tr.z;
-            }} else {{
-                int rho[3], tau[3], base[3];
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {{
-                    rho[i] = (int)((rec.x >> (13 + 2 * i)) & 3u);
-                    tau[i] = ((rec.x >> (19 + i)) & 1u) ? -1 : 1;
-                    base[i] = cell[i] + (int)((rec.x >> (22 + 3 * i)) & 7u) - 4;
-                }}
-                bind(f, a, *ctx.geom, k, base, rho, tau);
-            }}
-{dispatch}
-            total += acc;
-        }}
-        return total;
+        total += eval_coset<kWord, 0>(x, fast, frac, word, 0, f, ctx);
+{''.join(f"        total += eval_coset<kWord, {k}>(x, fast, frac, word, {k}, f, ctx);" + chr(10) for k in range(1, plan.M))}        return total;
+    }}
+    // coset-item driver (eval_brick_items): program id of coset k's kernel for class word
+    // `word` (identical kernel programs share an id) and the per-coset evaluation with a
+    // runtime coset index
+    __device__ __forceinline__ static int item_kernel(unsigned word, int k, const unsigned char* tables) {{
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
+        const int kern = (int)(cls_tab[max(word_class(word, k), 0)].x & 15u);
+        return {_prog_select(plan)};
+    }}
+    template <class F, class Ctx>
+    __device__ __forceinline__ static T eval_item(const T x[3], unsigned word, int k, F& f, const Ctx& ctx) {{
+        float frac[3] = {{0.f, 0.f, 0.f}};
+        const bool fast = fast_frame(x, frac);
+        return eval_coset<true, -1>(x, fast, frac, word, k, f, ctx);
     }}
 }};
 
@@ -692,6 +749,11 @@ constexpr int kN = {plan.N};
 constexpr int kDI = {d};
 constexpr int kLog2D = {d.bit_length() - 1};
 __device__ constexpr int kShiftI[kM][3] = {{{", ".join("{" + ", ".join(str(int(v)) for v in sh) + "}" for sh in plan.shifts)}}};
+// coset shift l_k[i] by selects: folds to a constant for a compile-time k (unrolled coset
+// loops) and stays in registers for a runtime k (coset-item driver)
+__device__ __forceinline__ int shift_i(int k, int i) {{
+{_shift_select(plan)}
+}}
 
 template <typename R>
 __device__ __forceinline__ int plane_code(const R xp0, const R xp1, const R xp2) {{
@@ -738,7 +800,7 @@ template <typename T>
 __device__ __forceinline__ void frame_f64(const T x[3], int k, int cell[3], double xp[3]) {{
 #pragma unroll
     for (int i = 0; i < 3; ++i) {{
-        const double xl = (double)x[i] - kShift[k][i];
+        const double xl = (double)x[i] - (double)shift_i(k, i);
         const double q = floor(xl * kInvD);  // power-of-two d: exact
         xp[i] = xl - q * kD;
         cell[i] = clamp_cell(q);
@@ -751,7 +813,7 @@ __device__ __forceinline__ void frame_f64(const T x[3], int k, int cell[3], doub
 __device__ __forceinline__ void frame_fast(const float frac[3], const int X[3], int k, int cell[3], float xp[3]) {{
 #pragma unroll
     for (int i = 0; i < 3; ++i) {{
-        const int xm = X[i] - kShiftI[k][i];
+        const int xm = X[i] - shift_i(k, i);
         cell[i] = xm >> kLog2D;
         const int p = xm & (kDI - 1);
         xp[i] = kDI == 1 ? frac[i] : (kDI == 2 ? (p ? frac[i] + 1.0f : frac[i]) : frac[i] + (float)p);
