@@ -50,6 +50,11 @@ WORKLOADS = {
     "bcc_quintic_2x203_fp32": ("bcc_quintic_rd", 405, "float32", 100_000_000),
     "fcc6_4x161_fp32": ("fcc_cubic", 321, "float32", 100_000_000),
     "zp3_cc256_fp32": ("cc_zp3", 255, "float32", 100_000_000),
+    # float64 (the reference's only precision, runtime.py:57, :248) for C3/C4
+    "bcc_linear_2x203_fp64": ("bcc_linear_rd", 405, "float64", 100_000_000),
+    "bcc_quintic_2x203_fp64": ("bcc_quintic_rd", 405, "float64", 100_000_000),
+    "fcc6_4x161_fp64": ("fcc_cubic", 321, "float64", 100_000_000),
+    "zp3_cc256_fp64": ("cc_zp3", 255, "float64", 100_000_000),
     # C5: Voronoi splines V1 at 512^3-equivalent samples (BCC 2x406^3, FCC 4x322^3), 10^9 points
     # per GPU.  PP data: tools/voronoi_pp.py (reference exact tools), plans: reference compiler.
     "c5_fcc_voronoi1_4x322_1e9_fp32": ("fcc_voronoi1", 643, "float32", 1_000_000_000),
@@ -181,8 +186,10 @@ def onchip_roofline(plan, esize, pts_per_s, sm_mhz):
         return None
     fl = codegen.weight_flops(plan)
     per_pt = plan.M * sum(fl) / len(fl)  # specialised (one kernel per coset), mean over kernels
-    peak = 148 * 128 * clk * (1.0 if esize == 4 else 1.0 / 64)
-    return {"bound": "fp32 pipe (weight programs)" if esize == 4 else "fp64 pipe", "unit": "Top/s (FMA = 1 op)",
+    # B200: 128 FP32 FMA lanes per SM per clock; FP64 at half rate (datasheet 40 vs 80 TFLOPS)
+    peak = 148 * 128 * clk * (1.0 if esize == 4 else 0.5)
+    return {"bound": "fp32 pipe (weight programs)" if esize == 4 else "fp64 pipe (half the fp32 rate)",
+            "unit": "Top/s (FMA = 1 op)",
             "flops_per_point": per_pt, "flops_per_coset_per_kernel": fl,
             "achieved": pts_per_s * per_pt / 1e12, "peak": peak / 1e12, "frac": pts_per_s * per_pt / peak}
 
@@ -355,40 +362,185 @@ def cpu_baseline(name, budget_s=15.0):
     }
 
 
+# ---------------------------------------------------------------------------------------
+# CPU arm: the REFERENCE itself (splineplan installed into baseline/_ref, PlanInterpreter.
+# eval_batch, runtime.py:244-248) on the host cores; the numpy port (oracle/) when the
+# install is absent.
+
+_REF_STATE = {}
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_available() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "splineplan"))
+
+
+def _ref_chunk(span):
+    lo, hi = span
+    st = _REF_STATE
+    return st["interp"].eval_batch(st["grid"], st["pts"][lo:hi])
+
+
+def ref_setup(name, seed=0):
+    """The reference's own grid / plan / interpreter for a workload (host, float64), the
+    same grid shape and point distribution as the GPU workload; state inherited by fork."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from splineplan.lattice import decompose_cartesian, named_lattice
+    from splineplan.plancompile import deserialize_plan
+    from splineplan.runtime import CoefficientGrid, PlanInterpreter
+
+    from paper_2102_08514_b200 import corpus
+
+    plan_name, hi, _, _ = WORKLOADS[name]
+    with open(corpus.PLAN_DIR / f"{_plan_name(plan_name)}.plan.json") as fh:
+        plan = deserialize_plan(fh.read())
+    cos = decompose_cartesian(named_lattice(plan.lattice_name))
+    grid = CoefficientGrid.zeros(cos, [0, 0, 0], [hi, hi, hi])  # runtime.py:65-78
+    rng = np.random.default_rng(2102_08514 + seed)
+    for a in grid.arrays:
+        a[...] = rng.random(a.shape, dtype=np.float32)
+    pts = (rng.random((1 << 20, 3), dtype=np.float32) * np.float32(hi + 1)).astype(np.float64)
+    interp = PlanInterpreter(plan)
+    interp._batch_tables()  # lowered tables built once, before the fork
+    _REF_STATE.clear()
+    _REF_STATE.update(interp=interp, grid=grid, pts=pts)
+
+
+REF_CHUNK = 8192
+
+
+def ref_run(n_points, pool, chunk=REF_CHUNK):
+    """Chunks of REF_CHUNK points over the pool (chunking is mandatory,
+    _poly_batch allocates n x terms x s); the calibration uses the same chunk size."""
+    spans = [(i, min(i + chunk, n_points)) for i in range(0, n_points, chunk)]
+    t0 = time.perf_counter()
+    if pool is None:
+        for sp in spans:
+            _ref_chunk(sp)
+    else:
+        pool.map(_ref_chunk, spans)
+    return time.perf_counter() - t0
+
+
+def ref_calibrated_sample(cores, target_s, pool=None):
+    """Points per sample so that one pooled sample takes ~target_s (calibrated on the pool
+    itself: memory-bound numpy scales sub-linearly with the worker count)."""
+    ref_run(256, None)  # first-touch costs
+    n0 = min(REF_CHUNK * cores, len(_REF_STATE["pts"]))
+    t = ref_run(n0, pool)
+    n = int(n0 / max(t, 1e-6) * target_s)
+    return max(256 * cores, min(n, len(_REF_STATE["pts"])))
+
+
+def cpu_baseline_reference(name, budget_s):
+    """cpu_baseline of one workload with the reference's own eval_batch (all host cores)."""
+    ref_setup(name)
+    cores = os.cpu_count() or 1
+    with mp.get_context("fork").Pool(cores) as pool:
+        n = ref_calibrated_sample(cores, budget_s, pool)
+        secs = ref_run(n, pool)
+    _REF_STATE.clear()
+    return {"value": n / secs / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{n} uniform points of {name} (same grid shape/distribution), splineplan "
+                      f"PlanInterpreter.eval_batch from baseline/_ref (runtime.py:244-248), float64, chunks of "
+                      f"8192 points over {cores} fork workers, {secs:.1f} s", "seconds": secs}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    name = HEADLINE
-    cpu_reference_setup(name)
+    name = args.workload
     cores = os.cpu_count() or 1
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        # bounded: the whole --steps K --warmup W run stays within ~ref_total_seconds
-        step_s = min(args.ref_step_seconds, args.ref_total_seconds / max(1, args.steps + args.warmup))
-        n = cpu_calibrated_sample(pool, cores, step_s)
-        for _ in range(args.warmup):
-            cpu_run(n, pool)
-        times = [cpu_run(n, pool) for _ in range(args.steps)]
+    step_s = min(args.ref_step_seconds, args.ref_total_seconds / max(1, args.steps + args.warmup))
+    port = None
+    if reference_available():
+        kind = "reference"
+        ref_setup(name)
+        with mp.get_context("fork").Pool(cores) as pool:
+            n = ref_calibrated_sample(cores, step_s, pool)
+            for _ in range(args.warmup):
+                ref_run(n, pool)
+            times = [ref_run(n, pool) for _ in range(args.steps)]
+        _REF_STATE.clear()
+        sample = (f"{n} uniform points per step, splineplan PlanInterpreter.eval_batch from baseline/_ref "
+                  f"(runtime.py:244-248, the unmodified reference), float64, chunks of 8192 points over "
+                  f"{cores} fork workers")
+        # the numpy port of the same algorithm (oracle/plan_numpy.py), for comparison
+        try:
+            port = cpu_baseline(name, min(5.0, step_s))
+        except Exception as exc:  # noqa: BLE001
+            port = {"unavailable": repr(exc)}
+    else:
+        kind = "port"
+        cpu_reference_setup(name)
+        with mp.get_context("fork").Pool(cores) as pool:
+            n = cpu_calibrated_sample(pool, cores, step_s)
+            for _ in range(args.warmup):
+                cpu_run(n, pool)
+            times = [cpu_run(n, pool) for _ in range(args.steps)]
+        sample = (f"{n} uniform points per step, numpy restatement of runtime.py:363-408 "
+                  f"(oracle/plan_numpy.py; baseline/_ref not installed), {cores} fork workers")
     secs = float(np.mean(times))
     value = n / secs / 1e9
+    plan_name, hi, _, _ = WORKLOADS[name]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": name, "points_per_step": n, "lattice": "CC3 256^3", "spline": "cc_tricubic",
-                   "boundary": "zero"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{n} uniform points per step, numpy restatement of runtime.py:363-408 "
-                                   f"(oracle/plan_numpy.py), {cores} fork workers"},
+        "config": {"workload": name, "points_per_step": n, "grid_hi": hi, "spline": plan_name, "boundary": "zero"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if port is not None:
+        line["port_baseline"] = port
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------------------------------
 # GPU arm
+
+
+def bench_c5_strong(args, device, rank, world, stream, dist, wname):
+    """C5 as north_star states it (BASELINE.json configs[4]): 10^9 points in
+    TOTAL sharded n/G over the G ranks (each rank generates its own shard, Morton-ordered as
+    protocol A), lattice replicated; per-rank evaluation time max-reduced over ranks; then, for a
+    caller who wants ONE output tensor, the all-gather of the shards over NCCL
+    (sharding.gather_results), timed separately."""
+    import torch
+
+    from paper_2102_08514_b200.sharding import gather_results, shard_range
+
+    total = WORKLOADS[wname][3]
+    a, b = shard_range(total, rank, world)
+    nloc = b - a
+    plan, grid, pts, interp = make_workload(wname, rank, device, n_override=nloc)
+    batch = interp.prepare(grid, pts, presorted=True)
+    out = torch.empty(nloc, dtype=grid.dtype, device=device)
+
+    def step():
+        interp.eval_batch(grid, batch, out=out, check=False)
+
+    step()
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 10))
+    ms = measure(step, steps, args.warmup, stream, dist)
+    gather_ms = 0.0
+    if dist is not None:
+        width = max(y - x for x, y in (shard_range(total, r, world) for r in range(world)))
+        full = torch.empty(world * width, dtype=grid.dtype, device=device)
+        gather_ms = measure(lambda: gather_results(out, total, out=full), steps, 1, stream, dist)
+        del full
+    res = {"workload": wname, "spline": WORKLOADS[wname][0], "scaling": "strong", "total_points": total,
+           "per_rank_points": nloc, "n_ranks": world, "ms_per_step": ms, "value": total / (ms * 1e-3) / 1e9,
+           "gather_ms": gather_ms, "value_with_gather": total / ((ms + gather_ms) * 1e-3) / 1e9, "unit": UNIT,
+           "gather": "all_gather_into_tensor of n*4 B over NCCL (NVLink), one output tensor on every rank"
+                     if world > 1 else "single rank: the output is already one tensor"}
+    del plan, grid, pts, interp, batch, out
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_ours(args):
@@ -460,6 +612,18 @@ def run_ours(args):
     }
     del host_pts, host_out
 
+    # ---- the public call on device tensors: eval_batch(grid, pts, order="morton") ------
+    # (Morton keys + device brick runs + the brick kernel, all inside the timed region)
+    def pub_step():
+        interp.eval_batch(grid, pts, out=out, check=False, order="morton")
+
+    pub_step()
+    torch.cuda.synchronize()
+    ms_pub = measure(pub_step, max(3, min(args.steps, 40)), args.warmup, stream, dist)
+    public_device = {"value": world * n / (ms_pub * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_pub,
+                     "path": "PlanInterpreter.eval_batch(grid, cuda points, out=..., order='morton'): "
+                             "sp_morton_keys + sp_brick_runs (count on the device) + brick kernel, no host sync"}
+
     # ---- hardware-texture-filtered variant (reported separately, with its error) ------
     texture = None
     try:
@@ -526,6 +690,7 @@ def run_ours(args):
             "kernel_ms": ms,
         },
         "e2e": e2e,
+        "public_device_morton": public_device,
         "unsorted_e2e_device": {"value": world * n / (ms_b * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms_b,
                                 "note": "protocol B: shuffled points; Morton keys + sort + brick runs + eval reading "
                                         "the points through the permutation + scatter to caller order, all "
@@ -597,8 +762,24 @@ def run_ours(args):
         line["prefilter_tma"] = bench_prefilter(args, device, rank, stream, dist, peak, hi=1023)
         line["render"] = bench_render(args, device)
 
+    # ---- C5 as north_star states it: 10^9 points in total over the G ranks ------------
+    if not args.headline_only:
+        line["c5_strong"] = [bench_c5_strong(args, device, rank, world, stream, dist, w)
+                             for w in ("c5_fcc_voronoi1_4x322_1e9_fp32", "c5_bcc_voronoi1_2x406_1e9_fp32")]
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(name, args.cpu_seconds)
+        # the reference itself (baseline/_ref) on the host cores: the headline config and,
+        # bounded, every other workload; the numpy port beside it for the headline
+        if reference_available():
+            line["cpu_baseline"] = cpu_baseline_reference(name, args.cpu_seconds)
+            line["cpu_baseline_port"] = cpu_baseline(name, min(args.cpu_seconds, 5.0))
+            for wname, w in line.get("workloads", {}).items():
+                try:
+                    w["cpu_baseline"] = cpu_baseline_reference(wname, args.cpu_seconds_per_workload)
+                except Exception as exc:  # noqa: BLE001
+                    w["cpu_baseline"] = {"unavailable": repr(exc)}
+        else:
+            line["cpu_baseline"] = cpu_baseline(name, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -620,6 +801,7 @@ def main():
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds-per-workload", type=float, default=3.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     ap.add_argument("--ref-total-seconds", type=float, default=150.0,
                     help="time budget of the whole --impl reference run (steps + warmup)")

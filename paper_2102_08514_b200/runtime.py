@@ -775,7 +775,9 @@ class PlanInterpreter:
                     raise RuntimeError_("sigma sentinel hit in batch evaluation")
                 return
         if b >= 0:
-            if sync_free:
+            # Morton-ordered input: brick runs found on the device with the count kept there
+            # (sp_brick_runs), no host round trip (prepare_points syncs for its run count)
+            if sync_free or (order == "morton" and 0 < n < (1 << 31)):
                 batch = prepare_points_async(p, b, presorted=(order == "morton"), stream=st, scratch=scratch)
             else:
                 batch = prepare_points(p, b, presorted=(order == "morton"), stream=st)

@@ -26,16 +26,24 @@ def shard_points(pts: torch.Tensor, rank: int, world: int) -> torch.Tensor:
     return pts[a:b]
 
 
-def gather_results(local: torch.Tensor, n_total: int, group=None) -> torch.Tensor:
-    """All-gather the per-rank result shards (shard_range order) into one tensor."""
+def gather_results(local: torch.Tensor, n_total: int, group=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """All-gather the per-rank result shards (shard_range order) into one tensor: one
+    all_gather_into_tensor of max-shard-width buffers (NCCL over NVLink); when every shard has
+    the same width (n_total divisible by the world size) the gathered buffer IS the result (no
+    compaction copy).  `out` (world * width elements) may be passed to reuse a buffer."""
     world = dist.get_world_size(group)
     sizes = [shard_range(n_total, r, world) for r in range(world)]
     width = max(b - a for a, b in sizes)
-    padded = torch.zeros(width, dtype=local.dtype, device=local.device)
-    padded[: local.shape[0]] = local
-    parts = [torch.empty_like(padded) for _ in range(world)]
-    dist.all_gather(parts, padded, group=group)
-    return torch.cat([p[: b - a] for p, (a, b) in zip(parts, sizes)])
+    if local.shape[0] == width:
+        padded = local.contiguous()
+    else:
+        padded = torch.zeros(width, dtype=local.dtype, device=local.device)
+        padded[: local.shape[0]] = local
+    full = out if out is not None else torch.empty(world * width, dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(full, padded, group=group)
+    if all(b - a == width for a, b in sizes):
+        return full[:n_total]
+    return torch.cat([full[r * width: r * width + (b - a)] for r, (a, b) in enumerate(sizes)])
 
 
 # ---------------------------------------------------------------------------------------
