@@ -27,6 +27,7 @@ an incoming plan against it exactly.
 from __future__ import annotations
 
 import os
+from itertools import product
 import re
 
 import numpy as np
@@ -471,7 +472,7 @@ def _signature_methods(plan: EvaluationPlan) -> str:
     coset in base K; the driver groups a brick's points by signature so that warps run one
     kernel per coset instead of every kernel that occurs among their lanes."""
     return f"""    static constexpr bool kSig = true;
-    static constexpr int kSigCount = {plan.K ** plan.M};
+    static constexpr int kSigCount = {len(set(kernel_programs(plan))) ** plan.M};
     static constexpr int kProgCount = {len(set(kernel_programs(plan)))};
     static constexpr int kMC = kM;
 """ + _word_class(plan) + """    template <class Ctx>
@@ -479,6 +480,9 @@ def _signature_methods(plan: EvaluationPlan) -> str:
         const int* sigma = reinterpret_cast<const int*>(ctx.tables);
         float frac[3] = {0.f, 0.f, 0.f};
         const bool fast = fast_frame(x, frac);
+        if constexpr (kCube) {  // all cosets' classes from the unit-cube table
+            if (fast) return reinterpret_cast<const unsigned*>(ctx.tables + kCubeOff)[cube_code(frac, ctx.X)];
+        }
         unsigned w = 0;
 #pragma unroll
         for (int k = 0; k < kM; ++k) {
@@ -500,7 +504,10 @@ def _signature_methods(plan: EvaluationPlan) -> str:
         const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
         int sig = 0;
 #pragma unroll
-        for (int k = 0; k < kM; ++k) sig = sig * """ + str(plan.K) + """ + (int)(cls_tab[max(word_class(word, k), 0)].x & 15u);
+        for (int k = 0; k < kM; ++k) {
+            const int kern = (int)(cls_tab[max(word_class(word, k), 0)].x & 15u);
+            sig = sig * """ + str(len(set(kernel_programs(plan)))) + """ + """ + _prog_select(plan) + """;  // program id
+        }
         return sig;
     }
 """
@@ -535,6 +542,114 @@ def _prog_select(plan: EvaluationPlan) -> str:
     for k in range(plan.K - 2, -1, -1):
         expr = f"(kern == {k} ? {ids[k]} : {expr})"
     return expr
+
+
+# ---------------------------------------------------------------------------------------
+# Unit-cube classification.  With X = floor(x), u = x - X in [0,1)^3 and d in {1, 2}, coset
+# k's frame is xp = u + m_k with m_k = (X - l_k) mod d (the parity of X), so every plane test
+# n.xp >= off of the plan is n.u >= off - n.m_k: for a normal in {-1,0,1}^3 either constant
+# (c <= min n.u or c >= sup n.u) or one of a few "genuine" tests n.u >= c.  The classes of ALL
+# cosets are therefore a function of (parity of X, how many thresholds each normal's n.u
+# reaches): a table of d^3 * prod(thresholds + 1) class words, built here in exact
+# arithmetic from the plan's own planes and sigma (runtime.py:374-379), replaces the M x Q
+# plane tests, M modulo reductions and M sigma lookups by ~10 float compares and one shared-
+# memory load.  Fast-domain points only (the sums n.u are exact in float32 there).
+
+CUBE_MAX_CODES = 8192
+
+
+def cube_tests(plan: EvaluationPlan):
+    """[(normal, [thresholds])] of the genuine unit-cube tests, or None when the plan does not
+    fit the scheme (d not in {1, 2} or not equal on all axes, normals outside {-1,0,1})."""
+    d = plan.diag[0]
+    if any(v != d for v in plan.diag) or d not in (1, 2) or plan.s != 3:
+        return None
+    tests = {}
+    for l in plan.shifts:
+        for p in product(range(d), repeat=3):
+            m = [(p[i] - int(l[i])) % d for i in range(3)]
+            for n, off in plan.planes:
+                if any(v not in (-1, 0, 1) for v in n):
+                    return None
+                c = Fraction(off) - sum(int(n[i]) * m[i] for i in range(3))
+                lo = sum(min(int(v), 0) for v in n)
+                hi = sum(max(int(v), 0) for v in n)
+                if lo < c < hi:
+                    tests.setdefault(tuple(int(v) for v in n), set()).add(c)
+    return [(n, sorted(t)) for n, t in sorted(tests.items())]
+
+
+def cube_table(plan: EvaluationPlan, tests) -> list:
+    """Class word per code (code = parity bits, then the per-normal states in mixed radix,
+    first normal most significant); kWordBits per coset, all ones = sigma sentinel."""
+    d = plan.diag[0]
+    bits = _word_bits(plan)
+    mask = (1 << bits) - 1
+    radices = [len(t) + 1 for _, t in tests]
+    table = []
+    for p in product(range(d), repeat=3):
+        for states in product(*[range(r) for r in radices]):
+            state = {n: st for (n, _), st in zip(tests, states)}
+            thr = {n: t for n, t in tests}
+            word = 0
+            for k, l in enumerate(plan.shifts):
+                m = [(p[i] - int(l[i])) % d for i in range(3)]
+                q = 0
+                for j, (n, off) in enumerate(plan.planes):
+                    nn = tuple(int(v) for v in n)
+                    c = Fraction(off) - sum(nn[i] * m[i] for i in range(3))
+                    lo = sum(min(v, 0) for v in nn)
+                    hi = sum(max(v, 0) for v in nn)
+                    if c <= lo:
+                        bit = 1
+                    elif c >= hi:
+                        bit = 0
+                    else:  # n.u >= c  <=>  state >= (index of c) + 1
+                        bit = 1 if state[nn] >= thr[nn].index(c) + 1 else 0
+                    q |= bit << j
+                cls = plan.sigma[q % plan.r]
+                word |= ((mask if cls < 0 else cls) & mask) << (bits * k)
+            table.append(word)
+    return table
+
+
+def _cube_source(plan: EvaluationPlan, fast_lo: float):
+    """(device source, table words) of the unit-cube classifier, or ("", None)."""
+    tests = cube_tests(plan)
+    if tests is None or _word_bits(plan) == 0 or os.environ.get("SP_CODEGEN_CUBE", "1") == "0":
+        return "", None
+    d = plan.diag[0]
+    ncodes = d ** 3
+    for _, t in tests:
+        ncodes *= len(t) + 1
+    # exactness: |n.u| < max |n|_1 must stay below 2^24 ulp(kFastLo) = 2 kFastLo
+    if ncodes > CUBE_MAX_CODES or max([sum(abs(v) for v in n) for n, _ in tests] + [0]) > 2 * fast_lo:
+        return "", None
+    lines = []
+    if d == 2:
+        lines.append("    int code = ((X[0] & 1) << 2) | ((X[1] & 1) << 1) | (X[2] & 1);")
+    else:
+        lines.append("    int code = 0;")
+    for n, thr in tests:
+        terms = []
+        for i, v in enumerate(n):
+            if v:
+                terms.append(("+ " if v > 0 else "- ") + f"u[{i}]")
+        expr = " ".join(terms).lstrip("+ ")
+        if expr.startswith("- "):
+            expr = "-" + expr[2:]
+        sts = " + ".join(f"(v >= {float(c)!r}f)" for c in thr)
+        lines.append(f"    {{ const float v = {expr}; code = code * {len(thr) + 1} + ({sts}); }}")
+    src = f"""
+// unit-cube classifier ({len(tests)} genuine tests, {ncodes} codes; see codegen.cube_tests)
+constexpr bool kCube = true;
+constexpr int kCubeCodes = {ncodes};
+__device__ __forceinline__ int cube_code(const float u[3], const int X[3]) {{
+{chr(10).join(lines)}
+    return code;
+}}
+"""
+    return src, cube_table(plan, tests)
 
 
 def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple:
@@ -581,14 +696,31 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
     fast_lo = 1.0
     while fast_lo < max(rmax / 2.0, float(d), 1.0):
         fast_lo *= 2.0
+    cube_src, cube_tab = _cube_source(plan, fast_lo)
+    if cube_tab is None:
+        cube_src = '''
+constexpr bool kCube = false;
+constexpr int kCubeCodes = 0;
+__device__ __forceinline__ int cube_code(const float u[3], const int X[3]) { return 0; }
+'''
+    else:
+        cube_src += "static const uint32_t kCubeTab[" + str(len(cube_tab)) + "] = {" + ", ".join(
+            f"{w:#x}u" for w in cube_tab) + "};\n"
     if plan.K == 1:
         dispatch = "            const T acc = kernel0<T>(y0, y1, y2, f);"
     else:
+        # one case per distinct weight program (identical kernels share one: no divergence
+        # between lanes whose classes select different-but-identical kernels)
+        progs = kernel_programs(plan)
+        rep = {}
+        for k, pid in enumerate(progs):
+            rep.setdefault(pid, k)
         cases = "\n".join(
-            f"                case {k}: acc = kernel{k}<T>(y0, y1, y2, f); break;" for k in range(plan.K)
+            f"                case {pid}: acc = kernel{k}<T>(y0, y1, y2, f); break;" for pid, k in sorted(rep.items())
         )
-        dispatch = f"            T acc = T(0);\n            switch (kern) {{\n{cases}\n            }}"
-    sig_ok = plan.K > 1 and _word_bits(plan) > 0 and plan.K ** plan.M <= 1024
+        dispatch = (f"            T acc = T(0);\n            const int prog = {_prog_select(plan)};\n"
+                    f"            switch (prog) {{\n{cases}\n            }}")
+    sig_ok = plan.K > 1 and _word_bits(plan) > 0 and len(set(kernel_programs(plan))) ** plan.M <= 1024
     sig_methods = _signature_methods(plan) if sig_ok else "    static constexpr bool kSig = false;\n" + _word_class(plan)
     if aff is not None:
         eval_src = _affine_eval_source(plan, aff[0], aff[1], min_blocks)
@@ -698,12 +830,23 @@ struct Eval {{
         return acc;
     }}
     template <bool kWord, class F, class Ctx>
-    __device__ __forceinline__ static T eval_impl(const T x[3], unsigned word, F& f, const Ctx& ctx) {{
-        float frac[3] = {{0.f, 0.f, 0.f}};
-        const bool fast = fast_frame(x, frac);
+    __device__ __forceinline__ static T sum_cosets(const T x[3], bool fast, const float frac[3], unsigned word, F& f,
+                                                   const Ctx& ctx) {{
         T total = T(0);
         total += eval_coset<kWord, 0>(x, fast, frac, word, 0, f, ctx);
 {''.join(f"        total += eval_coset<kWord, {k}>(x, fast, frac, word, {k}, f, ctx);" + chr(10) for k in range(1, plan.M))}        return total;
+    }}
+    template <bool kWord, class F, class Ctx>
+    __device__ __forceinline__ static T eval_impl(const T x[3], unsigned word, F& f, const Ctx& ctx) {{
+        float frac[3] = {{0.f, 0.f, 0.f}};
+        const bool fast = fast_frame(x, frac);
+        if constexpr (!kWord && kCube) {{  // fast-domain points: classes from the unit-cube table
+            if (fast)
+                return sum_cosets<true>(x, true, frac,
+                                        reinterpret_cast<const unsigned*>(ctx.tables + kCubeOff)[cube_code(frac, ctx.X)],
+                                        f, ctx);
+        }}
+        return sum_cosets<kWord>(x, fast, frac, word, f, ctx);
     }}
     // coset-item driver (eval_brick_items): program id of coset k's kernel for class word
     // `word` (identical kernel programs share an id) and the per-coset evaluation with a
@@ -754,6 +897,8 @@ __device__ constexpr int kShiftI[kM][3] = {{{", ".join("{" + ", ".join(str(int(v
 __device__ __forceinline__ int shift_i(int k, int i) {{
 {_shift_select(plan)}
 }}
+{cube_src}
+constexpr int kCubeOff = kSigmaBytes + kN * 16;  // cube table offset in the smem tables
 
 template <typename R>
 __device__ __forceinline__ int plane_code(const R xp0, const R xp1, const R xp2) {{
@@ -857,6 +1002,8 @@ extern const sp::GenEntry kGen_{ident} = {{
     &sp::occupancy_bricks<double, sp::gen_{ident}::Eval<double>>,
     sp::gen_{ident}::Eval<float>::kTrecBytes,
     &sp::launch_tex<sp::gen_{ident}::Eval<float>>,
+    {"sp::gen_" + ident + "::kCubeTab" if cube_tab is not None else "nullptr"},
+    {len(cube_tab) if cube_tab is not None else 0},
 }};
 """
     return src, {"ident": ident, "flops_per_coset": kflops, "words": len(words), "affine": aff is not None}

@@ -149,6 +149,8 @@ struct GenEntry {
     int (*bocc_f64)(size_t);
     int trec_bytes;  // per-tile address records (+ tables) in smem
     TexLaunchFn tex_f32;  // hardware-texture variant (float32)
+    const uint32_t* cube_tab;  // unit-cube class-word table (codegen.cube_table), or null
+    int cube_len;
 };
 
 }  // namespace sp

@@ -356,7 +356,10 @@ int sp_plan_create(const sp_plan_desc* desc, sp_plan** out) {
     if (p->gen) {
         // smem tables: int32 sigma[r] (16B aligned) + uint4 class records [N]
         const int sig_bytes = ((d.r * 4) + 15) & ~15;
-        std::vector<uint32_t> blob(sig_bytes / 4 + 4 * d.N, 0);
+        // ... + the generated unit-cube class-word table (codegen.cube_table), when present
+        std::vector<uint32_t> blob(sig_bytes / 4 + 4 * d.N + (p->gen->cube_tab ? p->gen->cube_len : 0), 0);
+        if (p->gen->cube_tab)
+            std::memcpy(blob.data() + sig_bytes / 4 + 4 * d.N, p->gen->cube_tab, (size_t)p->gen->cube_len * 4);
         for (int j = 0; j < d.r; ++j) blob[j] = (uint32_t)d.sigma[j];
         for (int c = 0; c < d.N; ++c) {
             int perm[3], sign[3], rho[3], tau[3];
