@@ -365,8 +365,8 @@ struct Eval {{
     // class max(sigma[q], 0), then the per-q coefficient table (computed per tile)
     __device__ static void tile_records(const EvalArgs<T>& a, const TileGeom& g, const unsigned char* tables,
                                         int4* trec, int tid) {{
-        const int* sigma = reinterpret_cast<const int*>(tables);
-        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
+        const int* sigma = reinterpret_cast<const int*>(tables + kSigOff);
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kClsOff);
         for (int idx = tid; idx < kM * kR; idx += kThreads) {{
             const int k = idx / kR, q = idx - k * kR;
             const uint4 rec = cls_tab[max(sigma[q], 0)];
@@ -388,7 +388,7 @@ struct Eval {{
     template <class F, class Ctx>
     __device__ __forceinline__ static T eval(const T x[3], F& f, const Ctx& ctx) {{
         const EvalArgs<T>& a = *ctx.a;
-        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
+        const int* sigma = sigma_of(ctx);
         bool fast = false;
         float frac[3] = {{0.f, 0.f, 0.f}};
         if constexpr (sizeof(T) == 4) {{
@@ -427,7 +427,7 @@ struct Eval {{
                 f.c2 = tr.z;
                 co = reinterpret_cast<const uint4*>(ctx.trec + kM * kR) + q * kNV;
             }} else {{
-                const uint4 rec = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes)[max(sigma[q], 0)];
+                const uint4 rec = reinterpret_cast<const uint4*>(ctx.tables + kClsOff)[max(sigma[q], 0)];
                 int rho[3], tau[3], base[3];
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {{
@@ -477,7 +477,7 @@ def _signature_methods(plan: EvaluationPlan) -> str:
     static constexpr int kMC = kM;
 """ + _word_class(plan) + """    template <class Ctx>
     __device__ __forceinline__ static unsigned classify_word(const T x[3], const Ctx& ctx) {
-        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
+        const int* sigma = sigma_of(ctx);
         float frac[3] = {0.f, 0.f, 0.f};
         const bool fast = fast_frame(x, frac);
         if constexpr (kCube) {  // all cosets' classes from the unit-cube table
@@ -501,7 +501,7 @@ def _signature_methods(plan: EvaluationPlan) -> str:
         return w;
     }
     __device__ __forceinline__ static int signature(unsigned word, const unsigned char* tables) {
-        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kClsOff);
         int sig = 0;
 #pragma unroll
         for (int k = 0; k < kM; ++k) {
@@ -696,7 +696,7 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
     fast_lo = 1.0
     while fast_lo < max(rmax / 2.0, float(d), 1.0):
         fast_lo *= 2.0
-    cube_src, cube_tab = _cube_source(plan, fast_lo)
+    cube_src, cube_tab = _cube_source(plan, fast_lo) if aff is None else ("", None)
     if cube_tab is None:
         cube_src = '''
 constexpr bool kCube = false;
@@ -737,7 +737,7 @@ struct Eval {{
     // {{coef of site/d component 0, 1, 2; constant offset of pib/d}} (computed per tile)
     __device__ static void tile_records(const EvalArgs<T>& a, const TileGeom& g, const unsigned char* tables,
                                         int4* trec, int tid) {{
-        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kClsOff);
         for (int idx = tid; idx < kM * kN; idx += kThreads) {{
             const int k = idx / kN, c = idx - k * kN;
             const uint4 rec = cls_tab[c];
@@ -783,8 +783,8 @@ struct Eval {{
     __device__ __forceinline__ static T eval_coset(const T x[3], bool fast, const float frac[3], unsigned word, int k,
                                                    F& f, const Ctx& ctx) {{
         const EvalArgs<T>& a = *ctx.a;
-        const int* sigma = reinterpret_cast<const int*>(ctx.tables);
-        const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kSigmaBytes);
+        const int* sigma = sigma_of(ctx);
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(ctx.tables + kClsOff);
         if (KC >= 0) k = KC;
         int cell[3];
         T yy[3];
@@ -852,7 +852,7 @@ struct Eval {{
     // `word` (identical kernel programs share an id) and the per-coset evaluation with a
     // runtime coset index
     __device__ __forceinline__ static int item_kernel(unsigned word, int k, const unsigned char* tables) {{
-        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kSigmaBytes);
+        const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kClsOff);
         const int kern = (int)(cls_tab[max(word_class(word, k), 0)].x & 15u);
         return {_prog_select(plan)};
     }}
@@ -898,7 +898,18 @@ __device__ __forceinline__ int shift_i(int k, int i) {{
 {_shift_select(plan)}
 }}
 {cube_src}
-constexpr int kCubeOff = kSigmaBytes + kN * 16;  // cube table offset in the smem tables
+// plan tables (sp_plan_create): class records | unit-cube table | sigma.  With the cube table
+// only the first two are staged into shared memory (sigma serves the rare float64-frame points
+// from global memory); without it all three are.
+constexpr int kClsOff = 0;
+constexpr int kCubeOff = kN * 16;
+constexpr int kSigOff = kCubeOff + ((kCubeCodes * 4 + 15) & ~15);
+constexpr int kSmemTableBytes = kCube ? kSigOff : kSigOff + kSigmaBytes;
+template <class Ctx>
+__device__ __forceinline__ const int* sigma_of(const Ctx& ctx) {{
+    return kCube ? reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(ctx.a->tables) + kSigOff)
+                 : reinterpret_cast<const int*>(ctx.tables + kSigOff);
+}}
 
 template <typename R>
 __device__ __forceinline__ int plane_code(const R xp0, const R xp1, const R xp2) {{
@@ -1004,6 +1015,7 @@ extern const sp::GenEntry kGen_{ident} = {{
     &sp::launch_tex<sp::gen_{ident}::Eval<float>>,
     {"sp::gen_" + ident + "::kCubeTab" if cube_tab is not None else "nullptr"},
     {len(cube_tab) if cube_tab is not None else 0},
+    sp::gen_{ident}::kSmemTableBytes,
 }};
 """
     return src, {"ident": ident, "flops_per_coset": kflops, "words": len(words), "affine": aff is not None}

@@ -151,6 +151,7 @@ struct GenEntry {
     TexLaunchFn tex_f32;  // hardware-texture variant (float32)
     const uint32_t* cube_tab;  // unit-cube class-word table (codegen.cube_table), or null
     int cube_len;
+    int smem_table_bytes;      // leading bytes of the plan tables staged into shared memory
 };
 
 }  // namespace sp

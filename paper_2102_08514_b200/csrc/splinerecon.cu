@@ -354,13 +354,15 @@ int sp_plan_create(const sp_plan_desc* desc, sp_plan** out) {
     }
 
     if (p->gen) {
-        // smem tables: int32 sigma[r] (16B aligned) + uint4 class records [N]
+        // plan tables (generated layout, codegen kClsOff / kCubeOff / kSigOff): uint4 class
+        // records [N] | unit-cube class-word table (codegen.cube_table, 16 B aligned) | int32
+        // sigma[r]; the leading gen->smem_table_bytes are staged into shared memory
         const int sig_bytes = ((d.r * 4) + 15) & ~15;
-        // ... + the generated unit-cube class-word table (codegen.cube_table), when present
-        std::vector<uint32_t> blob(sig_bytes / 4 + 4 * d.N + (p->gen->cube_tab ? p->gen->cube_len : 0), 0);
-        if (p->gen->cube_tab)
-            std::memcpy(blob.data() + sig_bytes / 4 + 4 * d.N, p->gen->cube_tab, (size_t)p->gen->cube_len * 4);
-        for (int j = 0; j < d.r; ++j) blob[j] = (uint32_t)d.sigma[j];
+        const int cube_words = p->gen->cube_tab ? ((p->gen->cube_len + 3) & ~3) : 0;
+        const int sig_off = 4 * d.N + cube_words;  // in 32-bit words
+        std::vector<uint32_t> blob(sig_off + sig_bytes / 4, 0);
+        if (p->gen->cube_tab) std::memcpy(blob.data() + 4 * d.N, p->gen->cube_tab, (size_t)p->gen->cube_len * 4);
+        for (int j = 0; j < d.r; ++j) blob[sig_off + j] = (uint32_t)d.sigma[j];
         for (int c = 0; c < d.N; ++c) {
             int perm[3], sign[3], rho[3], tau[3];
             if (!signed_perm(d.cls_T + 9 * c, perm, sign)) { delete p; return fail(SP_ERR_INVALID, "generated plan needs signed-permutation T"); }
@@ -383,14 +385,15 @@ int sp_plan_create(const sp_plan_desc* desc, sp_plan** out) {
                 if (pbd < -4 || pbd > 3) { delete p; return fail(SP_ERR_UNSUPPORTED, "class offset out of range"); }
                 x |= (uint32_t)(pbd + 4) << (22 + 3 * i);
             }
-            uint32_t* rec = blob.data() + sig_bytes / 4 + 4 * c;
+            uint32_t* rec = blob.data() + 4 * c;
             rec[0] = x;
             std::memcpy(rec + 1, tf, sizeof tf);
         }
         const uint32_t* dptr = nullptr;
         if (upload(p, blob, &dptr) != SP_OK) { delete p; return SP_ERR_CUDA; }
         p->d_tables = (void*)dptr;
-        p->table_bytes = (int)(blob.size() * 4);
+        p->table_bytes = p->gen->smem_table_bytes;  // staged into shared memory
+        if (p->table_bytes > (int)(blob.size() * 4)) { delete p; return fail(SP_ERR_INVALID, "plan table layout"); }
         p->kind = SP_KIND_GENERATED;
         p->name = std::string("gen:") + p->gen->name;
         *out = p;
