@@ -616,7 +616,10 @@ def cube_table(plan: EvaluationPlan, tests) -> list:
 def _cube_source(plan: EvaluationPlan, fast_lo: float):
     """(device source, table words) of the unit-cube classifier, or ("", None)."""
     tests = cube_tests(plan)
-    if tests is None or _word_bits(plan) == 0 or os.environ.get("SP_CODEGEN_CUBE", "1") == "0":
+    # single-coset plans: the cube tests cost as much as the plan's own plane tests (cc_zp3:
+    # 28.1 -> 26.2 Gpts/s measured with the table), so they keep the plane tests
+    if (tests is None or plan.M == 1 or _word_bits(plan) == 0
+            or os.environ.get("SP_CODEGEN_CUBE", "1") == "0"):
         return "", None
     d = plan.diag[0]
     ncodes = d ** 3

@@ -736,15 +736,26 @@ __device__ __forceinline__ void eval_brick_sig(const EvalArgs<T>& a, EvalCtx<T, 
     __shared__ unsigned short s_order[kSeg];
     __shared__ unsigned short s_key[kSeg];
     __shared__ int s_hist[kBuckets];
-    __shared__ T s_pts[3 * kSeg];
+    __shared__ __align__(16) T s_pts[3 * kSeg];
     const int tid = threadIdx.x, lane = tid & 31;
-    for (long long seg = p0; seg < p1; seg += kSeg) {
-        const int n = (int)min((long long)kSeg, p1 - seg);
+    // segments after the first start on a 16-byte boundary of the point array (vector loads)
+    constexpr int kAlignPts = sizeof(T) == 4 ? 4 : 2;
+    for (long long seg = p0, len = kSeg - (p0 % kAlignPts); seg < p1; seg += len, len = kSeg) {
+        const int n = (int)min(len, p1 - seg);
         for (int i = tid; i < kBuckets; i += kThreads) s_hist[i] = 0;
-        // the segment's points -> shared memory (coalesced, all loads in flight together)
-        {
+        // the segment's points -> shared memory (coalesced, all loads in flight together;
+        // 16-byte vectors for brick-order points with a 16-byte aligned segment start)
+        const T* src = a.pts + 3 * seg;
+        constexpr int kVecE = 16 / (int)sizeof(T);
+        if (!a.in_index32 && n == kSeg && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            constexpr int kNV = 3 * kSeg / kVecE / kThreads;
+            int4 v[kNV];
+#pragma unroll
+            for (int q = 0; q < kNV; ++q) v[q] = __ldg(reinterpret_cast<const int4*>(src) + tid + q * kThreads);
+#pragma unroll
+            for (int q = 0; q < kNV; ++q) reinterpret_cast<int4*>(s_pts)[tid + q * kThreads] = v[q];
+        } else {
             T v[3 * kPer];
-            const T* src = a.pts + 3 * seg;
 #pragma unroll
             for (int q = 0; q < 3 * kPer; ++q) {
                 const int e = tid + q * kThreads;
