@@ -172,6 +172,17 @@ int64_t sp_sort_points_temp_bytes(int64_t n);
 int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t lo0, int32_t lo1, int32_t lo2, int32_t bits,
                    int32_t log2_brick, void* sorted_pts, int32_t* perm, int64_t* brick_start, int32_t* n_bricks,
                    void* temp, int64_t temp_bytes, void* stream);
+/* sp_sort_points_payload: protocol B with the points as the sort payload — brick-id keys
+ * (Morton order of the bricks of 2^log2_brick cells in the frame lo + [0, 2^bits)^3, cells
+ * clamped into the frame), a radix sort of (key, {point, index}) over the brick-id bits only,
+ * the sorted points written to sorted_pts ((n,3), required) and their caller indices to perm,
+ * and the brick runs; the points are read once, coalesced, instead of through the permutation
+ * by the brick kernel.  Pair with sp_eval_bricks_perm32 (results in the caller's order) or
+ * sp_eval_bricks_dev (brick order).  temp: sp_sort_points_payload_temp_bytes(n, dtype) bytes. */
+int64_t sp_sort_points_payload_temp_bytes(int64_t n, int32_t dtype);
+int sp_sort_points_payload(const void* pts, int64_t n, int32_t dtype, int32_t lo0, int32_t lo1, int32_t lo2,
+                           int32_t bits, int32_t log2_brick, void* sorted_pts, int32_t* perm, int64_t* brick_start,
+                           int32_t* n_bricks, void* temp, int64_t temp_bytes, void* stream);
 int sp_eval_bricks_perm32(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,
                           const int64_t* brick_start, const int32_t* n_bricks_dev, int32_t n_bricks_cap,
                           int32_t log2_brick, const int32_t* perm, void* out, int32_t* err_flag, void* stream);

@@ -1260,6 +1260,165 @@ extern "C" int sp_sort_points(const void* pts, int64_t n, int32_t dtype, int32_t
     return SP_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// Protocol B with the points as the sort payload (sp_sort_points_payload): the caller's
+// points are read ONCE, coalesced, and moved through the radix sort together with their
+// index, so the brick kernel afterwards reads them in brick order (no random 12/24-byte point
+// reads through a permutation, which cost ~128 B of DRAM traffic per point).  Only the brick
+// id is sorted (3 * (bits - log2_brick) bits: 2 onesweep passes for <= 2^16 bricks): the brick
+// kernels need each brick's points contiguous, not Morton order inside the brick.
+template <typename T>
+struct PtIdx;  // 16 B (fp32) / 32 B (fp64) sort payload: the point and its caller index
+template <>
+struct __align__(16) PtIdx<float> {
+    float x, y, z;
+    int i;
+};
+template <>
+struct __align__(16) PtIdx<double> {
+    double x, y, z;
+    long long i;
+};
+
+template <typename T>
+__global__ void brick_key_payload_kernel(const T* __restrict__ pts, long long n, int lo0, int lo1, int lo2, int bits,
+                                         int log2b, int* __restrict__ keys, PtIdx<T>* __restrict__ vals) {
+    const int hi = (1 << bits) - 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const T x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+        const int c0 = min(max(sp::clamp_cell(x) - lo0, 0), hi) >> log2b;
+        const int c1 = min(max(sp::clamp_cell(y) - lo1, 0), hi) >> log2b;
+        const int c2 = min(max(sp::clamp_cell(z) - lo2, 0), hi) >> log2b;
+        keys[i] = (int)(spread3((uint32_t)c2) | (spread3((uint32_t)c1) << 1) | (spread3((uint32_t)c0) << 2));
+        PtIdx<T> v;
+        v.x = x;
+        v.y = y;
+        v.z = z;
+        v.i = (decltype(v.i))i;
+        vals[i] = v;
+    }
+}
+
+template <typename T>
+__global__ void split_payload_kernel(const PtIdx<T>* __restrict__ vals, long long n, T* __restrict__ pts,
+                                     int32_t* __restrict__ perm) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const PtIdx<T> v = vals[i];
+        pts[3 * i] = v.x;
+        pts[3 * i + 1] = v.y;
+        pts[3 * i + 2] = v.z;
+        perm[i] = (int32_t)v.i;
+    }
+}
+
+namespace {
+template <typename T>
+size_t payload_cub_bytes(int64_t n, int end_bit) {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                    static_cast<const PtIdx<T>*>(nullptr), static_cast<PtIdx<T>*>(nullptr), (int)n, 0,
+                                    end_bit);
+    cub::DeviceSelect::If(nullptr, b, static_cast<const int32_t*>(nullptr), static_cast<int64_t*>(nullptr),
+                          static_cast<int32_t*>(nullptr), (int)std::min<int64_t>(n, 1 << 30), IsHead{});
+    return std::max(a, b);
+}
+}  // namespace
+
+extern "C" int64_t sp_sort_points_payload_temp_bytes(int64_t n, int32_t dtype) {
+    if (n <= 0 || n >= (1ll << 31)) return 0;
+    const size_t vb = dtype == SP_F64 ? sizeof(PtIdx<double>) : sizeof(PtIdx<float>);
+    const size_t cub = dtype == SP_F64 ? payload_cub_bytes<double>(n, 30) : payload_cub_bytes<float>(n, 30);
+    return (int64_t)(2 * align256((size_t)n * 4) + 2 * align256((size_t)n * vb) + cub);
+}
+
+extern "C" int sp_sort_points_payload(const void* pts, int64_t n, int32_t dtype, int32_t lo0, int32_t lo1, int32_t lo2,
+                                      int32_t bits, int32_t log2_brick, void* sorted_pts, int32_t* perm,
+                                      int64_t* brick_start, int32_t* n_bricks, void* temp, int64_t temp_bytes,
+                                      void* stream) {
+    if (n < 0 || n >= (1ll << 31)) return fail(SP_ERR_INVALID, "sort points: n out of range");
+    if (bits < 0 || bits > 10) return fail(SP_ERR_INVALID, "bits must be in [0, 10]");
+    if (log2_brick < 0 || log2_brick > bits) return fail(SP_ERR_INVALID, "log2_brick out of range");
+    if (dtype != SP_F32 && dtype != SP_F64) return fail(SP_ERR_INVALID, "unknown dtype");
+    if (!brick_start || !n_bricks || (n > 0 && (!pts || !perm || !sorted_pts))) return fail(SP_ERR_INVALID, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        SP_CUDA(cudaMemsetAsync(n_bricks, 0, sizeof(int32_t), st));
+        SP_CUDA(cudaMemsetAsync(brick_start, 0, sizeof(int64_t), st));
+        return SP_OK;
+    }
+    const int kbits = 3 * (bits - log2_brick);  // brick-id bits
+    const size_t vb = dtype == SP_F64 ? sizeof(PtIdx<double>) : sizeof(PtIdx<float>);
+    const size_t kseg = align256((size_t)n * 4), vseg = align256((size_t)n * vb);
+    const size_t cub_bytes = dtype == SP_F64 ? payload_cub_bytes<double>(n, 30) : payload_cub_bytes<float>(n, 30);
+    const size_t need = 2 * kseg + 2 * vseg + cub_bytes;
+    void* tmp = temp;
+    if (!tmp || (size_t)temp_bytes < need) {
+        tmp = nullptr;
+        SP_CUDA(cudaMallocAsync(&tmp, need, st));
+    }
+    unsigned char* base = static_cast<unsigned char*>(tmp);
+    int32_t* k_in = reinterpret_cast<int32_t*>(base);
+    int32_t* k_out = reinterpret_cast<int32_t*>(base + kseg);
+    void* v_in = base + 2 * kseg;
+    void* v_out = base + 2 * kseg + vseg;
+    void* cub_tmp = base + 2 * kseg + 2 * vseg;
+    cudaError_t e = cudaSuccess;
+    size_t cb = cub_bytes;
+    if (dtype == SP_F32) {
+        brick_key_payload_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)pts, n, lo0, lo1, lo2, bits, log2_brick,
+                                                                     k_in, (PtIdx<float>*)v_in);
+        e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cub::DeviceRadixSort::SortPairs(cub_tmp, cb, k_in, k_out, (const PtIdx<float>*)v_in,
+                                                (PtIdx<float>*)v_out, (int)n, 0, std::max(kbits, 1), st);
+        if (e == cudaSuccess) {
+            split_payload_kernel<float><<<grid_for(n), 256, 0, st>>>((const PtIdx<float>*)v_out, n, (float*)sorted_pts, perm);
+            e = cudaGetLastError();
+        }
+    } else {
+        brick_key_payload_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)pts, n, lo0, lo1, lo2, bits,
+                                                                      log2_brick, k_in, (PtIdx<double>*)v_in);
+        e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cub::DeviceRadixSort::SortPairs(cub_tmp, cb, k_in, k_out, (const PtIdx<double>*)v_in,
+                                                (PtIdx<double>*)v_out, (int)n, 0, std::max(kbits, 1), st);
+        if (e == cudaSuccess) {
+            split_payload_kernel<double><<<grid_for(n), 256, 0, st>>>((const PtIdx<double>*)v_out, n, (double*)sorted_pts,
+                                                                      perm);
+            e = cudaGetLastError();
+        }
+    }
+    // brick runs: the keys ARE brick ids; heads scattered by brick id (k_in is free after the
+    // sort) and compacted when there are at most n bricks, else a compaction over the n keys
+    if (e == cudaSuccess) {
+        const long long nb = 1ll << kbits;
+        size_t sel = 0;
+        const bool by_heads = nb <= n && cub::DeviceSelect::If(nullptr, sel, k_in, brick_start, n_bricks, (int)nb,
+                                                               IsHead{}, st) == cudaSuccess;
+        if (by_heads && sel <= cub_bytes) {
+            e = cudaMemsetAsync(k_in, 0xff, (size_t)nb * 4, st);
+            if (e == cudaSuccess) {
+                brick_heads32_kernel<<<grid_for(n), 256, 0, st>>>(k_out, n, 0, k_in);
+                e = cudaGetLastError();
+            }
+            cb = cub_bytes;
+            if (e == cudaSuccess) e = cub::DeviceSelect::If(cub_tmp, cb, k_in, brick_start, n_bricks, (int)nb, IsHead{}, st);
+        } else {
+            thrust::counting_iterator<long long> idx(0);
+            const BrickHead32 head{k_out, 0};
+            cb = cub_bytes;
+            e = cub::DeviceSelect::If(cub_tmp, cb, idx, brick_start, n_bricks, (int)n, head, st);
+        }
+    }
+    if (e == cudaSuccess) {
+        brick_runs_tail<<<1, 1, 0, st>>>(n, n_bricks, brick_start);
+        e = cudaGetLastError();
+    }
+    if (tmp != temp) cudaFreeAsync(tmp, st);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "sort points (payload): %s", cudaGetErrorString(e));
+    return SP_OK;
+}
+
 extern "C" int sp_eval_bricks_perm32(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n,
                                      int32_t dtype, const int64_t* brick_start, const int32_t* n_bricks_dev,
                                      int32_t n_bricks_cap, int32_t log2_brick, const int32_t* perm, void* out,

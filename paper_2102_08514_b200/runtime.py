@@ -462,6 +462,10 @@ class PlanInterpreter:
     # (True) or let the brick kernel read them through the permutation (False)
     sort_gather = os.environ.get("SP_SORT_GATHER", "0") == "1"
 
+    # protocol B: move the points through the radix sort as its payload (brick-id keys, the
+    # points read once, coalesced) instead of reading them through the permutation
+    sort_payload = os.environ.get("SP_SORT_PAYLOAD", "1") == "1"
+
     # protocol-B workspaces kept (one per thread x stream x batch shape, most recent first out)
     sort_ws_keep = 4
 
@@ -608,7 +612,7 @@ class PlanInterpreter:
                              stream: torch.cuda.Stream | None = None):
         """Protocol B without the return to caller order: (values, perm) with values[k] the
         reconstruction at pts[perm[k]] (perm int32 on the grid's device — a valid index tensor,
-        int64 from 2^31 points; Morton brick order),
+        int64 from 2^31 points; brick order: grouped by brick, caller order within a brick),
         bit-identical to eval_batch(grid, pts)[perm].  For reductions over the batch (error
         norms, sums, histograms) the random per-value result writes of eval_batch(order=
         "sort") are skipped (sp_eval_bricks_unordered).  Device points, 3-D plans."""
@@ -653,15 +657,18 @@ class PlanInterpreter:
         # one cached workspace per (thread, stream): reuse is stream-ordered, and concurrent
         # callers never share one; allocated on `st` so that the caching
         # allocator recycles it in that stream's order when it is dropped
-        key = (threading.get_ident(), st.cuda_stream, dev.index, n, grid.dtype, self.sort_gather)
+        payload = self.sort_payload
+        key = (threading.get_ident(), st.cuda_stream, dev.index, n, grid.dtype, self.sort_gather, payload)
         with self._lock:
             cache = self.__dict__.setdefault("_sort_ws", {})
             ws = cache.pop(key, None)
         if ws is None:
+            tb = (lib.sp_sort_points_payload_temp_bytes(n, dtype) if payload else lib.sp_sort_points_temp_bytes(n))
             with torch.cuda.stream(st):
-                ws = (torch.empty_like(p) if self.sort_gather else None, torch.empty(n, dtype=torch.int32, device=dev),
+                ws = (torch.empty_like(p) if (self.sort_gather or payload) else None,
+                      torch.empty(n, dtype=torch.int32, device=dev),
                       torch.empty(n + 1, dtype=torch.int64, device=dev), torch.empty(1, dtype=torch.int32, device=dev),
-                      torch.empty(max(1, int(lib.sp_sort_points_temp_bytes(n))), dtype=torch.uint8, device=dev))
+                      torch.empty(max(1, int(tb)), dtype=torch.uint8, device=dev))
         with self._lock:
             cache[key] = ws
             while len(cache) > self.sort_ws_keep:
@@ -674,6 +681,23 @@ class PlanInterpreter:
             if unordered:  # the permutation is returned: not the cached workspace's
                 perm = torch.empty(n, dtype=torch.int32, device=dev)
                 gather = False
+            if payload:
+                # points moved through the radix sort (read once, coalesced), then the brick
+                # kernel on the sorted copy: results scattered to the caller's order (perm32)
+                # or left in brick order (unordered)
+                _native.check(lib.sp_sort_points_payload(p.data_ptr(), n, dtype, lo0, lo1, lo2, bits, b, sp_.data_ptr(),
+                                                         perm.data_ptr(), start.data_ptr(), count.data_ptr(),
+                                                         tmp.data_ptr(), tmp.numel(), st.cuda_stream))
+                if unordered:
+                    _native.check(lib.sp_eval_bricks_dev(h, ctypes.byref(gdesc), sp_.data_ptr(), n, dtype,
+                                                         start.data_ptr(), count.data_ptr(), n, b, None, res.data_ptr(),
+                                                         None if err is None else err.data_ptr(), st.cuda_stream))
+                    return perm
+                _native.check(lib.sp_eval_bricks_perm32(h, ctypes.byref(gdesc), sp_.data_ptr(), n, dtype,
+                                                        start.data_ptr(), count.data_ptr(), n, b, perm.data_ptr(),
+                                                        res.data_ptr(), None if err is None else err.data_ptr(),
+                                                        st.cuda_stream))
+                return None
             _native.check(lib.sp_sort_points(p.data_ptr(), n, dtype, lo0, lo1, lo2, bits, b,
                                              sp_.data_ptr() if gather else None, perm.data_ptr(), start.data_ptr(),
                                              count.data_ptr(), tmp.data_ptr(), tmp.numel(), st.cuda_stream))
