@@ -463,8 +463,12 @@ class PlanInterpreter:
     sort_gather = os.environ.get("SP_SORT_GATHER", "0") == "1"
 
     # protocol B: move the points through the radix sort as its payload (brick-id keys, the
-    # points read once, coalesced) instead of reading them through the permutation
-    sort_payload = os.environ.get("SP_SORT_PAYLOAD", "1") == "1"
+    # points read once, coalesced) instead of reading them through the permutation.  Measured
+    # (1e8 tricubic points, tools/protocol_b_timing.py): the 16-byte payload makes each onesweep
+    # pass 1.1 ms (3.3 ms for 3 passes, 4.7 ms with keys and split) and brick-sorted points
+    # without Morton order inside the brick cost the TMA kernel 1.97 ms instead of 0.9 — 9.14 ms
+    # in total vs 9.24 ms for the permuted-read path, so it stays off by default
+    sort_payload = os.environ.get("SP_SORT_PAYLOAD", "0") == "1"
 
     # protocol-B workspaces kept (one per thread x stream x batch shape, most recent first out)
     sort_ws_keep = 4
