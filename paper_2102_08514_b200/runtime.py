@@ -328,6 +328,17 @@ class PlanInterpreter:
         p = pts.to(device=grid.device, dtype=grid.dtype)
         return prepare_points(p, b, presorted=presorted)
 
+    def program(self):
+        """The plan's normative scalar program (runtime.py:227-230 -> build_program,
+        plancompile.py:564-699): a minilang.KernelProgram, rendered identically to the
+        reference's emit_kernel; minilang.execute runs it with injected fetches (host-side
+        specification aid, like the reference's; evaluation here runs on the GPU)."""
+        if self.__dict__.get("_program") is None:
+            from .minilang import build_program
+
+            self._program = build_program(self.plan)
+        return self._program
+
     def kernel_name(self, device=None) -> str:
         if self._lift is not None:
             return self._lift.kernel_name(device)
