@@ -180,6 +180,11 @@ EXPORTS = {
          ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
          ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
     ),
+    "sp_brick_runs_points": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
+    ),
     "sp_sort_points_payload_temp_bytes": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32]),
     "sp_sort_points_payload": (
         ctypes.c_int,

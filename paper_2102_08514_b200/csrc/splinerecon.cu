@@ -1073,6 +1073,34 @@ struct BrickHead {
 
 __global__ void brick_runs_tail(long long n, const int32_t* count, int64_t* brick_start) { brick_start[*count] = n; }
 
+// Brick heads straight from Morton-ordered points (sp_brick_runs_points): the brick key of
+// a point is the 64-bit Morton key of its clamped, biased unit cell (morton_kernel) shifted by
+// 3*log2b, i.e. the Morton code of its brick; no key array is written.
+__device__ __forceinline__ uint64_t brick_key_of(const float* p, int shift) {
+    uint32_t c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) c[a] = (uint32_t)min(max(sp::clamp_cell(p[a]) + (1 << 20), 0), (1 << 21) - 1);
+    return (spread3(c[2]) | (spread3(c[1]) << 1) | (spread3(c[0]) << 2)) >> shift;
+}
+__device__ __forceinline__ uint64_t brick_key_of(const double* p, int shift) {
+    uint32_t c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) c[a] = (uint32_t)min(max(sp::clamp_cell(p[a]) + (1 << 20), 0), (1 << 21) - 1);
+    return (spread3(c[2]) | (spread3(c[1]) << 1) | (spread3(c[0]) << 2)) >> shift;
+}
+template <typename T>
+struct BrickHeadPts {
+    const T* pts;
+    int shift;
+    __host__ __device__ bool operator()(long long i) const {
+#ifdef __CUDA_ARCH__
+        return i == 0 || brick_key_of(pts + 3 * i, shift) != brick_key_of(pts + 3 * (i - 1), shift);
+#else
+        return i == 0;
+#endif
+    }
+};
+
 extern "C" int64_t sp_brick_runs_temp_bytes(int64_t n) {
     if (n <= 0 || n >= (1ll << 31)) return 0;
     size_t bytes = 0;
@@ -1082,6 +1110,43 @@ extern "C" int64_t sp_brick_runs_temp_bytes(int64_t n) {
                               (int)n, head) != cudaSuccess)
         return -1;
     return (int64_t)bytes;
+}
+
+extern "C" int sp_brick_runs_points(const void* pts, int64_t n, int32_t dtype, int32_t log2_brick,
+                                    int64_t* brick_start, int32_t* n_bricks, void* temp, int64_t temp_bytes,
+                                    void* stream) {
+    if (n < 0 || n >= (1ll << 31)) return fail(SP_ERR_INVALID, "brick runs: n out of range");
+    if (log2_brick < 0 || log2_brick > 20) return fail(SP_ERR_INVALID, "log2_brick out of range");
+    if (dtype != SP_F32 && dtype != SP_F64) return fail(SP_ERR_INVALID, "unknown dtype");
+    if ((n > 0 && !pts) || !brick_start || !n_bricks) return fail(SP_ERR_INVALID, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        SP_CUDA(cudaMemsetAsync(n_bricks, 0, sizeof(int32_t), st));
+        SP_CUDA(cudaMemsetAsync(brick_start, 0, sizeof(int64_t), st));
+        return SP_OK;
+    }
+    thrust::counting_iterator<long long> idx(0);
+    size_t bytes = 0;
+    cudaError_t e;
+    auto run = [&](void* tmp, size_t& b) {
+        return dtype == SP_F32
+                   ? cub::DeviceSelect::If(tmp, b, idx, brick_start, n_bricks, (int)n,
+                                           BrickHeadPts<float>{(const float*)pts, 3 * log2_brick}, st)
+                   : cub::DeviceSelect::If(tmp, b, idx, brick_start, n_bricks, (int)n,
+                                           BrickHeadPts<double>{(const double*)pts, 3 * log2_brick}, st);
+    };
+    SP_CUDA(run(nullptr, bytes));
+    void* tmp = temp;
+    if (!tmp || (size_t)temp_bytes < bytes) {
+        tmp = nullptr;
+        SP_CUDA(cudaMallocAsync(&tmp, bytes, st));
+    }
+    e = run(tmp, bytes);
+    if (tmp != temp) cudaFreeAsync(tmp, st);
+    if (e != cudaSuccess) return fail(SP_ERR_CUDA, "brick runs (points): %s", cudaGetErrorString(e));
+    brick_runs_tail<<<1, 1, 0, st>>>(n, n_bricks, brick_start);
+    SP_CUDA(cudaGetLastError());
+    return SP_OK;
 }
 
 extern "C" int sp_brick_runs(const uint64_t* keys, int64_t n, int32_t log2_brick, int64_t* brick_start,

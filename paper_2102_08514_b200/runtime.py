@@ -947,6 +947,17 @@ def prepare_points_async(pts: torch.Tensor, log2_brick: int, *, presorted: bool 
     n = pts.shape[0]
     dtype = _native.SP_F32 if pts.dtype == torch.float32 else _native.SP_F64
     with torch.cuda.stream(st):
+        if presorted and n:
+            # brick runs straight from the points (no 8-byte key per point written and re-read)
+            start = torch.empty(n + 1, dtype=torch.int64, device=pts.device)
+            count = torch.empty(1, dtype=torch.int32, device=pts.device)
+            need = int(lib.sp_brick_runs_temp_bytes(n))
+            if scratch is None or scratch.numel() < need:
+                scratch = torch.empty(max(need, 1), dtype=torch.uint8, device=pts.device)
+            _native.check(lib.sp_brick_runs_points(pts.data_ptr(), n, dtype, int(log2_brick), start.data_ptr(),
+                                                   count.data_ptr(), scratch.data_ptr(), scratch.numel(),
+                                                   st.cuda_stream))
+            return PointBatch(pts, start, log2_brick, None, n_bricks_dev=count)
         keys = torch.empty(n, dtype=torch.int64, device=pts.device)
         _native.check(lib.sp_morton_keys(pts.data_ptr(), n, dtype, keys.data_ptr(), st.cuda_stream))
         perm = None
