@@ -155,7 +155,8 @@ int64_t sp_brick_runs_temp_bytes(int64_t n);
 /* sp_brick_runs_points: the same brick runs computed straight from Morton-ordered points
  * (dtype SP_F32 / SP_F64): a point's brick is the Morton code of its clamped unit cell shifted
  * by 3*log2_brick — identical runs to sp_morton_keys + sp_brick_runs, without the key array.
- * temp: sp_brick_runs_temp_bytes(n) bytes (NULL: stream-ordered allocation). */
+ * temp: sp_brick_runs_points_temp_bytes(n) bytes (NULL: stream-ordered allocation). */
+int64_t sp_brick_runs_points_temp_bytes(int64_t n);
 int sp_brick_runs_points(const void* pts, int64_t n, int32_t dtype, int32_t log2_brick, int64_t* brick_start,
                          int32_t* n_bricks, void* temp, int64_t temp_bytes, void* stream);
 int sp_eval_bricks_dev(const sp_plan* plan, const sp_grid_desc* grid, const void* pts, int64_t n, int32_t dtype,

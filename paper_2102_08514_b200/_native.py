@@ -180,6 +180,7 @@ EXPORTS = {
          ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
          ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
     ),
+    "sp_brick_runs_points_temp_bytes": (ctypes.c_int64, [ctypes.c_int64]),
     "sp_brick_runs_points": (
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,

@@ -12,6 +12,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <cub/device/device_scan.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
@@ -1073,28 +1074,25 @@ struct BrickHead {
 
 __global__ void brick_runs_tail(long long n, const int32_t* count, int64_t* brick_start) { brick_start[*count] = n; }
 
-// Brick heads straight from Morton-ordered points (sp_brick_runs_points): the brick key of
-// a point is the 64-bit Morton key of its clamped, biased unit cell (morton_kernel) shifted by
-// 3*log2b, i.e. the Morton code of its brick; no key array is written.
-__device__ __forceinline__ uint64_t brick_key_of(const float* p, int shift) {
-    uint32_t c[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) c[a] = (uint32_t)min(max(sp::clamp_cell(p[a]) + (1 << 20), 0), (1 << 21) - 1);
-    return (spread3(c[2]) | (spread3(c[1]) << 1) | (spread3(c[0]) << 2)) >> shift;
-}
-__device__ __forceinline__ uint64_t brick_key_of(const double* p, int shift) {
-    uint32_t c[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) c[a] = (uint32_t)min(max(sp::clamp_cell(p[a]) + (1 << 20), 0), (1 << 21) - 1);
-    return (spread3(c[2]) | (spread3(c[1]) << 1) | (spread3(c[0]) << 2)) >> shift;
+// Brick heads straight from Morton-ordered points (sp_brick_runs_points): two consecutive
+// points share a brick iff their clamped, biased unit cells (morton_kernel's key inputs)
+// agree after >> log2b on every axis — the same test as comparing their Morton keys >> 3*log2b,
+// without building the keys.
+template <typename T>
+__device__ __forceinline__ uint32_t brick_coord(T v, int log2b) {
+    return (uint32_t)min(max(sp::clamp_cell(v) + (1 << 20), 0), (1 << 21) - 1) >> log2b;
 }
 template <typename T>
 struct BrickHeadPts {
     const T* pts;
-    int shift;
+    int log2b;
     __host__ __device__ bool operator()(long long i) const {
 #ifdef __CUDA_ARCH__
-        return i == 0 || brick_key_of(pts + 3 * i, shift) != brick_key_of(pts + 3 * (i - 1), shift);
+        if (i == 0) return true;
+        const T* p = pts + 3 * i;
+        return brick_coord(p[0], log2b) != brick_coord(p[-3], log2b) ||
+               brick_coord(p[1], log2b) != brick_coord(p[-2], log2b) ||
+               brick_coord(p[2], log2b) != brick_coord(p[-1], log2b);
 #else
         return i == 0;
 #endif
@@ -1112,6 +1110,86 @@ extern "C" int64_t sp_brick_runs_temp_bytes(int64_t n) {
     return (int64_t)bytes;
 }
 
+// Brick runs of Morton-ordered points in three light passes: (1) one thread per point
+// computes its brick coordinates, gets the previous point's from the neighbouring lane
+// (shuffle; lane 0 reads it), flags "first point of its brick", and a warp ballot packs 32
+// flags into a word, counted per group of 8,192 points; (2) an exclusive scan of the group
+// counts; (3) one thread per word writes the indices of its set bits at the group offset +
+// the prefix of the group's earlier words.  The points are read once (coalesced) and 1 bit
+// per point after that; CUB's select over a point-reading predicate needed 0.92 ms per 1e8.
+constexpr int kRunGroup = 8192;  // points per count group = 256 words
+template <typename T>
+__global__ void brick_head_bits_kernel(const T* __restrict__ pts, long long n, int log2b, uint32_t* __restrict__ bits,
+                                       int* __restrict__ group_count) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    uint32_t c0 = 0, c1 = 0, c2 = 0;
+    if (i < n) {
+        c0 = brick_coord(pts[3 * i], log2b);
+        c1 = brick_coord(pts[3 * i + 1], log2b);
+        c2 = brick_coord(pts[3 * i + 2], log2b);
+    }
+    uint32_t p0 = __shfl_up_sync(0xffffffffu, c0, 1), p1 = __shfl_up_sync(0xffffffffu, c1, 1),
+             p2 = __shfl_up_sync(0xffffffffu, c2, 1);
+    if (lane == 0 && i > 0 && i < n) {
+        p0 = brick_coord(pts[3 * i - 3], log2b);
+        p1 = brick_coord(pts[3 * i - 2], log2b);
+        p2 = brick_coord(pts[3 * i - 1], log2b);
+    }
+    const bool h = i < n && (i == 0 || c0 != p0 || c1 != p1 || c2 != p2);
+    const uint32_t w = __ballot_sync(0xffffffffu, h);
+    if (lane == 0) {
+        bits[i >> 5] = w;
+        if (w) atomicAdd(group_count + (i / kRunGroup), __popc(w));
+    }
+}
+
+__global__ void brick_head_write_kernel(const uint32_t* __restrict__ bits, long long nwords,
+                                        const int* __restrict__ group_off, const int* __restrict__ group_count,
+                                        int ngroups, int64_t* __restrict__ brick_start, int32_t* __restrict__ n_bricks) {
+    // one block (256 threads) per group of 256 words; thread = word
+    __shared__ int warp_sum[8];
+    const long long wd = blockIdx.x * 256ll + threadIdx.x;
+    const uint32_t w = wd < nwords ? bits[wd] : 0u;
+    const int c = __popc(w);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_sum[wid] = incl;
+    __syncthreads();
+    int before = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) before += k < wid ? warp_sum[k] : 0;
+    long long pos = (long long)group_off[blockIdx.x] + before + incl - c;
+    uint32_t m = w;
+    while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        brick_start[pos++] = wd * 32 + b;
+    }
+    if ((int)blockIdx.x == ngroups - 1 && threadIdx.x == 0) *n_bricks = group_off[blockIdx.x] + group_count[blockIdx.x];
+}
+
+namespace {
+size_t align256_(size_t v) { return (v + 255) & ~(size_t)255; }
+// scratch: bits [n/32 words] | group counts | group offsets | scan temp
+size_t brick_runs_points_bytes(int64_t n) {
+    const long long ng = (n + kRunGroup - 1) / kRunGroup;
+    size_t scan = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan, static_cast<int*>(nullptr), static_cast<int*>(nullptr), (int)ng);
+    return align256_((size_t)ng * kRunGroup / 8) + 2 * align256_((size_t)ng * 4) + scan;
+}
+}  // namespace
+
+extern "C" int64_t sp_brick_runs_points_temp_bytes(int64_t n) {
+    if (n <= 0 || n >= (1ll << 31)) return 0;
+    return (int64_t)brick_runs_points_bytes(n);
+}
+
 extern "C" int sp_brick_runs_points(const void* pts, int64_t n, int32_t dtype, int32_t log2_brick,
                                     int64_t* brick_start, int32_t* n_bricks, void* temp, int64_t temp_bytes,
                                     void* stream) {
@@ -1125,27 +1203,41 @@ extern "C" int sp_brick_runs_points(const void* pts, int64_t n, int32_t dtype, i
         SP_CUDA(cudaMemsetAsync(brick_start, 0, sizeof(int64_t), st));
         return SP_OK;
     }
-    thrust::counting_iterator<long long> idx(0);
-    size_t bytes = 0;
-    cudaError_t e;
-    auto run = [&](void* tmp, size_t& b) {
-        return dtype == SP_F32
-                   ? cub::DeviceSelect::If(tmp, b, idx, brick_start, n_bricks, (int)n,
-                                           BrickHeadPts<float>{(const float*)pts, 3 * log2_brick}, st)
-                   : cub::DeviceSelect::If(tmp, b, idx, brick_start, n_bricks, (int)n,
-                                           BrickHeadPts<double>{(const double*)pts, 3 * log2_brick}, st);
-    };
-    SP_CUDA(run(nullptr, bytes));
+    const long long ng = (n + kRunGroup - 1) / kRunGroup;
+    const long long nwords = ng * (kRunGroup / 32);
+    const size_t need = brick_runs_points_bytes(n);
     void* tmp = temp;
-    if (!tmp || (size_t)temp_bytes < bytes) {
+    if (!tmp || (size_t)temp_bytes < need) {
         tmp = nullptr;
-        SP_CUDA(cudaMallocAsync(&tmp, bytes, st));
+        SP_CUDA(cudaMallocAsync(&tmp, need, st));
     }
-    e = run(tmp, bytes);
+    unsigned char* base = static_cast<unsigned char*>(tmp);
+    const size_t bits_bytes = align256_((size_t)ng * kRunGroup / 8);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(base);
+    int* cnt = reinterpret_cast<int*>(base + bits_bytes);
+    int* off = reinterpret_cast<int*>(base + bits_bytes + align256_((size_t)ng * 4));
+    void* scan_tmp = base + bits_bytes + 2 * align256_((size_t)ng * 4);
+    size_t scan_bytes = need - (bits_bytes + 2 * align256_((size_t)ng * 4));
+    cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)ng * 4, st);
+    const unsigned nblk = (unsigned)(nwords * 32 / sp::kThreads);  // covers the padded groups
+    if (e == cudaSuccess) {
+        if (dtype == SP_F32)
+            brick_head_bits_kernel<float><<<nblk, sp::kThreads, 0, st>>>((const float*)pts, n, log2_brick, bits, cnt);
+        else
+            brick_head_bits_kernel<double><<<nblk, sp::kThreads, 0, st>>>((const double*)pts, n, log2_brick, bits, cnt);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, off, (int)ng, st);
+    if (e == cudaSuccess) {
+        brick_head_write_kernel<<<(unsigned)ng, 256, 0, st>>>(bits, nwords, off, cnt, (int)ng, brick_start, n_bricks);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        brick_runs_tail<<<1, 1, 0, st>>>(n, n_bricks, brick_start);
+        e = cudaGetLastError();
+    }
     if (tmp != temp) cudaFreeAsync(tmp, st);
     if (e != cudaSuccess) return fail(SP_ERR_CUDA, "brick runs (points): %s", cudaGetErrorString(e));
-    brick_runs_tail<<<1, 1, 0, st>>>(n, n_bricks, brick_start);
-    SP_CUDA(cudaGetLastError());
     return SP_OK;
 }
 

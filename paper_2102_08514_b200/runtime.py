@@ -951,7 +951,7 @@ def prepare_points_async(pts: torch.Tensor, log2_brick: int, *, presorted: bool 
             # brick runs straight from the points (no 8-byte key per point written and re-read)
             start = torch.empty(n + 1, dtype=torch.int64, device=pts.device)
             count = torch.empty(1, dtype=torch.int32, device=pts.device)
-            need = int(lib.sp_brick_runs_temp_bytes(n))
+            need = int(lib.sp_brick_runs_points_temp_bytes(n))
             if scratch is None or scratch.numel() < need:
                 scratch = torch.empty(max(need, 1), dtype=torch.uint8, device=pts.device)
             _native.check(lib.sp_brick_runs_points(pts.data_ptr(), n, dtype, int(log2_brick), start.data_ptr(),
