@@ -35,25 +35,20 @@ class SplineError(ValueError):
     pass
 
 
-def _solve3(rows, rhs):
-    """Exact solution of a 3x3 system, or None when singular (Cramer on Fractions)."""
-    a = [[Fraction(v) for v in r] for r in rows]
-
-    def det(m):
-        return (m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1])
-                - m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0])
-                + m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0]))
-
-    d = det(a)
-    if d == 0:
-        return None
-    out = []
-    for c in range(3):
-        m = [row[:] for row in a]
-        for r in range(3):
-            m[r][c] = Fraction(rhs[r])
-        out.append(det(m) / d)
-    return tuple(out)
+def _solve(rows, rhs):
+    """Exact solution of a square system (Gauss-Jordan on Fractions), or None if singular."""
+    n = len(rows)
+    m = [[Fraction(v) for v in r] + [Fraction(b)] for r, b in zip(rows, rhs)]
+    for c in range(n):
+        piv = next((r for r in range(c, n) if m[r][c] != 0), None)
+        if piv is None:
+            return None
+        m[c], m[piv] = m[piv], m[c]
+        for r in range(n):
+            if r != c and m[r][c] != 0:
+                f = m[r][c] / m[c][c]
+                m[r] = [a - f * b for a, b in zip(m[r], m[c])]
+    return tuple(m[i][n] / m[i][i] for i in range(n))
 
 
 @dataclass
@@ -72,13 +67,12 @@ class SplinePiece:
         return True
 
     def vertices(self) -> tuple:
-        """Vertex enumeration (3-D): feasible intersections of half-space triples."""
+        """Vertex enumeration: feasible intersections of `dim` half-space boundaries."""
         if self._vertices is None:
-            if len(self.halfspaces[0][0]) != 3:
-                raise NotImplementedError("vertex enumeration is 3-D only")
+            dim = len(self.halfspaces[0][0])
             vs = set()
-            for h in combinations(self.halfspaces, 3):
-                p = _solve3([n for n, _ in h], [o for _, o in h])
+            for h in combinations(self.halfspaces, dim):
+                p = _solve([n for n, _ in h], [o for _, o in h])
                 if p is not None and self.contains(p):
                     vs.add(p)
             if not vs:
