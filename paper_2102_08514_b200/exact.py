@@ -97,6 +97,25 @@ class Poly:
                 out[e] = out.get(e, Fraction(0)) + c1 * c2
         return Poly(self.dim, out)
 
+    def divexact(self, d: "Poly") -> "Poly":
+        """Exact quotient self / d (multivariate division in lex order); raises ValueError
+        when d does not divide self."""
+        if d.is_zero():
+            raise ZeroDivisionError("division by the zero polynomial")
+        lead_d = max(d.terms)
+        cd = d.terms[lead_d]
+        rem = Poly(self.dim, self.terms)
+        quo: Dict[Exps, Fraction] = {}
+        while not rem.is_zero():
+            lead = max(rem.terms)
+            if any(a < b for a, b in zip(lead, lead_d)):
+                raise ValueError("polynomial division is not exact")
+            e = tuple(a - b for a, b in zip(lead, lead_d))
+            c = rem.terms[lead] / cd
+            quo[e] = quo.get(e, Fraction(0)) + c
+            rem = rem - Poly(self.dim, {e: c}) * d
+        return Poly(self.dim, quo)
+
     def __eq__(self, other) -> bool:
         return isinstance(other, Poly) and self.dim == other.dim and self.terms == other.terms
 
