@@ -227,6 +227,12 @@ int sp_morton_keys32(const void* pts, int64_t n, int32_t dtype, int32_t lo0, int
 
 /* out[perm[i]] = src[i]  (float or double, by dtype) — unpermute results of a sorted batch. */
 int sp_scatter(const void* src, const int64_t* perm, int64_t n, int32_t dtype, void* out, void* stream);
+/* L2-blocked variant with an int32 permutation: one pass over (perm, src) per destination window
+ * of `window` elements (<= 0: one pass), each writing only the values landing in its window, so
+ * every output sector is written whole while L2-resident (a random 4-byte scatter costs a DRAM
+ * read-modify-write per value).  Same result as out[perm[i]] = src[i]. */
+int sp_scatter32_blocked(const void* src, const int32_t* perm, int64_t n, int32_t dtype, int64_t window, void* out,
+                         void* stream);
 /* dst[i] = pts[perm[i]] (s=3 points) — gather points into sorted order. */
 int sp_gather_points(const void* pts, const int64_t* perm, int64_t n, int32_t dtype, void* dst, void* stream);
 

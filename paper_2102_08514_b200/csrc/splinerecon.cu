@@ -1673,6 +1673,39 @@ extern "C" int sp_scatter(const void* src, const int64_t* perm, int64_t n, int32
     return SP_OK;
 }
 
+// L2-blocked scatter out[perm[i]] = src[i] (int32 perm): destination indices are processed in
+// windows of `window` elements that fit in L2, one pass over (perm, src) per window, each pass
+// writing only the values whose destination falls in its window.  Every 32-byte sector of a
+// window is then written completely while it is L2-resident, so it reaches HBM as one full
+// sector write — a direct random scatter of 4-byte values makes HBM read-modify-write a
+// sector per value (ECC granularity).  Reads (perm, src) once per window.
+template <typename T>
+__global__ void scatter_window_kernel(const T* __restrict__ src, const int32_t* __restrict__ perm, long long n,
+                                      long long lo, long long hi, T* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long d = perm[i];
+        if (d >= lo && d < hi) out[d] = src[i];
+    }
+}
+
+extern "C" int sp_scatter32_blocked(const void* src, const int32_t* perm, int64_t n, int32_t dtype, int64_t window,
+                                    void* out, void* stream) {
+    if (n <= 0) return SP_OK;
+    if (!src || !perm || !out) return fail(SP_ERR_INVALID, "null argument");
+    if (dtype != SP_F32 && dtype != SP_F64) return fail(SP_ERR_INVALID, "unknown dtype");
+    if (window <= 0) window = n;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    for (int64_t lo = 0; lo < n; lo += window) {
+        const int64_t hi = std::min<int64_t>(n, lo + window);
+        if (dtype == SP_F32)
+            scatter_window_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)src, perm, n, lo, hi, (float*)out);
+        else
+            scatter_window_kernel<double><<<grid_for(n), 256, 0, st>>>((const double*)src, perm, n, lo, hi, (double*)out);
+        SP_CUDA(cudaGetLastError());
+    }
+    return SP_OK;
+}
+
 extern "C" int sp_gather_points(const void* pts, const int64_t* perm, int64_t n, int32_t dtype, void* dst, void* stream) {
     if (n <= 0) return SP_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

@@ -481,6 +481,10 @@ class PlanInterpreter:
     # in total vs 9.24 ms for the permuted-read path, so it stays off by default
     sort_payload = os.environ.get("SP_SORT_PAYLOAD", "0") == "1"
 
+    # protocol B result scatter: destination window (elements) of the L2-blocked scatter
+    # (sp_scatter32_blocked); 0 = the brick kernel scatters directly (sp_eval_bricks_indirect)
+    scatter_window = int(os.environ.get("SP_SCATTER_WINDOW", str(1 << 24)))
+
     # protocol-B workspaces kept (one per thread x stream x batch shape, most recent first out)
     sort_ws_keep = 4
 
@@ -722,6 +726,18 @@ class PlanInterpreter:
                                                            res.data_ptr(), None if err is None else err.data_ptr(),
                                                            st.cuda_stream))
                 return perm
+            if not gather and self.scatter_window > 0 and n > self.scatter_window:
+                # values in brick order, then an L2-blocked scatter to the caller's order (one
+                # pass per L2-sized destination window: tools/scatter_probe.py, 1e8 values 3.8 ->
+                # 2.2 ms) instead of the kernel's random 4-byte writes
+                vals = torch.empty_like(res)
+                _native.check(lib.sp_eval_bricks_unordered(h, ctypes.byref(gdesc), p.data_ptr(), n, dtype,
+                                                           start.data_ptr(), count.data_ptr(), n, b, perm.data_ptr(),
+                                                           vals.data_ptr(), None if err is None else err.data_ptr(),
+                                                           st.cuda_stream))
+                _native.check(lib.sp_scatter32_blocked(vals.data_ptr(), perm.data_ptr(), n, dtype, self.scatter_window,
+                                                       res.data_ptr(), st.cuda_stream))
+                return None
             fn = lib.sp_eval_bricks_perm32 if gather else lib.sp_eval_bricks_indirect
             _native.check(fn(h, ctypes.byref(gdesc), (sp_ if gather else p).data_ptr(), n, dtype, start.data_ptr(),
                              count.data_ptr(), n, b, perm.data_ptr(), res.data_ptr(),
