@@ -475,6 +475,7 @@ def _signature_methods(plan: EvaluationPlan) -> str:
     static constexpr int kSigCount = {len(set(kernel_programs(plan))) ** plan.M};
     static constexpr int kProgCount = {len(set(kernel_programs(plan)))};
     static constexpr int kMC = kM;
+    static constexpr int kSigSeg = {_sig_segment(plan)};  // points per signature-sort segment
 """ + _word_class(plan) + """    template <class Ctx>
     __device__ __forceinline__ static unsigned classify_word(const T x[3], const Ctx& ctx) {
         const int* sigma = sigma_of(ctx);
@@ -653,6 +654,33 @@ __device__ __forceinline__ int cube_code(const float u[3], const int X[3]) {{
 }}
 """
     return src, cube_table(plan, tests)
+
+
+def _smem_tables(plan: EvaluationPlan) -> int:
+    """Bytes of plan tables + per-tile address records a brick CTA keeps in shared memory."""
+    tests = cube_tests(plan)
+    cube = 0
+    if tests is not None and plan.M > 1 and _word_bits(plan) > 0:
+        n = plan.diag[0] ** 3
+        for _, t in tests:
+            n *= len(t) + 1
+        cube = ((n * 4 + 15) // 16) * 16 if n <= CUBE_MAX_CODES else 0
+    return plan.N * 16 + cube + plan.M * plan.N * 16
+
+
+def _sig_segment(plan: EvaluationPlan) -> int:
+    """Signature-sort segment: 1024 points, 512 when the plan's tables are large (BCC Voronoi:
+    N = 320, 20 KB cube table) so that three CTAs fit an SM (static arrays ~20 B per point)."""
+    return 512 if _smem_tables(plan) > 24 * 1024 else 1024
+
+
+def tile_budget_kb(plan: EvaluationPlan) -> int:
+    """Shared-memory tile budget (KB) of the brick kernels: 40, lowered for plans with large
+    tables so that tables + records + signature arrays + tile fit three CTAs per SM
+    (228 KB / 3 - 1 KB reserved per CTA)."""
+    static = _sig_segment(plan) * 20 + 2048 if plan.K > 1 else 2048
+    room = (75 * 1024 - _smem_tables(plan) - static) // 1024
+    return 40 if room >= 36 else max(20, room)  # measured: BCC Voronoi 27 KB + 512-point segments 22.4 -> 25.2
 
 
 def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple:
@@ -1019,6 +1047,7 @@ extern const sp::GenEntry kGen_{ident} = {{
     {"sp::gen_" + ident + "::kCubeTab" if cube_tab is not None else "nullptr"},
     {len(cube_tab) if cube_tab is not None else 0},
     sp::gen_{ident}::kSmemTableBytes,
+    {tile_budget_kb(plan)},
 }};
 """
     return src, {"ident": ident, "flops_per_coset": kflops, "words": len(words), "affine": aff is not None}

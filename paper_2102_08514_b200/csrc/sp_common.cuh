@@ -728,7 +728,7 @@ template <typename T, class Ev, typename V>
 __device__ __forceinline__ void eval_brick_sig(const EvalArgs<T>& a, EvalCtx<T, Ev>& ctx, long long p0, long long p1,
                                                bool staged, int c0, int c1, int c2, int B, const T* tile,
                                                const V* vtile, const unsigned char* tables) {
-    constexpr int kSeg = 1024;
+    constexpr int kSeg = Ev::kSigSeg;
     constexpr int kBuckets = Ev::kSigCount + 1;  // last bucket: per-point path
     static_assert(kBuckets <= 65535, "signature count");
     constexpr int kPer = kSeg / kThreads;
@@ -748,12 +748,16 @@ __device__ __forceinline__ void eval_brick_sig(const EvalArgs<T>& a, EvalCtx<T, 
         const T* src = a.pts + 3 * seg;
         constexpr int kVecE = 16 / (int)sizeof(T);
         if (!a.in_index32 && n == kSeg && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            constexpr int kNV = 3 * kSeg / kVecE / kThreads;
+            constexpr int kVecs = 3 * kSeg / kVecE;  // 16-byte vectors in the segment
+            constexpr int kNV = (kVecs + kThreads - 1) / kThreads;
+            static_assert(3 * kSeg % kVecE == 0, "segment size");
             int4 v[kNV];
 #pragma unroll
-            for (int q = 0; q < kNV; ++q) v[q] = __ldg(reinterpret_cast<const int4*>(src) + tid + q * kThreads);
+            for (int q = 0; q < kNV; ++q)
+                if (tid + q * kThreads < kVecs) v[q] = __ldg(reinterpret_cast<const int4*>(src) + tid + q * kThreads);
 #pragma unroll
-            for (int q = 0; q < kNV; ++q) reinterpret_cast<int4*>(s_pts)[tid + q * kThreads] = v[q];
+            for (int q = 0; q < kNV; ++q)
+                if (tid + q * kThreads < kVecs) reinterpret_cast<int4*>(s_pts)[tid + q * kThreads] = v[q];
         } else {
             T v[3 * kPer];
 #pragma unroll

@@ -152,6 +152,7 @@ struct GenEntry {
     const uint32_t* cube_tab;  // unit-cube class-word table (codegen.cube_table), or null
     int cube_len;
     int smem_table_bytes;      // leading bytes of the plan tables staged into shared memory
+    int tile_kb;               // shared-memory tile budget of the brick kernels (codegen.tile_budget_kb)
 };
 
 }  // namespace sp

@@ -463,7 +463,10 @@ namespace {
 
 // Tuning knobs (environment, read per call): SP_TILE_KB (shared-memory tile budget),
 // SP_PPT (points per thread per chunk, 0 = density-based).
-int tile_bytes() { return env_int("SP_TILE_KB", 40) * 1024; }
+// shared-memory tile budget: SP_TILE_KB, else the generated plan's (codegen.tile_budget_kb), else 40 KB
+int tile_bytes(const sp_plan* p = nullptr) {
+    return env_int("SP_TILE_KB", (p && p->gen && p->gen->tile_kb > 0) ? p->gen->tile_kb : 40) * 1024;
+}
 
 unsigned long long* g_stats = nullptr;  // device [4] when sp_debug_stats(1) is on
 
@@ -522,12 +525,12 @@ int build_args(const sp_plan* p, const sp_grid_desc* g, const void* pts, int64_t
         // scalar staging tile + padded row-vector tile (~1.5x the scalar capacity)
         // SP_VPAD=1: bank-conflict-padded row-vector tile (tuning knob; dense measured faster)
         const bool pad = env_int("SP_VPAD", 0) != 0;
-        a.tile_cap = tile_bytes() / (int)(sizeof(T) * (1 + (pad ? vec * 3 / 2 : vec)));
+        a.tile_cap = tile_bytes(p) / (int)(sizeof(T) * (1 + (pad ? vec * 3 / 2 : vec)));
         a.vec_cap = pad ? a.tile_cap * 3 / 2 : a.tile_cap;
     } else {
         // the closed-form BCC linear plan uses 32^3 fp32 bricks (brick_log2_typed): 80 KB tile
         // for the generic drivers (protocol B) so that those bricks still stage
-        a.tile_cap = (p->bcc_tet ? std::max(tile_bytes(), 80 * 1024) : tile_bytes()) / (int)sizeof(T);
+        a.tile_cap = (p->bcc_tet ? std::max(tile_bytes(p), 80 * 1024) : tile_bytes(p)) / (int)sizeof(T);
         a.vec_cap = 0;
     }
     a.stats = g_stats;
@@ -620,7 +623,7 @@ int brick_log2_typed(const sp_plan* p) {
     // barriers and staging amortised over ~8x more points than 16^3); SP_BCC_TET_L2B overrides
     if (p->bcc_tet && env_int("SP_BCC_TET_BRICK", 1) != 0) return env_int("SP_BCC_TET_L2B", sizeof(T) == 4 ? 5 : 4);
     const int vec = (p->kind == SP_KIND_TENSOR_BSPLINE && sizeof(T) == 4) ? (p->tp_degree == 1 ? 2 : 4) : 0;
-    const long long cap = tile_bytes() / (long long)(sizeof(T) * (1 + vec * 3 / 2));
+    const long long cap = tile_bytes(p) / (long long)(sizeof(T) * (1 + vec * 3 / 2));
     bool shifted = false;
     for (int k = 0; k < p->M; ++k)
         for (int i = 0; i < 3; ++i) shifted |= p->shifts[k][i] != 0;
