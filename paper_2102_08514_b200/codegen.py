@@ -501,6 +501,20 @@ def _signature_methods(plan: EvaluationPlan) -> str:
         }
         return w;
     }
+    // class word and signature together: fast-domain points read both from the cube tables
+    template <class Ctx>
+    __device__ __forceinline__ static int classify_key(const T x[3], const Ctx& ctx, unsigned& word) {
+        if constexpr (kCube && kCubeSig) {
+            float frac[3] = {0.f, 0.f, 0.f};
+            if (fast_frame(x, frac)) {
+                const int code = cube_code(frac, ctx.X);
+                word = reinterpret_cast<const unsigned*>(ctx.tables + kCubeOff)[code];
+                return (int)ctx.tables[kCubeSigOff + code];
+            }
+        }
+        word = classify_word(x, ctx);
+        return signature(word, ctx.tables);
+    }
     __device__ __forceinline__ static int signature(unsigned word, const unsigned char* tables) {
         const uint4* cls_tab = reinterpret_cast<const uint4*>(tables + kClsOff);
         int sig = 0;
@@ -664,7 +678,8 @@ def _smem_tables(plan: EvaluationPlan) -> int:
         n = plan.diag[0] ** 3
         for _, t in tests:
             n *= len(t) + 1
-        cube = ((n * 4 + 15) // 16) * 16 if n <= CUBE_MAX_CODES else 0
+        sig = n if plan.K > 1 else 0  # signature byte per code
+        cube = ((n * 4 + sig + 15) // 16) * 16 if n <= CUBE_MAX_CODES else 0
     return plan.N * 16 + cube + plan.M * plan.N * 16
 
 
@@ -731,10 +746,31 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
     if cube_tab is None:
         cube_src = '''
 constexpr bool kCube = false;
+constexpr bool kCubeSig = false;
 constexpr int kCubeCodes = 0;
 __device__ __forceinline__ int cube_code(const float u[3], const int X[3]) { return 0; }
 '''
     else:
+        # K > 1: each code's point signature (program id per coset, base P, as
+        # Eval::signature computes it from the word) in a byte table after the class words,
+        # so the signature-grouped driver's pass 1 is two shared loads per point
+        ncodes = len(cube_tab)
+        sig_codes = []
+        progs = kernel_programs(plan)
+        P = len(set(progs))
+        bits = _word_bits(plan)
+        if plan.K > 1 and P ** plan.M <= 255:
+            for w in cube_tab:
+                sig = 0
+                for k in range(plan.M):
+                    c = (w >> (bits * k)) & ((1 << bits) - 1)
+                    c = 0 if c == (1 << bits) - 1 else c  # sentinel -> class 0 (max(raw, 0))
+                    sig = sig * P + progs[plan.classes[c].kernel]
+                sig_codes.append(sig)
+            sig_codes += [0] * (-len(sig_codes) % 4)
+            cube_tab = cube_tab + [sig_codes[i] | sig_codes[i + 1] << 8 | sig_codes[i + 2] << 16 | sig_codes[i + 3] << 24
+                                   for i in range(0, len(sig_codes), 4)]
+        cube_src += f"constexpr bool kCubeSig = {'true' if sig_codes else 'false'};\n"
         cube_src += "static const uint32_t kCubeTab[" + str(len(cube_tab)) + "] = {" + ", ".join(
             f"{w:#x}u" for w in cube_tab) + "};\n"
     if plan.K == 1:
@@ -934,7 +970,8 @@ __device__ __forceinline__ int shift_i(int k, int i) {{
 // from global memory); without it all three are.
 constexpr int kClsOff = 0;
 constexpr int kCubeOff = kN * 16;
-constexpr int kSigOff = kCubeOff + ((kCubeCodes * 4 + 15) & ~15);
+constexpr int kCubeSigOff = kCubeOff + kCubeCodes * 4;  // byte per code (kCubeSig)
+constexpr int kSigOff = kCubeOff + (((kCubeCodes * 4) + (kCubeSig ? (kCubeCodes + 3) / 4 * 4 : 0) + 15) & ~15);
 constexpr int kSmemTableBytes = kCube ? kSigOff : kSigOff + kSigmaBytes;
 template <class Ctx>
 __device__ __forceinline__ const int* sigma_of(const Ctx& ctx) {{

@@ -781,10 +781,7 @@ __device__ __forceinline__ void eval_brick_sig(const EvalArgs<T>& a, EvalCtx<T, 
                                 (unsigned)(ctx.X[2] - c2) < (unsigned)B;
             int key = kBuckets - 1;
             unsigned w = 0u;
-            if (fin && staged && inside) {
-                w = Ev::classify_word(x, ctx);
-                key = Ev::signature(w, tables);
-            }
+            if (fin && staged && inside) key = Ev::classify_key(x, ctx, w);
             s_word[i] = w;
             s_key[i] = (unsigned short)key;
             atomicAdd(&s_hist[key], 1);
