@@ -31,6 +31,7 @@ from .plan import (  # noqa: F401
 )
 from .corpus import build_plan, load_plan, DIRECTION_SETS, CORPUS, REFERENCE_LOOKUPS  # noqa: F401
 from .minilang import KernelProgram, build_program, emit_kernel, execute, parse_kernel  # noqa: F401
+from .boxplan import box_spline_plan, compile_pp_plan, extract_pp_form  # noqa: F401
 
 __version__ = "0.1.0"
 
