@@ -28,6 +28,7 @@ same checksum — which tests/test_tpplan.py checks against reference-compiled p
 from __future__ import annotations
 
 from fractions import Fraction
+from math import gcd
 from itertools import combinations, permutations, product
 from typing import Sequence
 
@@ -68,48 +69,77 @@ def _rank1_group(corners: list, axes: tuple, weight_of: dict):
 
 def _min_exact_cover(n: int, rows: list) -> list:
     """Smallest exact cover of {0..n-1} by `rows` (sets of indices); among the smallest, the
-    one whose sorted list of sorted index tuples is least.  Depth-first over the element
-    with the fewest usable rows, pruned by a max-row-size bound; rows as int bitmasks."""
+    one whose sorted list of sorted index tuples is least — the cover the reference's
+    exhaustive search returns (plancompile.py:233-268), found without enumerating every
+    minimum cover:
+
+    * the minimum cardinality k comes from a feasibility search ("coverable with <= m rows?")
+      pruned by the fractional bound sum_e 1/maxrow(e) (each chosen row contributes <= 1),
+      with failed (set, m) states memoised;
+    * the least key is then built greedily: in any exact cover the row holding the smallest
+      uncovered element sorts first among the rows still to choose, so taking, for that
+      element, the least row tuple that still admits a cover of the remaining budget is
+      lexicographically optimal.
+    """
     masks = [sum(1 << e for e in row) for row in rows]
+    sizes = [len(r) for r in rows]
     by_elem = [[] for _ in range(n)]
     for i, row in enumerate(rows):
         for e in row:
             by_elem[e].append(i)
-    biggest = max(len(r) for r in rows)
-    best = {"rows": None, "key": None}
+    unit = 1
+    for sz in set(sizes):
+        unit = unit * sz // gcd(unit, sz)
+    wt = [unit // max((sizes[i] for i in by_elem[e]), default=1) for e in range(n)]
+    fail: dict = {}
 
-    def key_of(chosen):
-        return tuple(sorted(tuple(sorted(rows[i])) for i in chosen))
-
-    def search(left: int, nleft: int, chosen: list):
-        if not left:
-            k = key_of(chosen)
-            b = best["rows"]
-            if b is None or len(chosen) < len(b) or (len(chosen) == len(b) and k < best["key"]):
-                best["rows"], best["key"] = list(chosen), k
-            return
-        if best["rows"] is not None and len(chosen) + -(-nleft // biggest) > len(best["rows"]):
-            return
-        e_best, use_best = -1, None
-        m = left
+    def bound(left: int) -> int:
+        tot, m = 0, left
         while m:
             low = m & -m
-            e = low.bit_length() - 1
+            tot += wt[low.bit_length() - 1]
             m ^= low
-            use = [i for i in by_elem[e] if masks[i] & ~left == 0]
+        return -(-tot // unit)
+
+    def usable(e: int, left: int) -> list:
+        return [i for i in by_elem[e] if masks[i] & ~left == 0]
+
+    def feasible(left: int, m: int) -> bool:
+        if not left:
+            return True
+        if m <= 0 or bound(left) > m or fail.get(left, -1) >= m:
+            return False
+        e_best, use_best, mm = -1, None, left
+        while mm:
+            low = mm & -mm
+            e = low.bit_length() - 1
+            mm ^= low
+            use = usable(e, left)
             if use_best is None or len(use) < len(use_best):
                 e_best, use_best = e, use
                 if len(use) <= 1:
                     break
-        for i in use_best:
-            chosen.append(i)
-            search(left & ~masks[i], nleft - len(rows[i]), chosen)
-            chosen.pop()
+        for i in sorted(use_best, key=lambda i: -sizes[i]):
+            if feasible(left & ~masks[i], m - 1):
+                return True
+        fail[left] = max(fail.get(left, -1), m)
+        return False
 
-    search((1 << n) - 1, n, [])
-    if best["rows"] is None:
-        raise PlanError("no exact cover of the kernel sites")
-    return best["rows"]
+    full = (1 << n) - 1
+    k = bound(full)
+    while not feasible(full, k):
+        k += 1
+    chosen, left = [], full
+    while left:
+        e = (left & -left).bit_length() - 1
+        for i in sorted(usable(e, left), key=lambda i: tuple(sorted(rows[i]))):
+            if feasible(left & ~masks[i], k - len(chosen) - 1):
+                chosen.append(i)
+                left &= ~masks[i]
+                break
+        else:  # pragma: no cover - feasible(full, k) guarantees a continuation
+            raise PlanError("no exact cover of the kernel sites")
+    return chosen
 
 
 def _cover_and_sort(sites: list, cands: list) -> tuple:

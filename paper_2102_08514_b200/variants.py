@@ -18,9 +18,8 @@ from __future__ import annotations
 from dataclasses import replace
 
 from .exact import Poly
-from .plan import EvaluationPlan, PlanError, PlanKernel, PlanOptions
+from .plan import EvaluationPlan, PlanKernel, PlanOptions
 
-MAX_REGROUP_SITES = 32
 from .tpplan import group_fetches, order_fetches
 
 
@@ -44,11 +43,6 @@ def group_site_weights(group) -> list:
 def plan_variant(plan: EvaluationPlan, options: PlanOptions) -> EvaluationPlan:
     """The plan the reference compiler would emit for `options` (same analysis)."""
     grouped = options.grouped and plan.basis_nonnegative  # plancompile.py:350-351
-    if grouped and not plan.options.grouped and max(k.nearest_count for k in plan.kernels) > MAX_REGROUP_SITES:
-        # the minimum-exact-cover search grows exponentially with the site count (ZP3: 53
-        # sites per kernel; the reference's own grouped compile ran for hours here too)
-        raise PlanError(f"grouping {max(k.nearest_count for k in plan.kernels)} sites per kernel is an exponential "
-                        f"search; use PlanOptions(grouped=False) or a grouped plan compiled by the reference")
     kernels = []
     for kern in plan.kernels:
         sw = sorted(sw for grp in kern.groups for sw in group_site_weights(grp))

@@ -70,3 +70,60 @@ def test_tensor_plans_evaluate_like_the_oracle(degree, cuda):
     ones = CoefficientGrid(cos, [torch.ones(20, 20, 20, dtype=torch.float64)], [(0, 0, 0)], "clamp", device=cuda)
     pou = interp.eval_batch(ones, torch.from_numpy(pts).to(cuda))
     assert float((pou - 1).abs().max()) < 1e-12
+
+
+def _exhaustive_cover(n, rows):
+    """The reference's search (plancompile.py:233-268) restated as the checker: every exact
+    cover, smallest cardinality, then least sorted tuple of sorted rows."""
+    best = None
+    by_elem = {e: [i for i, r in enumerate(rows) if e in r] for e in range(n)}
+
+    def dfs(left, chosen):
+        nonlocal best
+        if not left:
+            key = (len(chosen), tuple(sorted(tuple(sorted(rows[i])) for i in chosen)))
+            if best is None or key < best[0]:
+                best = (key, list(chosen))
+            return
+        e = min(left, key=lambda e: (sum(1 for i in by_elem[e] if rows[i] <= left), e))
+        for i in by_elem[e]:
+            if rows[i] <= left:
+                chosen.append(i)
+                dfs(left - rows[i], chosen)
+                chosen.pop()
+
+    dfs(frozenset(range(n)), [])
+    return best[1]
+
+
+def test_min_exact_cover_matches_exhaustive_search():
+    """The fast cover (fractional bound + greedy least key) returns the reference's cover on
+    random instances with many tied minimum covers."""
+    import random
+
+    from paper_2102_08514_b200.tpplan import _min_exact_cover
+
+    rng = random.Random(5)
+    for _ in range(300):
+        n = rng.randint(1, 12)
+        rows = {frozenset([e]) for e in range(n)}
+        for _ in range(rng.randint(0, 3 * n)):
+            k = rng.choice([2, 2, 4, 4, 8])
+            if k <= n:
+                rows.add(frozenset(rng.sample(range(n), k)))
+        rows = sorted(rows, key=lambda r: (len(r), sorted(r)))
+        rng.shuffle(rows)
+        got = _min_exact_cover(n, rows)
+        want = _exhaustive_cover(n, rows)
+        key = lambda c: tuple(sorted(tuple(sorted(rows[i])) for i in c))  # noqa: E731
+        assert len(got) == len(want) and key(got) == key(want)
+
+
+def test_grouped_zp3_resolves():
+    """build_plan('cc_zp3') with default options: 53 sites per kernel grouped exactly."""
+    plan = corpus.build_plan("cc_zp3")
+    assert plan.options.grouped
+    for k in plan.kernels:
+        sites = sorted(s for g in k.groups for s in g.sites)
+        assert len(sites) == len(set(sites)) == 53
+    assert plan.grouped_fetch_counts()[0] < plan.nearest_fetch_counts()[0]
