@@ -353,8 +353,11 @@ class _BoxRecurrence:
 
     def __init__(self, cols):
         self.dim = len(cols[0])
-        self.root = tuple(sorted(tuple(Fraction(v) for v in c) for c in cols))
+        if any(Fraction(v).denominator != 1 for c in cols for v in c):
+            raise PlanError("box-spline direction columns must be integer vectors")
+        self.root = tuple(sorted(tuple(int(v) for v in c) for c in cols))
         self.info = {}
+        self.memo = {}
 
     def _info(self, key):
         if key not in self.info:
@@ -369,26 +372,53 @@ class _BoxRecurrence:
                 self.info[key] = None
             else:
                 B = [[basis[j][i] for j in range(self.dim)] for i in range(self.dim)]  # columns
-                self.info[key] = (tuple(idx), _inverse(B), abs(_det(B)))
+                det = _det(B)
+                binv = _inverse(B)
+                adj = tuple(tuple(int(v * det) for v in row) for row in binv)  # integer adjugate
+                # support facets of M_key: a node whose point lies strictly outside is zero
+                # (x0 is off every knot plane, and the facets of every sub-zonotope shifted by
+                # the removed columns are knot planes, so "strictly" loses nothing)
+                big = len(key) > self.dim
+                hs = tuple((n, int(o)) for n, o in _zonotope(list(key)).hs) if big else ()
+                planes = tuple((n, int(o)) for n, o in _knot_planes(list(key))) if big else ()
+                self.info[key] = (tuple(idx), binv, abs(det), hs, planes, adj, int(det))
         return self.info[key]
 
     def piece(self, x0) -> Poly:
-        memo = {}
-        dim = self.dim
+        """Polynomial (absolute coordinates) of the piece containing the off-plane point x0.
 
-        def rec(cols, shift):
-            key = (cols, shift)
+        Every node M_cols(x - shift) of the recurrence is one polynomial on each cell of its
+        own knot-plane arrangement, so node values are memoised across calls by (cols, shift,
+        side of y0 = x0 - shift on each knot plane of cols) and carried in absolute x.  Side
+        tests run on integers: y0 = Y / den with den the common denominator of x0."""
+        dim = self.dim
+        memo = self.memo
+        den = 1
+        for v in x0:
+            den = den * Fraction(v).denominator // gcd(den, Fraction(v).denominator)
+        X = tuple(int(Fraction(v) * den) for v in x0)
+
+        def idot(n, y):
+            return sum(a * b for a, b in zip(n, y))
+
+        def rec(cols, shift, Y):
+            inf = self._info(cols)
+            for n, o in inf[3]:
+                if idot(n, Y) > o * den:
+                    return Poly(dim)
+            if len(cols) == dim:
+                D = inf[6] * den
+                for row in inf[5]:
+                    t = idot(row, Y)
+                    if not (0 <= t < D if D > 0 else D < t <= 0):
+                        return Poly(dim)
+                return Poly.const(dim, 1 / inf[2])
+            key = (cols, shift, tuple(idot(n, Y) > o * den for n, o in inf[4]))
             if key in memo:
                 return memo[key]
-            inf = self._info(cols)
-            y0 = tuple(a - b for a, b in zip(x0, shift))
-            binv, det = inf[1], inf[2]
-            t0 = [_dot(row, y0) for row in binv]
-            if len(cols) == dim:
-                val = Poly.const(dim, 1 / det) if all(F0 <= t < F1 for t in t0) else Poly(dim)
-                memo[key] = val
-                return val
-            tpoly = [_affine_poly(dim, binv[r], t0[r]) for r in range(dim)]
+            binv = inf[1]
+            # t(x) = binv (x - shift): affine in the absolute coordinates
+            tpoly = [_affine_poly(dim, binv[r], -_dot(binv[r], shift)) for r in range(dim)]
             tau, mult = {}, {}
             for c in cols:
                 mult[c] = mult.get(c, 0) + 1
@@ -405,20 +435,18 @@ class _BoxRecurrence:
                 c1 = tau[c]
                 c2 = Poly.const(dim, m) - c1
                 if not c1.is_zero():
-                    ch = rec(sub, shift)
+                    ch = rec(sub, shift, Y)
                     if not ch.is_zero():
                         acc = acc + c1 * ch
                 if not c2.is_zero():
-                    ch = rec(sub, tuple(a + b for a, b in zip(shift, c)))
+                    ch = rec(sub, tuple(a + b for a, b in zip(shift, c)), tuple(a - den * b for a, b in zip(Y, c)))
                     if not ch.is_zero():
                         acc = acc + c2 * ch
             val = Poly(dim, {e: v / (len(cols) - dim) for e, v in acc.terms.items()})
             memo[key] = val
             return val
 
-        p = rec(self.root, tuple([F0] * dim))
-        ident = [[F1 if i == j else F0 for j in range(dim)] for i in range(dim)]
-        return compose_affine(p, ident, [-v for v in x0])  # delta = x - x0
+        return rec(self.root, tuple([0] * dim), X)
 
 
 class BoxPP:

@@ -375,18 +375,21 @@ def test_sync_free_brick_runs_match(name, presorted, cuda):
 
 @pytest.mark.parametrize("name,dtype", [("cc_tricubic", torch.float32), ("bcc_quintic_rd", torch.float32),
                                         ("fcc_cubic", torch.float64), ("bcc_linear_rd", torch.float32)])
-@pytest.mark.parametrize("gather", [False, True])
-def test_sorted32_protocol_b_matches_given_order(name, dtype, gather, cuda):
+@pytest.mark.parametrize("gather,window", [(False, 0), (True, 0), (False, 1 << 12), (False, 1000)])
+def test_sorted32_protocol_b_matches_given_order(name, dtype, gather, window, cuda):
     """order='sort' (sp_sort_points: 30-bit keys in the grid frame, CUB pair sort, device
     brick runs; then either a gathered copy + sp_eval_bricks_perm32, or
     sp_eval_bricks_indirect reading the caller's points through the permutation; both scatter
     back) is bit-identical to the chunk kernel on shuffled points, including points outside
-    the grid (clamped keys) and NaN."""
+    the grid (clamped keys) and NaN.  window > 0: values in brick order, then the L2-blocked
+    result scatter (sp_scatter32_blocked, one pass per destination window)."""
     from paper_2102_08514_b200.runtime import _sort_frame
 
     g, plan, grid = _setup(name, "mirror", dtype, cuda)
     interp = PlanInterpreter(plan)
     interp.sort_gather = gather
+    if window:
+        interp.scatter_window = window
     rng = np.random.default_rng(17)
     hi = max(a.shape[0] for a in grid.arrays) * plan.diag[0]
     pts = rng.uniform(-3, hi + 3, size=(200_000, 3))
