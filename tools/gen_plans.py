@@ -25,7 +25,7 @@ EXTRA = {
     "cc_tricubic": (E3 * 4, "CC3"),
     "cc_triquadratic": (E3 * 3, "CC3"),
     "cc_zp3": (E3 + DIAG, "CC3"),
-    "bcc_quartic": (DIAG + E3 + E3, "BCC"),
+    "bcc_quartic": (DIAG + [(2, 0, 0), (0, 2, 0), (0, 0, 2)], "BCC"),
 }
 # Voronoi splines: PP data built by tools/voronoi_pp.py from the reference's exact tools
 # and imported through the reference's own import path (spline.py:667-713).

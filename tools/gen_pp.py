@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "paper_2102_08514_b200", "pp")
 E3 = [(1, 0, 0), (0, 1, 0), (0, 0, 1)]
 DIAG = [(1, 1, 1), (-1, 1, 1), (1, -1, 1), (1, 1, -1)]
-EXTRA = {"cc_tricubic": E3 * 4, "cc_zp3": E3 + DIAG, "bcc_quartic": DIAG + E3 + E3}
+EXTRA = {"cc_tricubic": E3 * 4, "cc_zp3": E3 + DIAG, "bcc_quartic": DIAG + [(2, 0, 0), (0, 2, 0), (0, 0, 2)]}
 
 
 def main(names):
