@@ -233,6 +233,14 @@ int sp_scatter(const void* src, const int64_t* perm, int64_t n, int32_t dtype, v
  * read-modify-write per value).  Same result as out[perm[i]] = src[i]. */
 int sp_scatter32_blocked(const void* src, const int32_t* perm, int64_t n, int32_t dtype, int64_t window, void* out,
                          void* stream);
+/* out[perm[i]] = src[i] for a PERMUTATION perm of [0, n): the (perm, src) pairs are radix-sorted
+ * by the destination's bits >= 11 (two 8-bit passes at 1e8), then one CTA per 2048-element
+ * destination window writes it with full coalesced stores (no partial-sector writes).  temp:
+ * >= sp_scatter32_perm_temp_bytes(n, dtype) bytes of device memory (NULL: allocated on the
+ * stream). */
+int64_t sp_scatter32_perm_temp_bytes(int64_t n, int32_t dtype);
+int sp_scatter32_perm(const void* src, const int32_t* perm, int64_t n, int32_t dtype, void* out, void* temp,
+                      int64_t temp_bytes, void* stream);
 /* dst[i] = pts[perm[i]] (s=3 points) — gather points into sorted order. */
 int sp_gather_points(const void* pts, const int64_t* perm, int64_t n, int32_t dtype, void* dst, void* stream);
 

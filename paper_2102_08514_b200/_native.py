@@ -139,6 +139,12 @@ EXPORTS = {
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p,
          ctypes.c_void_p],
     ),
+    "sp_scatter32_perm_temp_bytes": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int32]),
+    "sp_scatter32_perm": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+         ctypes.c_int64, ctypes.c_void_p],
+    ),
     "sp_scatter": (
         ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
     ),

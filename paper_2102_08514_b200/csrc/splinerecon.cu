@@ -1709,6 +1709,95 @@ extern "C" int sp_scatter32_blocked(const void* src, const int32_t* perm, int64_
     return SP_OK;
 }
 
+// Result scatter for a permutation, without partial-sector writes: a radix sort of the
+// (destination, value) pairs by the destination's high bits only (bits >= kPermWinBits, two
+// 8-bit onesweep passes at 1e8) puts the 2^kPermWinBits values of every destination window
+// into that window's own slot range (perm is a permutation, so each window holds exactly
+// its size); one CTA per window then places them in shared memory and writes the window
+// with full coalesced stores.
+constexpr int kPermWinBits = 11;
+
+template <typename T>
+__global__ void __launch_bounds__(256) perm_window_kernel(const int32_t* __restrict__ dst, const T* __restrict__ val,
+                                                          long long n, T* __restrict__ out) {
+    constexpr int W = 1 << kPermWinBits;
+    __shared__ T buf[W];
+    for (long long w = blockIdx.x; w * W < n; w += gridDim.x) {
+        const long long b0 = w * W;
+        const int m = (int)std::min<long long>(W, n - b0);
+        for (int i = threadIdx.x; i < m; i += 256) buf[dst[b0 + i] & (W - 1)] = val[b0 + i];
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += 256) out[b0 + i] = buf[i];
+        __syncthreads();
+    }
+}
+
+namespace {
+template <typename T>
+size_t perm_scatter_cub_bytes(int64_t n) {
+    size_t a = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                    static_cast<const T*>(nullptr), static_cast<T*>(nullptr), (int)n, kPermWinBits, 31);
+    return a;
+}
+int perm_end_bit(int64_t n) {
+    int b = 1;
+    while (b < 31 && (1ll << b) < n) ++b;
+    return std::max(b, kPermWinBits + 1);
+}
+}  // namespace
+
+extern "C" int64_t sp_scatter32_perm_temp_bytes(int64_t n, int32_t dtype) {
+    if (n <= 0 || n >= (1ll << 31)) return 0;
+    const size_t e = dtype == SP_F64 ? 8 : 4;
+    const size_t cub = dtype == SP_F64 ? perm_scatter_cub_bytes<double>(n) : perm_scatter_cub_bytes<float>(n);
+    return (int64_t)(align256((size_t)n * 4) + align256((size_t)n * e) + cub);
+}
+
+extern "C" int sp_scatter32_perm(const void* src, const int32_t* perm, int64_t n, int32_t dtype, void* out, void* temp,
+                                 int64_t temp_bytes, void* stream) {
+    if (n <= 0) return SP_OK;
+    if (n >= (1ll << 31)) return fail(SP_ERR_INVALID, "permutation scatter: n out of range");
+    if (!src || !perm || !out) return fail(SP_ERR_INVALID, "null argument");
+    if (dtype != SP_F32 && dtype != SP_F64) return fail(SP_ERR_INVALID, "unknown dtype");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t e = dtype == SP_F64 ? 8 : 4;
+    const size_t ds = align256((size_t)n * 4), vs = align256((size_t)n * e);
+    const size_t need = (size_t)sp_scatter32_perm_temp_bytes(n, dtype);
+    void* tmp = temp;
+    if (!tmp || (size_t)temp_bytes < need) {
+        tmp = nullptr;
+        SP_CUDA(cudaMallocAsync(&tmp, need, st));
+    }
+    unsigned char* base = static_cast<unsigned char*>(tmp);
+    int32_t* dsorted = reinterpret_cast<int32_t*>(base);
+    void* vsorted = base + ds;
+    void* cub_tmp = base + ds + vs;
+    size_t cb = need - ds - vs;
+    const int end_bit = perm_end_bit(n);
+    const long long nwin = (n + (1 << kPermWinBits) - 1) >> kPermWinBits;
+    const int blocks = (int)std::min<long long>(nwin, 148ll * 8);
+    cudaError_t err;
+    if (dtype == SP_F32) {
+        err = cub::DeviceRadixSort::SortPairs(cub_tmp, cb, perm, dsorted, (const float*)src, (float*)vsorted, (int)n,
+                                              kPermWinBits, end_bit, st);
+        if (err == cudaSuccess) {
+            perm_window_kernel<float><<<blocks, 256, 0, st>>>(dsorted, (const float*)vsorted, n, (float*)out);
+            err = cudaGetLastError();
+        }
+    } else {
+        err = cub::DeviceRadixSort::SortPairs(cub_tmp, cb, perm, dsorted, (const double*)src, (double*)vsorted, (int)n,
+                                              kPermWinBits, end_bit, st);
+        if (err == cudaSuccess) {
+            perm_window_kernel<double><<<blocks, 256, 0, st>>>(dsorted, (const double*)vsorted, n, (double*)out);
+            err = cudaGetLastError();
+        }
+    }
+    if (tmp != temp) cudaFreeAsync(tmp, st);
+    if (err != cudaSuccess) return fail(SP_ERR_CUDA, "permutation scatter: %s", cudaGetErrorString(err));
+    return SP_OK;
+}
+
 extern "C" int sp_gather_points(const void* pts, const int64_t* perm, int64_t n, int32_t dtype, void* dst, void* stream) {
     if (n <= 0) return SP_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

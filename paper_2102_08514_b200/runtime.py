@@ -484,6 +484,10 @@ class PlanInterpreter:
     # protocol B result scatter: destination window (elements) of the L2-blocked scatter
     # (sp_scatter32_blocked); 0 = the brick kernel scatters directly (sp_eval_bricks_indirect)
     scatter_window = int(os.environ.get("SP_SCATTER_WINDOW", str(1 << 24)))
+    # ... done as a radix sort of the (destination, value) pairs by the destination's high bits
+    # plus one full-store pass per 2048-value window (sp_scatter32_perm) instead of one pass
+    # over all pairs per L2 window
+    scatter_sorted = os.environ.get("SP_SCATTER_SORTED", "1") == "1"
 
     # protocol-B workspaces kept (one per thread x stream x batch shape, most recent first out)
     sort_ws_keep = 4
@@ -735,8 +739,14 @@ class PlanInterpreter:
                                                            start.data_ptr(), count.data_ptr(), n, b, perm.data_ptr(),
                                                            vals.data_ptr(), None if err is None else err.data_ptr(),
                                                            st.cuda_stream))
-                _native.check(lib.sp_scatter32_blocked(vals.data_ptr(), perm.data_ptr(), n, dtype, self.scatter_window,
-                                                       res.data_ptr(), st.cuda_stream))
+                if self.scatter_sorted:
+                    tmp2 = torch.empty(max(1, int(lib.sp_scatter32_perm_temp_bytes(n, dtype))), dtype=torch.uint8,
+                                       device=dev)
+                    _native.check(lib.sp_scatter32_perm(vals.data_ptr(), perm.data_ptr(), n, dtype, res.data_ptr(),
+                                                        tmp2.data_ptr(), tmp2.numel(), st.cuda_stream))
+                else:
+                    _native.check(lib.sp_scatter32_blocked(vals.data_ptr(), perm.data_ptr(), n, dtype,
+                                                           self.scatter_window, res.data_ptr(), st.cuda_stream))
                 return None
             fn = lib.sp_eval_bricks_perm32 if gather else lib.sp_eval_bricks_indirect
             _native.check(fn(h, ctypes.byref(gdesc), (sp_ if gather else p).data_ptr(), n, dtype, start.data_ptr(),

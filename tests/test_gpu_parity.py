@@ -375,14 +375,16 @@ def test_sync_free_brick_runs_match(name, presorted, cuda):
 
 @pytest.mark.parametrize("name,dtype", [("cc_tricubic", torch.float32), ("bcc_quintic_rd", torch.float32),
                                         ("fcc_cubic", torch.float64), ("bcc_linear_rd", torch.float32)])
-@pytest.mark.parametrize("gather,window", [(False, 0), (True, 0), (False, 1 << 12), (False, 1000)])
-def test_sorted32_protocol_b_matches_given_order(name, dtype, gather, window, cuda):
+@pytest.mark.parametrize("gather,window,sorted_scatter", [(False, 0, True), (True, 0, True), (False, 1 << 12, True),
+                                                           (False, 1000, False)])
+def test_sorted32_protocol_b_matches_given_order(name, dtype, gather, window, sorted_scatter, cuda):
     """order='sort' (sp_sort_points: 30-bit keys in the grid frame, CUB pair sort, device
     brick runs; then either a gathered copy + sp_eval_bricks_perm32, or
     sp_eval_bricks_indirect reading the caller's points through the permutation; both scatter
     back) is bit-identical to the chunk kernel on shuffled points, including points outside
-    the grid (clamped keys) and NaN.  window > 0: values in brick order, then the L2-blocked
-    result scatter (sp_scatter32_blocked, one pass per destination window)."""
+    the grid (clamped keys) and NaN.  window > 0: values in brick order, then the result
+    scatter — sp_scatter32_perm (pairs sorted by the destination's high bits, full-store
+    windows) or sp_scatter32_blocked (one pass per L2 window)."""
     from paper_2102_08514_b200.runtime import _sort_frame
 
     g, plan, grid = _setup(name, "mirror", dtype, cuda)
@@ -390,6 +392,7 @@ def test_sorted32_protocol_b_matches_given_order(name, dtype, gather, window, cu
     interp.sort_gather = gather
     if window:
         interp.scatter_window = window
+    interp.scatter_sorted = sorted_scatter
     rng = np.random.default_rng(17)
     hi = max(a.shape[0] for a in grid.arrays) * plan.diag[0]
     pts = rng.uniform(-3, hi + 3, size=(200_000, 3))
