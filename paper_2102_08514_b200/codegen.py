@@ -550,9 +550,19 @@ def kernel_programs(plan: EvaluationPlan) -> list:
 
 
 def _prog_select(plan: EvaluationPlan) -> str:
+    """Program id of kernel `kern`: the identity, else a bit field of one packed constant (a
+    shift and a mask whatever K is, instead of a K-deep select chain)."""
     ids = kernel_programs(plan)
     if ids == list(range(plan.K)):
         return "kern"
+    width = max(1, (max(ids)).bit_length())
+    packed = 0
+    for k, pid in enumerate(ids):
+        packed |= pid << (width * k)
+    if width * plan.K <= 32:
+        return f"(int)(({packed:#x}u >> ({width} * kern)) & {(1 << width) - 1}u)"
+    if width * plan.K <= 64:
+        return f"(int)(({packed:#x}ull >> ({width} * kern)) & {(1 << width) - 1}ull)"
     expr = str(ids[-1])
     for k in range(plan.K - 2, -1, -1):
         expr = f"(kern == {k} ? {ids[k]} : {expr})"
