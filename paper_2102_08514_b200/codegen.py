@@ -697,10 +697,19 @@ def _smem_tables(plan: EvaluationPlan) -> int:
     return plan.N * 16 + cube + plan.M * plan.N * 16
 
 
+def _env_override(var: str, name: str, default: int) -> int:
+    """Build-time tuning override: $var = "name:n,name:n" (occupancy / smem experiments)."""
+    for item in filter(None, os.environ.get(var, "").split(",")):
+        k, v = item.split(":")
+        if k == name:
+            return int(v)
+    return default
+
+
 def _sig_segment(plan: EvaluationPlan) -> int:
     """Signature-sort segment: 1024 points, 512 when the plan's tables are large (BCC Voronoi:
     N = 320, 20 KB cube table) so that three CTAs fit an SM (static arrays ~20 B per point)."""
-    return 512 if _smem_tables(plan) > 24 * 1024 else 1024
+    return _env_override("SP_CODEGEN_SIGSEG", plan.name, 512 if _smem_tables(plan) > 24 * 1024 else 1024)
 
 
 def tile_budget_kb(plan: EvaluationPlan) -> int:
@@ -709,7 +718,8 @@ def tile_budget_kb(plan: EvaluationPlan) -> int:
     (228 KB / 3 - 1 KB reserved per CTA)."""
     static = _sig_segment(plan) * 20 + 2048 if plan.K > 1 else 2048
     room = (75 * 1024 - _smem_tables(plan) - static) // 1024
-    return 40 if room >= 36 else max(20, room)  # measured: BCC Voronoi 27 KB + 512-point segments 22.4 -> 25.2
+    budget = 40 if room >= 36 else max(20, room)  # measured: BCC Voronoi 27 KB + 512-point segments 22.4 -> 25.2
+    return _env_override("SP_CODEGEN_TILEKB", plan.name, budget)
 
 
 def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple:
@@ -742,10 +752,7 @@ def generate_plan_source(plan: EvaluationPlan, stem: str | None = None) -> tuple
     if plan.K > 1 and max(kflops) <= 128:
         min_blocks = 3  # signature driver: 80 registers, 3 CTAs/SM (measured +11 % over 2)
     # build-time override for occupancy experiments: SP_CODEGEN_MINBLOCKS="stem:n,stem:n"
-    for item in filter(None, os.environ.get("SP_CODEGEN_MINBLOCKS", "").split(",")):
-        k, v = item.split(":")
-        if k == stem:
-            min_blocks = int(v)
+    min_blocks = _env_override("SP_CODEGEN_MINBLOCKS", stem, min_blocks)
     planes = []
     for j, (n, off) in enumerate(plan.planes):
         planes.append(f"    q |= ({_plane_expr(n)} >= R({float(off)!r})) ? {1 << j} : 0;")
