@@ -24,7 +24,8 @@ from paper_2102_08514_b200 import corpus  # noqa: E402
 from paper_2102_08514_b200.plan import PlanOptions  # noqa: E402
 from paper_2102_08514_b200.runtime import CoefficientGrid, PlanInterpreter  # noqa: E402
 
-PLANS = ["cc_trilinear", "cc_tricubic", "bcc_linear_rd", "bcc_quintic_rd", "fcc_cubic", "cc_zp3", "bcc_quartic"]
+PLANS = ["cc_trilinear", "cc_tricubic", "bcc_linear_rd", "bcc_quintic_rd", "fcc_cubic", "cc_zp3", "bcc_quartic",
+         "fcc_voronoi1", "bcc_voronoi1"]
 
 
 def grid_for(name, hi, boundary, dtype, dev, seed):
@@ -60,6 +61,15 @@ def main():
                     interp.sort_gather = gather
                     torch.testing.assert_close(interp.eval_batch(grid, pts, order="sort"), want, rtol=0, atol=0)
                 interp.sort_gather = False
+                # protocol B with the result scatter as a separate pass (both variants)
+                interp.scatter_window = 1024
+                for sorted_scatter in (True, False):
+                    interp.scatter_sorted = sorted_scatter
+                    torch.testing.assert_close(interp.eval_batch(grid, pts, order="sort"), want, rtol=0, atol=0)
+                vals, perm = interp.eval_batch_unordered(grid, pts)
+                torch.testing.assert_close(vals, want[perm.long()], rtol=0, atol=0)
+                interp.scatter_window = type(interp).scatter_window
+                interp.scatter_sorted = True
                 cases += 1
                 print(f"ok {name} {str(dtype)[6:]} {boundary} ({interp.kernel_name()})", flush=True)
         if name in ("cc_tricubic", "bcc_linear_rd"):
