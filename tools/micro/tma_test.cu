@@ -56,7 +56,7 @@ int main(int argc, char** argv) {
     const int big = argc > 2 ? atoi(argv[2]) : 0;   // box shape: 1 = 16^3, else 12x11x11
     const int neg = argc > 3 ? atoi(argv[3]) : 1;   // coords: 1 = (-2,3,6), 0 = (0,0,0), 2 = (2,3,6)
     const int bx = big ? 16 : 12, by = big ? 16 : 11, bz = big ? 16 : 11;
-    const int C0 = neg == 1 ? -2 : (neg == 2 ? 2 : 0), C1 = neg ? 3 : 0, C2 = neg == 3 ? -4 : (neg ? 8 : 0);
+    const int C0 = neg == 1 ? -2 : (neg == 2 ? 2 : 0), C1 = neg ? 3 : 0, C2 = neg == 3 ? -4 : (neg == 4 ? 5 : (neg == 5 ? -3 : (neg ? 8 : 0)));
     cudaMalloc(&o, bx * by * bz * 4);
     EncodeTiledFn enc = nullptr;
     cudaDriverEntryPointQueryResult q;
