@@ -568,3 +568,24 @@ def test_stream_argument_other_than_current(order, cuda):
         np.testing.assert_array_equal(got_np, want.numpy().astype(np.float64))
     vals, perm = interp.eval_batch_unordered(grid, base, stream=st)
     torch.testing.assert_close(vals.cpu(), want[perm.long().cpu()], rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("n,offset", [(100_003, 0), (100_000, 1), (5, 0), (1, 0), (4097, 0)])
+def test_brick_runs_from_points_kernels(n, offset, dtype, cuda):
+    """sp_brick_runs_points: the four-points-per-thread head-bits kernel (16-byte aligned
+    points, any n) and the one-point-per-thread fallback (a misaligned view) give the runs of
+    the host definition — a new run wherever a point's brick differs from its predecessor's."""
+    from paper_2102_08514_b200.runtime import prepare_points, prepare_points_async
+
+    rng = np.random.default_rng(n + offset)
+    base = rng.uniform(-40, 300, size=(n + offset, 3))
+    base = base[np.lexsort((base[:, 2] // 8, base[:, 1] // 8, base[:, 0] // 8))]  # runs of equal bricks
+    base[n // 3: n // 3 + 5] = np.nan  # non-finite points form / break runs like the host path
+    pts_all = torch.from_numpy(base).to(cuda, dtype)
+    pts = pts_all[offset:]
+    for b in (3, 4):
+        ref = prepare_points(pts, b, presorted=True)
+        asy = prepare_points_async(pts, b, presorted=True)
+        assert asy.n_bricks == ref.n_bricks
+        torch.testing.assert_close(asy.brick_start[: asy.n_bricks + 1], ref.brick_start, rtol=0, atol=0)
