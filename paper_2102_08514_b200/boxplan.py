@@ -6,9 +6,11 @@ stages: PP extraction over the knot-plane arrangement of the support (spline.py:
 (analysis.py:113-267), a greedy symmetry search rewriting sub-regions onto reference kernels
 (analysis.py:279-399), and plan assembly with fetch grouping / ordering
 (plancompile.py:150-380).  This module restates the same algorithm so the drop-in can
-compile a box-spline plan without the reference; `box_spline_plan(columns, lattice)` returns
-the `EvaluationPlan` the reference compiler emits — the same canonical document and
-checksum (tests/test_boxplan.py compares against the catalog's reference-compiled plans).
+compile a box-spline plan without the reference; `box_spline_plan(columns, lattice, cosets)`
+returns the `EvaluationPlan` the reference compiler emits — the same canonical document and
+checksum — and `compile_pp_plan` does the same for any PP spline (e.g. an imported Voronoi
+document).  tests/test_boxplan.py compares against the catalog's reference-compiled plans and
+PP documents and against reference-compiled plans of direction sets outside the catalog.
 
 Design notes (own implementation, not a translation):
 
@@ -17,9 +19,12 @@ Design notes (own implementation, not a translation):
   points that are vertices (tight on full-rank constraint sets), facets are the half-spaces
   tight on an affinely (s-1)-dimensional vertex set — the same canonical form the reference
   sorts cells and compares classes with;
-* each piece polynomial comes from the box-spline recurrence run symbolically around the
-  cell's centroid (side decisions of the half-open base case taken at the centroid,
-  barycentric coordinates carried as affine polynomials);
+* each piece polynomial comes from the box-spline recurrence run symbolically at the cell's
+  centroid (side decisions of the half-open base case taken there, barycentric coordinates
+  carried as affine polynomials in absolute coordinates); a node whose point lies outside its
+  sub-zonotope is zero, and node values are shared across cells keyed by the node's own
+  knot-plane side vector — 4-20x faster than a per-cell recurrence (bcc_quartic 12 s vs the
+  reference's 252 s), same polynomials;
 * the symmetry search walks the signed-permutation group in the reference's order and
   matches weight polynomials exactly, then fits the integer affine site renaming.
 """
@@ -30,7 +35,6 @@ import random
 from fractions import Fraction
 from itertools import combinations, permutations, product
 from math import floor, gcd
-from typing import Sequence
 
 from .exact import Poly
 from .plan import ClassTransform, EvaluationPlan, PlanError, PlanKernel, PlanOptions
@@ -97,10 +101,8 @@ def _det(a):
 
 
 def _nullspace_vector(rows, dim):
-    """One nonzero vector orthogonal to `rows` (rank dim-1)."""
-    for j in range(dim):
-        e = [F1 if i == j else F0 for i in range(dim)]
-        # Gram-Schmidt-free: solve rows . v = 0 with v_j fixed by elimination
+    """One nonzero vector orthogonal to `rows` (rank dim-1): reduced row echelon form, the
+    free column set to 1."""
     m = [[Fraction(v) for v in r] for r in rows]
     pivots, rank = [], 0
     for c in range(dim):
