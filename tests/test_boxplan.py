@@ -4,10 +4,9 @@ Anchors: the shipped catalog plans and PP documents (compiled by the reference, 
 gen_plans.py / gen_pp.py) and tests/golden/boxplan/ (direction sets outside the catalog,
 compiled by the reference end to end, tests/golden/make_boxplan_golden.py).  Equality is on
 the full wire document (plan_to_dict), i.e. the same checksum.  The slow corpus members
-(fcc_cubic 12 s, bcc_quintic_rd 45 s, cc_tricubic 85 s, bcc_voronoi1 45 s, cc_zp3 2 min)
-run with SP_SLOW_TESTS=1; all of them were checked equal when this test was written.
-bcc_quartic (DIAG + 2·E3): 720 pieces in 12 s here vs 252 s for the reference's extraction,
-document byte-identical.
+(cc_tricubic 41 s, bcc_voronoi1 40 s, cc_zp3 36 s) run with SP_SLOW_TESTS=1; all of them
+were checked equal.  bcc_quartic (DIAG + 2·E3): 720 pieces in 12 s here vs 252 s for the
+reference's extraction, document byte-identical.
 """
 import os
 
@@ -31,8 +30,8 @@ GOLDEN_CASES = {
     "cc3_e3_d2": (E3 + [(1, 1, 1), (1, -1, 1)], "CC3"),
 }
 
-FAST = ["tp2", "zp", "qc_tensor", "cc_trilinear", "bcc_linear_rd", "bcc_quartic"]
-SLOW_NAMES = ["fcc_cubic", "bcc_quintic_rd", "cc_tricubic"]
+FAST = ["tp2", "zp", "qc_tensor", "cc_trilinear", "bcc_linear_rd", "bcc_quartic", "fcc_cubic", "bcc_quintic_rd"]
+SLOW_NAMES = ["cc_tricubic"]
 
 
 @pytest.mark.parametrize("name", FAST + [pytest.param(n, marks=pytest.mark.skipif(not SLOW, reason="SP_SLOW_TESTS"))
