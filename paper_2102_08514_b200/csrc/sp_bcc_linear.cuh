@@ -348,4 +348,216 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Leaner tile path (bcc_tet_brick_kernel_v2).  Same values, bit for bit, as bcc_tet_tile:
+//  * rint(y/2) by the magic-number add: t = fma(y, 1/2, 1.5*2^p) rounds y/2 (exact) to the
+//    nearest integer, ties to even (the magic is even), so f = t - magic is rint(y/2) and the
+//    low mantissa bits of t hold that integer: no FRND / F2I on the conversion pipe;
+//  * tile reads through one 32-bit shared-window address (no generic->shared conversion per
+//    point), byte offsets folded into the strides;
+//  * the brick test is made once per quad of points: four straight-line evaluations when all
+//    four lie in the brick (always, for brick runs of finite in-range points).
+template <typename T>
+struct TetMagic;
+template <>
+struct TetMagic<float> {
+    static constexpr float kM = 12582912.0f;                // 1.5 * 2^23
+    static constexpr unsigned kBits = 0x4B400000u;          // its bit pattern: k = bits(t) - kBits
+    __device__ static __forceinline__ unsigned bits(float t) { return __float_as_uint(t); }
+};
+template <>
+struct TetMagic<double> {
+    static constexpr double kM = 6755399441055744.0;        // 1.5 * 2^52: low word of bits(t) is k
+    static constexpr unsigned kBits = 0u;
+    __device__ static __forceinline__ unsigned bits(double t) { return (unsigned)__double2loint(t); }
+};
+
+template <typename T>
+__device__ __forceinline__ T lds_at(unsigned addr);
+template <>
+__device__ __forceinline__ float lds_at<float>(unsigned addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+template <>
+__device__ __forceinline__ double lds_at<double>(unsigned addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+
+// One in-brick point from the staged tile; `sbias` = shared address of the tile element of
+// coset-0 cell (0,0,0) minus kBits * (S0 + S1 + S2) bytes (so the raw magic bits index it).
+template <int E, typename T>
+__device__ __forceinline__ T bcc_tet_tile_v2(T x0, T x1, T x2, unsigned sbias, unsigned sbase) {
+    constexpr T kM = TetMagic<T>::kM;
+    constexpr int SZ = (int)sizeof(T);
+    constexpr int S0 = E * E * SZ, S1 = E * SZ, S2 = SZ, ODD = E * E * E * SZ;
+    const T y0 = x0 - T(1), y1 = x1 - T(1), y2 = x2 - T(1);
+    const T t0 = fma(y0, T(0.5), kM), t1 = fma(y1, T(0.5), kM), t2 = fma(y2, T(0.5), kM);
+    const T d0 = fma(t0 - kM, T(-2), y0), d1 = fma(t1 - kM, T(-2), y1), d2 = fma(t2 - kM, T(-2), y2);
+    TetSel<T> t;
+    t.n0 = d0 < T(0);
+    t.n1 = d1 < T(0);
+    t.n2 = d2 < T(0);
+    const T w0 = fabs(d0), w1 = fabs(d1), w2 = fabs(d2);
+    t.c01 = w0 >= w1;
+    t.c02 = w0 >= w2;
+    t.c12 = w1 >= w2;
+    const T mx01 = fmax(w0, w1), mn01 = fmin(w0, w1);
+    t.wa = fmax(mx01, w2);
+    t.wb = fmin(mn01, w2);
+    t.wm = fmax(mn01, fmin(mx01, w2));
+    const int ss0 = t.n0 ? -S0 : S0, ss1 = t.n1 ? -S1 : S1, ss2 = t.n2 ? -S2 : S2;
+    const int sa = t.c01 ? (t.c02 ? ss0 : ss2) : (t.c12 ? ss1 : ss2);
+    const int sb = t.c01 ? (t.c12 ? ss2 : ss1) : (t.c02 ? ss2 : ss0);
+    const unsigned aE = sbias + TetMagic<T>::bits(t0) * (unsigned)S0 + TetMagic<T>::bits(t1) * (unsigned)S1 +
+                        TetMagic<T>::bits(t2) * (unsigned)S2;
+    const unsigned aO = aE + (unsigned)ODD - (unsigned)((t.n0 ? S0 : 0) + (t.n1 ? S1 : 0) + (t.n2 ? S2 : 0));
+    const unsigned aB = t.wm > t.wb ? aO - (unsigned)sb : aO;  // tet_guard_b (see bcc_tet_tile)
+    SP_CHECK(aE - sbase < (unsigned)ODD && aE + sa - sbase < (unsigned)ODD && aO - sbase - ODD < (unsigned)ODD &&
+             aB - sbase - ODD < (unsigned)ODD);
+    (void)sbase;
+    return tet_combine<T>(t, lds_at<T>(aE), lds_at<T>(aE + (unsigned)sa), lds_at<T>(aO), lds_at<T>(aB));
+}
+
+template <typename T, int L2B, int MINB = (sizeof(T) == 4 ? 3 : 2)>
+__global__ void __launch_bounds__(kThreads, MINB)
+    bcc_tet_brick_kernel_v2(const EvalArgs<T> a, const long long* __restrict__ brick_start, int nbricks) {
+    constexpr int B = 1 << L2B;
+    constexpr int E = B / 2 + 2;
+    constexpr int VOL = E * E * E;
+    constexpr int SZ = (int)sizeof(T);
+    constexpr T kF = BccTetTraits<T>::kFast;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* const tile = reinterpret_cast<T*>(smem);  // [2 * VOL]: coset 0 | coset 1
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(tile);
+    const int tid = threadIdx.x;
+    if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);
+
+    auto load_quad = [&](long long j0, T xs[12]) {
+        if (j0 + 4 <= a.n) {
+            if constexpr (sizeof(T) == 4) {
+                const float4* src = reinterpret_cast<const float4*>(a.pts + 3 * j0);
+#pragma unroll
+                for (int v = 0; v < 3; ++v) {
+                    const float4 t = __ldg(src + v);
+                    xs[4 * v] = t.x;
+                    xs[4 * v + 1] = t.y;
+                    xs[4 * v + 2] = t.z;
+                    xs[4 * v + 3] = t.w;
+                }
+            } else {
+                const double2* src = reinterpret_cast<const double2*>(a.pts + 3 * j0);
+#pragma unroll
+                for (int v = 0; v < 6; ++v) {
+                    const double2 t = __ldg(src + v);
+                    xs[2 * v] = t.x;
+                    xs[2 * v + 1] = t.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 12; ++e) xs[e] = j0 + e / 3 < a.n ? __ldg(a.pts + 3 * j0 + e) : T(0);
+        }
+    };
+
+    for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
+        int c[3];
+        {
+            const T* x = a.pts + 3 * brick_start[b];  // uniform loads (broadcast)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) c[i] = (clamp_cell(x[i]) >> L2B) << L2B;
+        }
+        const long long p0 = brick_start[b], p1 = brick_start[b + 1];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int z0b = (c[0] >> 1) - 1 - a.grid.org[k][0];
+            const int z1b = (c[1] >> 1) - 1 - a.grid.org[k][1];
+            const int z2b = (c[2] >> 1) - 1 - a.grid.org[k][2];
+            const int g0 = a.grid.ext[k][0], g1 = a.grid.ext[k][1], g2 = a.grid.ext[k][2];
+            if (a.grid.boundary == SP_ZERO)
+                stage_cube<SP_ZERO, E>(tile + k * VOL, a.grid.data[k], z0b, z1b, z2b, g0, g1, g2, tid);
+            else if (a.grid.boundary == SP_CLAMP)
+                stage_cube<SP_CLAMP, E>(tile + k * VOL, a.grid.data[k], z0b, z1b, z2b, g0, g1, g2, tid);
+            else
+                stage_cube<SP_MIRROR, E>(tile + k * VOL, a.grid.data[k], z0b, z1b, z2b, g0, g1, g2, tid);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const long long q0 = p0 >> 2, q1 = (p1 + 3) >> 2;
+        // two quads in flight per thread, ping-ponged between two register sets (no copies);
+        // the first one is loaded while the tile lands
+        T xa[12], xb[12];
+        long long q = q0 + tid;
+        if (q < q1) load_quad(q << 2, xa);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+        const int lo0 = (c[0] >> 1) - 1, lo1 = (c[1] >> 1) - 1, lo2 = (c[2] >> 1) - 1;
+        const int base = -(lo0 * E * E + lo1 * E + lo2);  // tile index of coset-0 cell (0,0,0)
+        const unsigned sbias = sbase + (unsigned)(base * SZ) -
+                               TetMagic<T>::kBits * (unsigned)(E * E * SZ + E * SZ + SZ);
+        const bool dom = (T)c[0] > -kF && (T)c[1] > -kF && (T)c[2] > -kF && (T)(c[0] + B) < kF &&
+                         (T)(c[1] + B) < kF && (T)(c[2] + B) < kF;
+        const T blo0 = dom ? (T)c[0] : kF, blo1 = (T)c[1], blo2 = (T)c[2];  // dom false: no point passes
+        const T bhi0 = (T)(c[0] + B), bhi1 = (T)(c[1] + B), bhi2 = (T)(c[2] + B);
+
+        auto process = [&](long long q, const T xs[12]) {
+            const long long j0 = q << 2;
+            T r[4];
+            auto in_brick = [&](int u) {  // non-short-circuit: one predicate chain
+                return (xs[3 * u] >= blo0) & (xs[3 * u] < bhi0) & (xs[3 * u + 1] >= blo1) & (xs[3 * u + 1] < bhi1) &
+                       (xs[3 * u + 2] >= blo2) & (xs[3 * u + 2] < bhi2);
+            };
+            if (in_brick(0) & in_brick(1) & in_brick(2) & in_brick(3)) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) r[u] = bcc_tet_tile_v2<E, T>(xs[3 * u], xs[3 * u + 1], xs[3 * u + 2], sbias, sbase);
+            } else {
+#pragma unroll 1
+                for (int u = 0; u < 4; ++u) {  // rare: one call site each, registers selected
+                    auto pick = [&](int o) { return u == 0 ? xs[o] : u == 1 ? xs[3 + o] : u == 2 ? xs[6 + o] : xs[9 + o]; };
+                    const T x0 = pick(0), x1 = pick(1), x2 = pick(2);
+                    T v;
+                    if ((x0 >= blo0) & (x0 < bhi0) & (x1 >= blo1) & (x1 < bhi1) & (x2 >= blo2) & (x2 < bhi2))
+                        v = bcc_tet_tile_v2<E, T>(x0, x1, x2, sbias, sbase);
+                    else if (fabs(x0) < kF && fabs(x1) < kF && fabs(x2) < kF)
+                        v = bcc_tet_global<T, T>(a, x0 - T(1), x1 - T(1), x2 - T(1));
+                    else if (isfinite(x0) && isfinite(x1) && isfinite(x2))
+                        v = bcc_tet_global<double, T>(a, (double)x0 - 1.0, (double)x1 - 1.0, (double)x2 - 1.0);
+                    else
+                        v = T(NAN);
+                    r[0] = u == 0 ? v : r[0];
+                    r[1] = u == 1 ? v : r[1];
+                    r[2] = u == 2 ? v : r[2];
+                    r[3] = u == 3 ? v : r[3];
+                }
+            }
+            if (j0 >= p0 && j0 + 4 <= p1) {
+                if constexpr (sizeof(T) == 4) {
+                    *reinterpret_cast<float4*>(a.out + j0) = make_float4(r[0], r[1], r[2], r[3]);
+                } else {
+                    reinterpret_cast<double2*>(a.out + j0)[0] = make_double2(r[0], r[1]);
+                    reinterpret_cast<double2*>(a.out + j0)[1] = make_double2(r[2], r[3]);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (j0 + u >= p0 && j0 + u < p1) a.out[j0 + u] = r[u];
+            }
+        };
+
+#pragma unroll 1
+        for (; q < q1; q += 2 * kThreads) {
+            const bool has_b = q + kThreads < q1;
+            if (has_b) load_quad((q + kThreads) << 2, xb);
+            process(q, xa);
+            if (!has_b) break;
+            if (q + 2 * kThreads < q1) load_quad((q + 2 * kThreads) << 2, xa);
+            process(q + kThreads, xb);
+        }
+        __syncthreads();  // the tile is restaged for the next brick
+    }
+}
+
 }  // namespace sp
