@@ -804,13 +804,17 @@ int try_bricks_bcc_tet(const sp_plan* p, const sp::EvalArgs<T>& a, const int64_t
     static const int variant = env_int("SP_BCC_TET_VARIANT", 0);
     const bool db = variant == 2;
     const size_t smem = (db ? 4 : 2) * (size_t)E * E * E * sizeof(T);  // two cosets (x2 double-buffered)
-    auto kern = log2b == 3   ? sp::bcc_tet_brick_kernel_v2<T, 3>
-                : log2b == 4 ? sp::bcc_tet_brick_kernel_v2<T, 4>
+    // float64: the round-2 kernel (two float64 quads in flight need 128 registers and spill:
+    // 102.6 vs 106.8 Gpts/s measured at C3)
+    constexpr bool lean = sizeof(T) == 4;
+    auto kern = log2b == 3   ? (lean ? sp::bcc_tet_brick_kernel_v2<T, 3> : sp::bcc_tet_brick_kernel<T, 3>)
+                : log2b == 4 ? (lean ? sp::bcc_tet_brick_kernel_v2<T, 4> : sp::bcc_tet_brick_kernel<T, 4>)
                 : variant == 1 ? sp::bcc_tet_brick_kernel<T, 5, false, sizeof(T) == 4 ? 4 : 2>
                 : variant == 2 ? sp::bcc_tet_brick_kernel<T, 5, true, sizeof(T) == 4 ? 3 : 2, true>
                 : variant == 3 ? sp::bcc_tet_brick_kernel<T, 5>
                 : variant == 4 ? sp::bcc_tet_brick_kernel_v2<T, 5, sizeof(T) == 4 ? 4 : 3>
-                               : sp::bcc_tet_brick_kernel_v2<T, 5>;
+                : lean       ? sp::bcc_tet_brick_kernel_v2<T, 5>
+                               : sp::bcc_tet_brick_kernel<T, 5>;
     const int per_sm = sp::cached_occupancy(kern, smem);
     const int blocks = std::max(1, std::min(nbricks, p->num_sms * per_sm));
     kern<<<blocks, sp::kThreads, smem, st>>>(a, bs, nbricks);

@@ -127,3 +127,52 @@ def test_slab_halo_covers_the_gpu_kernels(name, boundary, cuda):
         sel = own == r
         got = interp.eval_batch(local, pts[sel])
         torch.testing.assert_close(got, want[sel], rtol=0, atol=0)
+
+
+_BCC_VARIANT_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from tests.test_gpu_scale import _bcc_variant_case
+torch.save(_bcc_variant_case(torch.device("cuda", 0), getattr(torch, sys.argv[3])), sys.argv[2])
+"""
+
+
+def _bcc_variant_case(cuda, dtype):
+    """BCC linear at the C3 grid: 2e6 Morton-ordered points plus points the lean kernel must
+    route to its per-point path (outside the grid, |x| beyond the float fast domain, NaN,
+    plane ties), evaluated through the brick kernel (the variant the process selects)."""
+    plan, grid, hi = _grid("bcc_linear_rd", dtype, cuda)
+    gen = torch.Generator(device=cuda).manual_seed(21)
+    pts = (torch.rand((2_000_000, 3), generator=gen, device=cuda) * (hi + 9) - 4).to(dtype)
+    ties = torch.floor(torch.rand((8192, 3), generator=gen, device=cuda) * (hi + 1) * 2) / 2
+    odd = torch.tensor([[float("nan"), 3.0, 4.0], [5e6, 1.0, 2.0], [-3e7, 7.5, 1.0], [1e30, 2.0, 2.0]],
+                       device=cuda).repeat(64, 1)
+    pts = torch.cat([pts, ties.to(dtype), odd.to(dtype)])
+    pts = pts[morton_order(pts)].contiguous()
+    return PlanInterpreter(plan).eval_batch(grid, pts, order="morton").cpu()
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_bcc_linear_lean_kernel_is_bit_identical(dtype, cuda, tmp_path):
+    """The default BCC linear brick kernel (bcc_tet_brick_kernel_v2: magic-number rint,
+    quad-level brick test) returns the same bits as the round-2 kernel (SP_BCC_TET_VARIANT=3)
+    and as the generic brick driver (BccTetEval), NaN positions included."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for label, env in (("v2", {}), ("v1", {"SP_BCC_TET_VARIANT": "3"}), ("generic", {"SP_BCC_TET_BRICK": "0"})):
+        path = str(tmp_path / f"{label}.pt")
+        r = subprocess.run([sys.executable, "-c", _BCC_VARIANT_SCRIPT, root, path, dtype],
+                           env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[label] = torch.load(path)
+    a = outs["v2"]
+    assert torch.isnan(a).sum().item() == 64
+    for label in ("v1", "generic"):
+        b = outs[label]
+        assert torch.equal(torch.isnan(a), torch.isnan(b)), label
+        assert torch.equal(a.nan_to_num(0.0).view(torch.int32 if a.dtype == torch.float32 else torch.int64),
+                           b.nan_to_num(0.0).view(torch.int32 if b.dtype == torch.float32 else torch.int64)), label
