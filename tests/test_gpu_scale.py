@@ -131,8 +131,8 @@ def test_slab_halo_covers_the_gpu_kernels(name, boundary, cuda):
 
 _BCC_VARIANT_SCRIPT = r"""
 import sys, torch
-sys.path.insert(0, sys.argv[1])
-from tests.test_gpu_scale import _bcc_variant_case
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
+from test_gpu_scale import _bcc_variant_case
 torch.save(_bcc_variant_case(torch.device("cuda", 0), getattr(torch, sys.argv[3])), sys.argv[2])
 """
 
