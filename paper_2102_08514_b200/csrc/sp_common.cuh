@@ -69,6 +69,7 @@ struct EvalArgs {
     int vec_cap;                // row-vector tile capacity in elements (0: no row-vector tile)
     const int* nbricks_dev;     // nullable: brick count in device memory (sync-free brick runs)
     int prefetch_pts;           // TMA brick kernel: bulk-prefetch each next brick's points into L2
+    int plain_pts;              // TMA brick kernel: plain-point loop (SP_TMA_PLAIN, default on)
 };
 
 // Checked build (build.py --checked -> libsplinerecon_checked.so, loaded with SP_CHECKED=1):
@@ -118,6 +119,9 @@ __device__ __forceinline__ int floordiv_i(int a, int d) {
 // NaN to 0, so this is branch-free (non-finite points are masked out by the callers).
 __device__ __forceinline__ int clamp_cell(float v) { return min(max(__float2int_rd(v), -kCellClamp), kCellClamp); }
 __device__ __forceinline__ int clamp_cell(double v) { return min(max(__double2int_rd(v), -kCellClamp), kCellClamp); }
+// floor(v) as int, saturating (cvt.rmi), NaN -> 0: equals clamp_cell(v) for |v| < 2^30
+__device__ __forceinline__ int floor_int(float v) { return __float2int_rd(v); }
+__device__ __forceinline__ int floor_int(double v) { return __double2int_rd(v); }
 
 __device__ __forceinline__ int mirror_index(int v, int n) {
     // runtime.py:191-196 (period 2n-2)

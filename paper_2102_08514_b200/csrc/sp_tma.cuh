@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
     };
 
     if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);
+    const bool plain = !a.in_index32 && !a.out_index && !a.out_index32 && !a.dbg && a.plain_pts;
     if (tid == 0 && (int)blockIdx.x < nbricks) issue(blockIdx.x, 0);
     unsigned phase = 0u;  // bit s = mbarrier parity of buffer s
     int it = 0;
@@ -189,6 +190,54 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
         ctx.err = 0;
         ctx.load_geom(geom, 1);
         const long long p0 = brick_start[b], p1 = brick_start[b + 1];
+        if (plain) {
+            // plain brick-order points (no permutations, no debug output): direct point loads and
+            // stores, and "inside the staged brick" from the saturating floor conversions (far
+            // points fail it) plus one NaN test (x0 + x1 + x2 != itself); the others take
+            // eval_one's paths
+            const T* px = a.pts + 3 * (p0 + tid);
+            T y0 = T(0), y1 = T(0), y2 = T(0);
+            if (p0 + tid < p1) {
+                y0 = __ldg(px);
+                y1 = __ldg(px + 1);
+                y2 = __ldg(px + 2);
+            }
+#pragma unroll 1
+            for (long long j = p0 + tid; j < p1; j += kThreads) {
+                const T x[3] = {y0, y1, y2};
+                px += 3 * kThreads;
+                if (j + kThreads < p1) {
+                    y0 = __ldg(px);
+                    y1 = __ldg(px + 1);
+                    y2 = __ldg(px + 2);
+                }
+                T v;
+                const int X0 = floor_int(x[0]), X1 = floor_int(x[1]), X2 = floor_int(x[2]);
+                const T sum = x[0] + x[1] + x[2];
+                if (((unsigned)(X0 - c0) < (unsigned)B) & ((unsigned)(X1 - c1) < (unsigned)B) &
+                    ((unsigned)(X2 - c2) < (unsigned)B) & (sum == sum)) {
+                    ctx.X[0] = X0;  // = clamp_cell(x): |x| < 2^30 inside a staged brick
+                    ctx.X[1] = X1;
+                    ctx.X[2] = X2;
+                    TileFetch<T, V> f;
+                    f.tile = tile;
+                    f.vtile = vtile;
+                    SP_TILE_LIMIT(f, ctx.geom->total);
+                    v = Ev::template eval<TileFetch<T, V>>(x, f, ctx);
+                } else {
+                    ctx.index = j;
+                    ctx.X[0] = clamp_cell(x[0]);
+                    ctx.X[1] = clamp_cell(x[1]);
+                    ctx.X[2] = clamp_cell(x[2]);
+                    v = eval_one<T, Ev, V>(x, true, c0, c1, c2, B, tile, vtile, ctx);
+                }
+                SP_CHECK(j >= 0 && j < a.n);
+                a.out[j] = v;
+            }
+            if (ctx.err && a.err) atomicOr(a.err, 1);
+            __syncthreads();  // vtile / geom / this buffer are rewritten next iteration
+            continue;
+        }
         T xn0 = T(0), xn1 = T(0), xn2 = T(0);
         if (p0 + tid < p1) {
             const T* px = point_ptr(a, p0 + tid);
