@@ -69,7 +69,7 @@ struct EvalArgs {
     int vec_cap;                // row-vector tile capacity in elements (0: no row-vector tile)
     const int* nbricks_dev;     // nullable: brick count in device memory (sync-free brick runs)
     int prefetch_pts;           // TMA brick kernel: bulk-prefetch each next brick's points into L2
-    int plain_pts;              // TMA brick kernel: plain-point loop (SP_TMA_PLAIN, default on)
+    int plain_pts;              // brick kernels: plain-point loop (SP_PLAIN_PTS, default on)
 };
 
 // Checked build (build.py --checked -> libsplinerecon_checked.so, loaded with SP_CHECKED=1):
@@ -923,15 +923,38 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
             __syncthreads();
             continue;
         }
+        // plain brick-order points (no permutations, no debug output) in an exact brick (corner
+        // + B <= 2^30): points inside the staged brick are recognised from the saturating floor
+        // conversions plus one NaN test and evaluated from the tile directly (same values: X is
+        // clamp_cell(x) there); the others take the checked path below
+        const bool plain = !a.in_index32 && !a.out_index && !a.out_index32 && !a.dbg && a.plain_pts && staged &&
+                           c0 + B <= kCellClamp && c1 + B <= kCellClamp && c2 + B <= kCellClamp;
 #pragma unroll 1
         for (long long j = p0 + tid; j < p1; j += kThreads) {
             ctx.index = j;
             const T x[3] = {xn0, xn1, xn2};
             if (j + kThreads < p1) {
-                const T* px = point_ptr(a, j + kThreads);
+                const T* px = plain ? a.pts + 3 * (j + kThreads) : point_ptr(a, j + kThreads);
                 xn0 = __ldg(px);
                 xn1 = __ldg(px + 1);
                 xn2 = __ldg(px + 2);
+            }
+            if (plain) {
+                const int X0 = floor_int(x[0]), X1 = floor_int(x[1]), X2 = floor_int(x[2]);
+                const T sum = x[0] + x[1] + x[2];
+                if (((unsigned)(X0 - c0) < (unsigned)B) & ((unsigned)(X1 - c1) < (unsigned)B) &
+                    ((unsigned)(X2 - c2) < (unsigned)B) & (sum == sum)) {
+                    ctx.X[0] = X0;
+                    ctx.X[1] = X1;
+                    ctx.X[2] = X2;
+                    TileFetch<T, V> f;
+                    f.tile = tile;
+                    f.vtile = vtile;
+                    SP_TILE_LIMIT(f, ctx.geom->total);
+                    SP_CHECK(j >= 0 && j < a.n);
+                    a.out[j] = Ev::template eval<TileFetch<T, V>>(x, f, ctx);
+                    continue;
+                }
             }
             T v;
             const bool fin = isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]);

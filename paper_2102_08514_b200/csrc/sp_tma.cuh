@@ -195,6 +195,8 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
             // stores, and "inside the staged brick" from the saturating floor conversions (far
             // points fail it) plus one NaN test (x0 + x1 + x2 != itself); the others take
             // eval_one's paths
+            // bricks at the clamp limit (corner + B > 2^30) keep the clamped path for every point
+            const bool bexact = c0 + B <= kCellClamp && c1 + B <= kCellClamp && c2 + B <= kCellClamp;
             const T* px = a.pts + 3 * (p0 + tid);
             T y0 = T(0), y1 = T(0), y2 = T(0);
             if (p0 + tid < p1) {
@@ -214,9 +216,9 @@ __global__ void __launch_bounds__(kThreads, Ev::kMinBlocks)
                 T v;
                 const int X0 = floor_int(x[0]), X1 = floor_int(x[1]), X2 = floor_int(x[2]);
                 const T sum = x[0] + x[1] + x[2];
-                if (((unsigned)(X0 - c0) < (unsigned)B) & ((unsigned)(X1 - c1) < (unsigned)B) &
+                if (bexact & ((unsigned)(X0 - c0) < (unsigned)B) & ((unsigned)(X1 - c1) < (unsigned)B) &
                     ((unsigned)(X2 - c2) < (unsigned)B) & (sum == sum)) {
-                    ctx.X[0] = X0;  // = clamp_cell(x): |x| < 2^30 inside a staged brick
+                    ctx.X[0] = X0;  // = clamp_cell(x): |X| < 2^30 inside an exact brick
                     ctx.X[1] = X1;
                     ctx.X[2] = X2;
                     TileFetch<T, V> f;

@@ -837,7 +837,7 @@ int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, 
     a.in_index32 = in_index32;
     a.nbricks_dev = nbricks_dev;
     a.prefetch_pts = env_int("SP_PREFETCH_PTS", 1);
-    a.plain_pts = env_int("SP_TMA_PLAIN", 1);
+    a.plain_pts = env_int("SP_PLAIN_PTS", 1);
     if constexpr (sizeof(T) == 4) {
         const int t = try_bricks_tma(p, g, a, bstart, nbricks, log2b, st);
         if (t != 0) return t > 0 ? SP_OK : t;
