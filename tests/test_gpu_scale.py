@@ -9,7 +9,8 @@ from paper_2102_08514_b200.runtime import CoefficientGrid, PlanInterpreter, mort
 
 pytestmark = pytest.mark.gpu
 
-CONFIGS = {  # C2, C3, C4 (ZP3, FCC-6), C5 (Voronoi at 512^3-equivalent samples)
+CONFIGS = {  # C1, C2, C3, C4 (ZP3, FCC-6), C5 (Voronoi at 512^3-equivalent samples)
+    "cc_trilinear": 63,
     "cc_tricubic": 255,
     "bcc_linear_rd": 405,
     "bcc_quintic_rd": 405,
@@ -133,15 +134,16 @@ _BCC_VARIANT_SCRIPT = r"""
 import sys, torch
 sys.path[:0] = [sys.argv[1], sys.argv[1] + "/tests"]
 from test_gpu_scale import _bcc_variant_case
-torch.save(_bcc_variant_case(torch.device("cuda", 0), getattr(torch, sys.argv[3])), sys.argv[2])
+name = sys.argv[4] if len(sys.argv) > 4 else "bcc_linear_rd"
+torch.save(_bcc_variant_case(torch.device("cuda", 0), getattr(torch, sys.argv[3]), name), sys.argv[2])
 """
 
 
-def _bcc_variant_case(cuda, dtype):
-    """BCC linear at the C3 grid: 2e6 Morton-ordered points plus points the lean kernel must
-    route to its per-point path (outside the grid, |x| beyond the float fast domain, NaN,
-    plane ties), evaluated through the brick kernel (the variant the process selects)."""
-    plan, grid, hi = _grid("bcc_linear_rd", dtype, cuda)
+def _bcc_variant_case(cuda, dtype, name="bcc_linear_rd"):
+    """A BASELINE grid: 2e6 Morton-ordered points plus points the fast loops must route to
+    their checked path (outside the grid, |x| beyond the float fast domain, NaN, plane ties),
+    evaluated through the brick kernels (the variant the process's environment selects)."""
+    plan, grid, hi = _grid(name, dtype, cuda)
     gen = torch.Generator(device=cuda).manual_seed(21)
     pts = (torch.rand((2_000_000, 3), generator=gen, device=cuda) * (hi + 9) - 4).to(dtype)
     ties = torch.floor(torch.rand((8192, 3), generator=gen, device=cuda) * (hi + 1) * 2) / 2
@@ -165,7 +167,7 @@ def test_bcc_linear_lean_kernel_is_bit_identical(dtype, cuda, tmp_path):
     outs = {}
     for label, env in (("v2", {}), ("v1", {"SP_BCC_TET_VARIANT": "3"}), ("generic", {"SP_BCC_TET_BRICK": "0"})):
         path = str(tmp_path / f"{label}.pt")
-        r = subprocess.run([sys.executable, "-c", _BCC_VARIANT_SCRIPT, root, path, dtype],
+        r = subprocess.run([sys.executable, "-c", _BCC_VARIANT_SCRIPT, root, path, dtype, "bcc_linear_rd"],
                            env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs[label] = torch.load(path)
@@ -176,3 +178,29 @@ def test_bcc_linear_lean_kernel_is_bit_identical(dtype, cuda, tmp_path):
         assert torch.equal(torch.isnan(a), torch.isnan(b)), label
         assert torch.equal(a.nan_to_num(0.0).view(torch.int32 if a.dtype == torch.float32 else torch.int64),
                            b.nan_to_num(0.0).view(torch.int32 if b.dtype == torch.float32 else torch.int64)), label
+
+
+@pytest.mark.parametrize("name,dtype", [("cc_tricubic", "float32"), ("cc_trilinear", "float32"),
+                                        ("cc_tricubic", "float64"), ("bcc_quintic_rd", "float32"),
+                                        ("cc_zp3", "float32")])
+def test_plain_point_loops_are_bit_identical(name, dtype, cuda, tmp_path):
+    """The plain-point loops of brick_kernel_tma / brick_kernel (direct loads and stores,
+    inside-the-brick test from the floor conversions + one NaN test) return the same bits as
+    the checked loops (SP_PLAIN_PTS=0) on BASELINE grids with outliers, NaN and ties."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for label, env in (("plain", {}), ("checked", {"SP_PLAIN_PTS": "0"})):
+        path = str(tmp_path / f"{label}.pt")
+        r = subprocess.run([sys.executable, "-c", _BCC_VARIANT_SCRIPT, root, path, dtype, name],
+                           env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[label] = torch.load(path)
+    a, b = outs["plain"], outs["checked"]
+    assert torch.isnan(a).sum().item() == 64
+    assert torch.equal(torch.isnan(a), torch.isnan(b))
+    it = torch.int32 if a.dtype == torch.float32 else torch.int64
+    assert torch.equal(a.nan_to_num(0.0).view(it), b.nan_to_num(0.0).view(it))
