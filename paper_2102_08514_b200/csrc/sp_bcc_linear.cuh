@@ -357,7 +357,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
 //  * tile reads through one 32-bit shared-window address (no generic->shared conversion per
 //    point), byte offsets folded into the strides;
 //  * the brick test is made once per quad of points: four straight-line evaluations when all
-//    four lie in the brick (always, for brick runs of finite in-range points).
+//    four lie in the brick (always, for brick runs of finite in-range points);
+//  * two quads in flight per thread in two register sets used alternately (no copies).
+// The default for float32 (245.6 -> 260 Gpts/s at C3); float64 keeps bcc_tet_brick_kernel
+// (its two float64 quads need 128 registers and spill).
 template <typename T>
 struct TetMagic;
 template <>
