@@ -358,9 +358,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
 //    point), byte offsets folded into the strides;
 //  * the brick test is made once per quad of points: four straight-line evaluations when all
 //    four lie in the brick (always, for brick runs of finite in-range points);
-//  * two quads in flight per thread in two register sets used alternately (no copies).
-// The default for float32 (245.6 -> 260 Gpts/s at C3); float64 keeps bcc_tet_brick_kernel
-// (its two float64 quads need 128 registers and spill).
+//  * points in groups of three 16-byte vectors (4 float32 / 2 float64 points), two groups in
+//    flight per thread in two register sets used alternately (no copies).
 template <typename T>
 struct TetMagic;
 template <>
@@ -440,8 +439,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const int tid = threadIdx.x;
     if (a.nbricks_dev) nbricks = min(nbricks, *a.nbricks_dev);
 
-    auto load_quad = [&](long long j0, T xs[12]) {
-        if (j0 + 4 <= a.n) {
+    // a group = the G points of three 16-byte vectors (4 float32 / 2 float64 points)
+    constexpr int G = 16 / SZ, LG = SZ == 4 ? 2 : 1;
+    auto load_group = [&](long long j0, T xs[3 * G]) {
+        if (j0 + G <= a.n) {
             if constexpr (sizeof(T) == 4) {
                 const float4* src = reinterpret_cast<const float4*>(a.pts + 3 * j0);
 #pragma unroll
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
             } else {
                 const double2* src = reinterpret_cast<const double2*>(a.pts + 3 * j0);
 #pragma unroll
-                for (int v = 0; v < 6; ++v) {
+                for (int v = 0; v < 3; ++v) {
                     const double2 t = __ldg(src + v);
                     xs[2 * v] = t.x;
                     xs[2 * v + 1] = t.y;
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
             }
         } else {
 #pragma unroll
-            for (int e = 0; e < 12; ++e) xs[e] = j0 + e / 3 < a.n ? __ldg(a.pts + 3 * j0 + e) : T(0);
+            for (int e = 0; e < 3 * G; ++e) xs[e] = j0 + e / 3 < a.n ? __ldg(a.pts + 3 * j0 + e) : T(0);
         }
     };
 
@@ -489,12 +490,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 stage_cube<SP_MIRROR, E>(tile + k * VOL, a.grid.data[k], z0b, z1b, z2b, g0, g1, g2, tid);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
-        const long long q0 = p0 >> 2, q1 = (p1 + 3) >> 2;
-        // two quads in flight per thread, ping-ponged between two register sets (no copies);
+        const long long q0 = p0 >> LG, q1 = (p1 + G - 1) >> LG;
+        // two groups in flight per thread, ping-ponged between two register sets (no copies);
         // the first one is loaded while the tile lands
-        T xa[12], xb[12];
+        T xa[3 * G], xb[3 * G];
         long long q = q0 + tid;
-        if (q < q1) load_quad(q << 2, xa);
+        if (q < q1) load_group(q << LG, xa);
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
         const int lo0 = (c[0] >> 1) - 1, lo1 = (c[1] >> 1) - 1, lo2 = (c[2] >> 1) - 1;
@@ -506,20 +507,28 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const T blo0 = dom ? (T)c[0] : kF, blo1 = (T)c[1], blo2 = (T)c[2];  // dom false: no point passes
         const T bhi0 = (T)(c[0] + B), bhi1 = (T)(c[1] + B), bhi2 = (T)(c[2] + B);
 
-        auto process = [&](long long q, const T xs[12]) {
-            const long long j0 = q << 2;
-            T r[4];
+        auto process = [&](long long q, const T xs[3 * G]) {
+            const long long j0 = q << LG;
+            T r[G];
             auto in_brick = [&](int u) {  // non-short-circuit: one predicate chain
                 return (xs[3 * u] >= blo0) & (xs[3 * u] < bhi0) & (xs[3 * u + 1] >= blo1) & (xs[3 * u + 1] < bhi1) &
                        (xs[3 * u + 2] >= blo2) & (xs[3 * u + 2] < bhi2);
             };
-            if (in_brick(0) & in_brick(1) & in_brick(2) & in_brick(3)) {
+            bool all = true;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) r[u] = bcc_tet_tile_v2<E, T>(xs[3 * u], xs[3 * u + 1], xs[3 * u + 2], sbias, sbase);
+            for (int u = 0; u < G; ++u) all &= in_brick(u);
+            if (all) {
+#pragma unroll
+                for (int u = 0; u < G; ++u) r[u] = bcc_tet_tile_v2<E, T>(xs[3 * u], xs[3 * u + 1], xs[3 * u + 2], sbias, sbase);
             } else {
 #pragma unroll 1
-                for (int u = 0; u < 4; ++u) {  // rare: one call site each, registers selected
-                    auto pick = [&](int o) { return u == 0 ? xs[o] : u == 1 ? xs[3 + o] : u == 2 ? xs[6 + o] : xs[9 + o]; };
+                for (int u = 0; u < G; ++u) {  // rare: one call site each, registers selected
+                    auto pick = [&](int o) {
+                        T v = xs[o];
+#pragma unroll
+                        for (int w = 1; w < G; ++w) v = u == w ? xs[3 * w + o] : v;
+                        return v;
+                    };
                     const T x0 = pick(0), x1 = pick(1), x2 = pick(2);
                     T v;
                     if ((x0 >= blo0) & (x0 < bhi0) & (x1 >= blo1) & (x1 < bhi1) & (x2 >= blo2) & (x2 < bhi2))
@@ -530,22 +539,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
                         v = bcc_tet_global<double, T>(a, (double)x0 - 1.0, (double)x1 - 1.0, (double)x2 - 1.0);
                     else
                         v = T(NAN);
-                    r[0] = u == 0 ? v : r[0];
-                    r[1] = u == 1 ? v : r[1];
-                    r[2] = u == 2 ? v : r[2];
-                    r[3] = u == 3 ? v : r[3];
+#pragma unroll
+                    for (int w = 0; w < G; ++w) r[w] = u == w ? v : r[w];
                 }
             }
-            if (j0 >= p0 && j0 + 4 <= p1) {
+            if (j0 >= p0 && j0 + G <= p1) {
                 if constexpr (sizeof(T) == 4) {
                     *reinterpret_cast<float4*>(a.out + j0) = make_float4(r[0], r[1], r[2], r[3]);
                 } else {
-                    reinterpret_cast<double2*>(a.out + j0)[0] = make_double2(r[0], r[1]);
-                    reinterpret_cast<double2*>(a.out + j0)[1] = make_double2(r[2], r[3]);
+                    *reinterpret_cast<double2*>(a.out + j0) = make_double2(r[0], r[1]);
                 }
             } else {
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < G; ++u)
                     if (j0 + u >= p0 && j0 + u < p1) a.out[j0 + u] = r[u];
             }
         };
@@ -553,10 +559,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll 1
         for (; q < q1; q += 2 * kThreads) {
             const bool has_b = q + kThreads < q1;
-            if (has_b) load_quad((q + kThreads) << 2, xb);
+            if (has_b) load_group((q + kThreads) << LG, xb);
             process(q, xa);
             if (!has_b) break;
-            if (q + 2 * kThreads < q1) load_quad((q + 2 * kThreads) << 2, xa);
+            if (q + 2 * kThreads < q1) load_group((q + 2 * kThreads) << LG, xa);
             process(q + kThreads, xb);
         }
         __syncthreads();  // the tile is restaged for the next brick

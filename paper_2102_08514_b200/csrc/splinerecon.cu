@@ -797,24 +797,24 @@ int try_bricks_bcc_tet(const sp_plan* p, const sp::EvalArgs<T>& a, const int64_t
     if (log2b < 3 || log2b > 5) return 0;
     const long long* bs = reinterpret_cast<const long long*>(bstart);
     const int E = (1 << log2b) / 2 + 2;
-    // SP_BCC_TET_VARIANT (tuning): 0 = lean tile path, two quads in flight per thread
+    // SP_BCC_TET_VARIANT (tuning): 0 = lean tile path, two point groups in flight per thread
     // (bcc_tet_brick_kernel_v2, default); 3 = the round-2 kernel (register prefetch of the
     // next quad, per-point brick test); 1 = no prefetch, 4 CTAs/SM; 2 = prefetch +
     // double-buffered tile; 4 = the lean kernel at 4 CTAs/SM (fp32).  All give identical values.
     static const int variant = env_int("SP_BCC_TET_VARIANT", 0);
     const bool db = variant == 2;
     const size_t smem = (db ? 4 : 2) * (size_t)E * E * E * sizeof(T);  // two cosets (x2 double-buffered)
-    // float64: the round-2 kernel (two float64 quads in flight need 128 registers and spill:
-    // 102.6 vs 106.8 Gpts/s measured at C3)
-    constexpr bool lean = sizeof(T) == 4;
-    auto kern = log2b == 3   ? (lean ? sp::bcc_tet_brick_kernel_v2<T, 3> : sp::bcc_tet_brick_kernel<T, 3>)
-                : log2b == 4 ? (lean ? sp::bcc_tet_brick_kernel_v2<T, 4> : sp::bcc_tet_brick_kernel<T, 4>)
+    // the round-2 kernel: variant 3, or float64 with SP_BCC_TET_LEAN64=0 (the lean kernel's
+    // 2-point float64 groups: 106.7 -> 114.9 Gpts/s at C3)
+    static const bool lean64 = env_int("SP_BCC_TET_LEAN64", 1) != 0;
+    const bool old = variant == 3 || (sizeof(T) == 8 && !lean64);
+    auto kern = log2b == 3   ? (old ? sp::bcc_tet_brick_kernel<T, 3> : sp::bcc_tet_brick_kernel_v2<T, 3>)
+                : log2b == 4 ? (old ? sp::bcc_tet_brick_kernel<T, 4> : sp::bcc_tet_brick_kernel_v2<T, 4>)
                 : variant == 1 ? sp::bcc_tet_brick_kernel<T, 5, false, sizeof(T) == 4 ? 4 : 2>
                 : variant == 2 ? sp::bcc_tet_brick_kernel<T, 5, true, sizeof(T) == 4 ? 3 : 2, true>
-                : variant == 3 ? sp::bcc_tet_brick_kernel<T, 5>
                 : variant == 4 ? sp::bcc_tet_brick_kernel_v2<T, 5, sizeof(T) == 4 ? 4 : 3>
-                : lean       ? sp::bcc_tet_brick_kernel_v2<T, 5>
-                               : sp::bcc_tet_brick_kernel<T, 5>;
+                : old        ? sp::bcc_tet_brick_kernel<T, 5>
+                               : sp::bcc_tet_brick_kernel_v2<T, 5>;
     const int per_sm = sp::cached_occupancy(kern, smem);
     const int blocks = std::max(1, std::min(nbricks, p->num_sms * per_sm));
     kern<<<blocks, sp::kThreads, smem, st>>>(a, bs, nbricks);
