@@ -70,6 +70,8 @@ struct EvalArgs {
     const int* nbricks_dev;     // nullable: brick count in device memory (sync-free brick runs)
     int prefetch_pts;           // TMA brick kernel: bulk-prefetch each next brick's points into L2
     int plain_pts;              // brick kernels: plain-point loop (SP_PLAIN_PTS, default on)
+    int box_pad[3];             // single-coset plans: extra staged cells at the high end per axis
+                                // (bank-conflict-free tile pitches for scalar float64 rows)
 };
 
 // Checked build (build.py --checked -> libsplinerecon_checked.so, loaded with SP_CHECKED=1):
@@ -431,7 +433,7 @@ __device__ __forceinline__ void warp_geometry(const EvalArgs<T>& a, const int* r
         i = lane - 3 * k;
         const int d = a.fr.diag[i], l = a.fr.shift[k][i], dl = a.fr.dlog2[i];
         const long long b0 = (long long)floordiv_d(red[i] - l, d, dl) + a.fr.reach_lo[i] - a.margin;
-        const long long b1 = (long long)floordiv_d(red[3 + i] - l, d, dl) + a.fr.reach_hi[i] + a.margin;
+        const long long b1 = (long long)floordiv_d(red[3 + i] - l, d, dl) + a.fr.reach_hi[i] + a.margin + a.box_pad[i];
         e = min(b1 - b0 + 1, (long long)(1 << 20));
         geom.lo[k][i] = (int)b0;
         geom.ex[k][i] = (int)e;

@@ -838,6 +838,17 @@ int eval_bricks_typed(const sp_plan* p, const sp_grid_desc* g, const void* pts, 
     a.nbricks_dev = nbricks_dev;
     a.prefetch_pts = env_int("SP_PREFETCH_PTS", 1);
     a.plain_pts = env_int("SP_PLAIN_PTS", 1);
+    // float64 tensor-product tiles are read as scalar rows (LDS.64, 16 bank slots): widen the
+    // staged box so that Morton-adjacent cells fall in different bank slots (SP_F64_PAD=0: off)
+    if (sizeof(T) == 8 && p->kind == SP_KIND_TENSOR_BSPLINE && g->M == 1 && log2b >= 2 && log2b <= 4 &&
+        env_int("SP_F64_PAD", 1) != 0) {
+        const int B = 1 << log2b;
+        const int need_x = B + p->reach_hi[2] - p->reach_lo[2], need_y = B + p->reach_hi[1] - p->reach_lo[1];
+        int bx = need_x, by = need_y;
+        choose_box_pitch(need_x, need_y, B, 16, 1, bx, by);
+        a.box_pad[2] = bx - need_x;
+        a.box_pad[1] = by - need_y;
+    }
     if constexpr (sizeof(T) == 4) {
         const int t = try_bricks_tma(p, g, a, bstart, nbricks, log2b, st);
         if (t != 0) return t > 0 ? SP_OK : t;
